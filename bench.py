@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""Benchmark: permutation cost evaluations/s (U1 = one reference evaluate()).
+
+Workload (BASELINE.json target: ">= 100x the host CPU in permutation
+evaluations/sec on one B200 for N=1024 ring cost"): config C4 -- the
+1024-host synthetic hierarchical matrix (fixtures.py, fixed-point variant so
+every cost is bit-exact vs the reference), ring all-reduce cost model.  A step
+scores one batch of random orders that is resident in HBM (2 GiB of uint16
+orders per GPU, far larger than the 126 MB L2), with the per-order bijection
+check on, exactly as the reference's evaluate() validates every order.
+
+Arms
+  (default)          our CUDA path; one process per GPU under torchrun, each
+                     GPU scores its own batch (weak scaling, no collective in
+                     the data path), time = max over ranks of CUDA-event time.
+  --impl reference   the reference's own evaluate() (oracle/_ref, compiled from
+                     the unmodified sources) on all host threads, rank 0 only.
+
+Extra keys: roofline (dominant kernel), cpu_baseline, e2e (host buffers through
+the C ABI rw_evaluate_batch, H2D/D2H inside the timed region), clocks,
+gpu_launches, and `extras` (N=13 exhaustive time, C1 time-to-best-ring).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "permutation cost evals/sec (ring, N=1024, U1 = one reference evaluate())"
+UNIT = "evals/s"
+WORKLOAD = "C4: N=1024 ring all-reduce cost, synthetic 3-level hierarchical matrix (fixed-point q/16 us, S=2^27)"
+N = 1024
+BATCH = 1 << 21  # orders per GPU per step: 2M x 1024 x 2 B = 4 GiB of uint16 orders in HBM
+E2E_BATCH = 1 << 16
+CPU_SECONDS = 10.0
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference --
+def cpu_reference_rate(m: np.ndarray, seconds: float, threads: int):
+    """Reference evaluate() (oracle/_ref) on `threads` host threads; returns evals/s and the sample."""
+    from oracle.pyoracle import Port, Reference, make_spec, reference_available
+    spec = make_spec(0, N, float(2 ** 27), 2, 1, 0)
+    kind = "reference" if reference_available() else "port"
+    eng = Reference() if kind == "reference" else Port()
+    rng = np.random.default_rng(7)
+    pool = rng.permuted(np.tile(np.arange(N, dtype=np.int32), (max(64, min(65536, threads * 512)), 1)), axis=1)
+
+    def run(orders):
+        if kind == "reference":
+            eng.evaluate_batch(m, orders, spec, threads=threads)
+        else:
+            eng.evaluate_batch(m, orders, spec)
+
+    run(pool[: max(threads * 4, 16)])  # warm caches / threads
+    done = 0
+    t = time.perf_counter()
+    while True:
+        run(pool)
+        done += pool.shape[0]
+        dt = time.perf_counter() - t
+        if dt >= seconds:
+            break
+    return done / dt, {"kind": kind, "cores": threads if kind == "reference" else 1,
+                       "sample": f"{done} evaluations of random C4 orders (pool of {pool.shape[0]}), {dt:.1f} s"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import paper_2105_14088_b200 as rw  # fixture generator only (host code)
+    m = rw.fixtures.config_matrix("C4", "fixed")
+    threads = os.cpu_count() or 1
+    per_step = max(1.0, 20.0 / max(1, args.steps))
+    for _ in range(args.warmup):
+        cpu_reference_rate(m, min(per_step, 1.0), threads)
+    rates = []
+    t0 = time.perf_counter()
+    info = None
+    for _ in range(args.steps):
+        r, info = cpu_reference_rate(m, per_step, threads)
+        rates.append(r)
+    elapsed = time.perf_counter() - t0
+    value = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": N, "model": "ring", "threads": threads},
+            "cpu_baseline": dict(info, value=value, unit=UNIT),
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm ---
+def make_orders_device(torch, count: int, n: int, seed: int):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    out = torch.empty((count, n), dtype=torch.int16, device="cuda")
+    step = 1 << 15
+    for s in range(0, count, step):
+        e = min(count, s + step)
+        out[s:e] = torch.rand((e - s, n), device="cuda", generator=g).argsort(dim=1).to(torch.int16)
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2105_14088_b200 as rw
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    m = rw.fixtures.config_matrix("C4", "fixed")
+    prob = rw.Problem(m, device=local)
+    spec = rw.fixtures.ring_spec(N, rw.fixtures.SIZE_FIXED)
+    batch = args.batch
+    orders = make_orders_device(torch, batch, N, seed=1234 + rank)
+    costs = torch.empty(batch, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        prob.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    prob.sync_errors()
+
+    # parity spot check of this very batch against the reference costs (oracle port, 8 rows)
+    if rank == 0:
+        from oracle.pyoracle import Port, make_spec
+        rows = orders[:8].cpu().numpy().view(np.uint16).astype(np.int32)
+        want = Port().evaluate_batch(m, rows, make_spec(0, N, rw.fixtures.SIZE_FIXED))
+        assert np.array_equal(costs[:8].cpu().numpy(), want), "GPU costs differ from the oracle"
+
+    # ---- timed region: device-resident orders (value) ----
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    with ClockSampler(local) as clocks:
+        ev[0].record(stream)
+        for k in range(args.steps):
+            step()
+            ev[k + 1].record(stream)
+        barrier()
+    prob.sync_errors()
+    per_launch_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * batch * args.steps / (max_ms / 1000.0)
+
+    # ---- e2e: host int32 orders through rw_evaluate_batch (H2D + D2H inside) ----
+    e2e_batch = args.e2e_batch
+    host_orders = torch.empty((e2e_batch, N), dtype=torch.int32, pin_memory=True)
+    host_orders.copy_(orders[:e2e_batch].to(torch.int32).cpu())
+    host_np = host_orders.numpy()
+    host_costs_t = torch.empty(e2e_batch, dtype=torch.float64, pin_memory=True)
+    host_costs = host_costs_t.numpy()
+    import ctypes as C
+    from paper_2105_14088_b200 import _lib
+    cs = spec._c()
+
+    def e2e_step():
+        _lib.check(_lib.lib.rw_evaluate_batch(prob.handle, C.byref(cs), _lib.ptr(host_np, C.c_int32), e2e_batch,
+                                              _lib.ptr(host_costs, C.c_double), 0, None))
+
+    for _ in range(2):
+        e2e_step()
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    barrier()
+    e2e_dt = time.perf_counter() - t0
+    te = torch.tensor([e2e_dt], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * e2e_batch * e2e_steps / float(te.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    bytes_per_eval = 2 * N + N * 2 + 8  # order read + L*e lookups (u16) + cost write
+    launch_ms = statistics.mean(per_launch_ms)
+    achieved = bytes_per_eval * batch / (launch_ms / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("ring_eval_bytes_per_launch")
+    clock = clocks.summary()
+
+    cpu_value, cpu_info = (None, {"kind": "skipped", "cores": 0, "sample": "--no-cpu"})
+    if not args.no_cpu:
+        cpu_value, cpu_info = cpu_reference_rate(m, CPU_SECONDS, os.cpu_count() or 1)
+
+    extras = {}
+    if not args.no_extras:
+        extras = run_extras(rw, torch)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": N, "model": "ring", "orders_per_gpu_per_step": batch,
+                   "order_bytes_in_hbm": batch * N * 2, "l2_policy": "inputs larger than L2 (2 B x N x batch)",
+                   "validation": "bijection check on every order", "parallelism": f"dp{world} (independent batches)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_ring<u16,u16,global,validate>",
+                     "algorithmic_bytes_per_eval": bytes_per_eval,
+                     "lookups_per_s": N * batch / (launch_ms / 1000.0),
+                     "note": "random 2-byte gathers from an L2-resident 2 MiB matrix: one 32 B sector per lookup; "
+                             "the HBM fraction understates the L2/L1 sector load (see DESIGN.md)"},
+        "cpu_baseline": dict(cpu_info, value=cpu_value, unit=UNIT),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_batch * N * 4,
+                "d2h_bytes_per_step": e2e_batch * 8, "api": "rw_evaluate_batch (C ABI, pinned host int32 orders)"},
+        "clocks": clock,
+        "gpu_launches": args.steps,
+        "extras": extras,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_extras(rw, torch):
+    """Secondary north-star numbers (single GPU, small): exhaustive N=13 and C1 time-to-best-ring."""
+    out = {}
+    m13 = rw.fixtures.config_matrix("C2")
+    M13 = rw.CostMatrix.from_array(m13)
+    spec13 = rw.CollectiveSpec(rw.Algorithm.Ring, 13, 1.0)
+    rw.brute_force(M13, spec13, threshold=13)  # warm
+    t = time.perf_counter()
+    sol = rw.brute_force(M13, spec13, threshold=13)
+    out["exhaustive_n13"] = {"seconds": time.perf_counter() - t, "cost": sol.cost, "order": sol.order.perm,
+                             "evaluations": sol.evaluations, "reference_seconds_container": 180.8,
+                             "golden_cost": 338.0}
+    gpath = os.path.join(ROOT, "tests", "golden", "anneal.json")
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        ref = [r for r in g["results"] if r["config"] == "C1"]
+        target = min(r["cost"] for r in ref)
+        m = rw.fixtures.config_matrix("C1", "fixed")
+        prob = rw.Problem(m)
+        spec = rw.fixtures.ring_spec(64, rw.fixtures.SIZE_FIXED)
+        best = None
+        t = time.perf_counter()
+        for steps in (8, 32, 128, 256):
+            order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps))
+            best = (cost, steps, ev)
+            if cost <= target:
+                break
+        out["time_to_best_ring_c1"] = {"seconds": time.perf_counter() - t, "target_reference_min_seeds0_9": target,
+                                       "reached": best[0] <= target, "cost": best[0], "steps_per_level": best[1],
+                                       "evaluations": best[2],
+                                       "reference_seconds_container": statistics.median(r["seconds"] for r in ref)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--e2e-batch", type=int, default=E2E_BATCH)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,207 @@
+/*
+ * rankweave_c.h -- C ABI of the B200-native rank-reordering solver
+ * (librankweave_b200.so).  Plain pointers and sizes only; no C++ or torch
+ * types cross this boundary.
+ *
+ * The reference (arxiv/paper_2105_14088, "rankweave") exposes its hot path as
+ * C++ free functions in proj/include/rankweave/ headers and has no C ABI, FFI or
+ * Python binding (proj/python/CMakeLists.txt:1 is a placeholder).  Each entry
+ * point below names the reference interface it replaces; the C++ drop-in
+ * headers in include/rankweave/ are implemented on top of these calls, and
+ * the Python package paper_2105_14088_b200 binds them with ctypes
+ * (INTEGRATION.md shows the bindings).
+ *
+ * Conventions
+ *  - Every call returns rw_status.  On failure rw_last_error() returns the
+ *    message of the failing call on the calling thread.  RW_ERR_DOMAIN carries
+ *    the reference's domain_error text (types.hpp:12-27, exit code 3).
+ *  - All buffers are caller-owned.  The only library-owned object is the
+ *    opaque rw_problem: one cost matrix resident in device memory.
+ *  - Host-buffer entry points are synchronous.  *_device entry points take
+ *    device pointers and a cudaStream_t passed as void* and are asynchronous.
+ *  - Thread safety: distinct threads may call concurrently; every host-buffer
+ *    call runs on a per-thread stream of the problem's device.
+ */
+#ifndef RANKWEAVE_C_H
+#define RANKWEAVE_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RW_ABI_VERSION 1
+
+typedef enum rw_status {
+  RW_OK = 0,
+  RW_ERR_IO = 2,       /* rankweave::io_error      (types.hpp:21-24) */
+  RW_ERR_DOMAIN = 3,   /* rankweave::domain_error  (types.hpp:14-17) */
+  RW_ERR_CUDA = 5,     /* CUDA runtime failure (no device, OOM, fault) */
+  RW_ERR_NCCL = 6,     /* collective failure (multi-GPU helpers) */
+  RW_ERR_INTERNAL = 7
+} rw_status;
+
+/* rankweave::Algorithm / CostMode / HdPairing (types.hpp:29-31). */
+enum { RW_RING = 0, RW_HALVING_DOUBLING = 1, RW_DOUBLE_BINARY_TREE = 2, RW_BCUBE = 3 };
+enum { RW_LATENCY_ONLY = 0, RW_LATENCY_TIMES_SIZE = 1 };
+enum { RW_PAIRING_PAPER = 0, RW_PAIRING_XOR = 1 };
+/* rankweave::ScheduleSemantics (types.hpp:99-103). */
+enum { RW_SEQUENTIAL_HOPS = 0, RW_BULK_SYNCHRONOUS_ROUNDS = 1, RW_CRITICAL_PATH = 2 };
+/* rankweave::SolveMethod (solver.hpp:26). */
+enum { RW_METHOD_BRUTE_FORCE = 0, RW_METHOD_ANNEAL = 1, RW_METHOD_EXTERNAL = 2 };
+
+/* Device storage of the matrix (chosen at rw_problem_create). */
+enum {
+  RW_STORAGE_AUTO = 0, /* u16 fixed point if exact, else f32 if exact, else f64 */
+  RW_STORAGE_U16 = 1,  /* value = q * 2^-frac_bits, q < 65536 */
+  RW_STORAGE_F32 = 2,
+  RW_STORAGE_F64 = 3
+};
+
+/* rw_evaluate_batch* flags. */
+enum {
+  RW_EVAL_EXACT = 1u << 0,       /* reference-identical ring summation (sorted) */
+  RW_EVAL_NO_VALIDATE = 1u << 1  /* skip the per-order bijection check */
+};
+
+/* rankweave::CollectiveSpec (types.hpp:73-80). */
+typedef struct rw_spec {
+  int32_t algorithm;
+  int32_t n;
+  double size_bytes;
+  int32_t bcube_b;
+  int32_t cost_mode;
+  int32_t hd_pairing;
+} rw_spec;
+
+/* rankweave::SolverConfig (solver.hpp:14-22); budget in seconds. */
+typedef struct rw_solver_config {
+  double budget_s;
+  uint64_t seed;
+  double initial_temperature;
+  double cooling;
+  int32_t steps_per_temperature;
+  int32_t restarts;
+  int32_t brute_force_threshold;
+  int32_t reserved;
+} rw_solver_config;
+
+/* GPU extension of the search configuration (not in the reference). */
+typedef struct rw_gpu_config {
+  int32_t chains;       /* SA chains on this call; <= 0: one per restart */
+  int32_t chain_begin;  /* global id of the first chain (multi-GPU sharding) */
+  int32_t chain_total;  /* total chains across all ranks (<= 0: chains) */
+  int32_t polish;       /* 1: 2-opt/swap best-improvement polish of the winner */
+  int64_t max_proposals;/* total proposal budget for this call (0: schedule) */
+} rw_gpu_config;
+
+typedef struct rw_problem rw_problem;
+
+typedef struct rw_problem_info {
+  int32_t n;
+  int32_t device;
+  int32_t storage;      /* RW_STORAGE_U16 / F32 / F64 */
+  int32_t frac_bits;    /* u16 only */
+  int32_t symmetric;
+  int32_t zero_diagonal;
+  int64_t device_bytes; /* matrix bytes resident on the device */
+  double max_value;
+} rw_problem_info;
+
+/* Per-call search report (optional out-parameter of rw_anneal). */
+typedef struct rw_search_report {
+  int64_t winner_chain;   /* global id of the chain that produced the result */
+  int64_t chains;         /* chains run by this call */
+  int64_t proposals;      /* Metropolis proposals (sequential-equivalent) */
+  int32_t levels;         /* temperature levels in the schedule */
+  int32_t levels_run;     /* levels completed before the budget expired */
+  double initial_temperature;
+  double seconds;         /* wall time of the call */
+} rw_search_report;
+
+/* Per-call evaluation report (optional out-parameter). */
+typedef struct rw_eval_report {
+  int32_t bit_exact;    /* 1: every cost equals the reference's bits */
+  int32_t kernel;       /* internal kernel id */
+  float kernel_ms;      /* device time of the scoring kernels */
+  int64_t lookups;      /* matrix lookups performed */
+} rw_eval_report;
+
+/* ---- library ---------------------------------------------------------- */
+const char* rw_last_error(void);
+int32_t rw_abi_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int32_t rw_device_count(void);
+
+/* validate(CollectiveSpec) (types.cpp:143-163): RW_ERR_DOMAIN with the
+ * reference's message when the spec is invalid. */
+rw_status rw_validate_spec(const rw_spec* spec);
+
+/* ---- problem: the device-resident CostMatrix (types.hpp:42-53) --------- */
+/* Validates like the reference evaluate path (square, n >= 1); the matrix
+ * itself is NOT validated (evaluate() does not call validate(CostMatrix)). */
+rw_status rw_problem_create(const double* rtt_us, int32_t n, int32_t storage_hint, int32_t device,
+                            rw_problem** out);
+rw_status rw_problem_destroy(rw_problem* p);
+rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out);
+
+/* ---- cost model (cost_model.hpp:28-36) --------------------------------- */
+/* evaluate(m, order, spec): reference-identical bits for every matrix. */
+rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* perm, double* cost);
+/* B orders (row-major B x n int32, host) -> B costs (host). */
+rw_status rw_evaluate_batch(const rw_problem* p, const rw_spec* spec, const int32_t* perms, int64_t batch,
+                            double* costs, uint32_t flags, rw_eval_report* report);
+/* Same with device buffers; perm_bytes is 2 (uint16) or 4 (int32). Async on
+ * `stream`.  Validation failures are reported by the next rw_sync_errors(). */
+rw_status rw_evaluate_batch_device(const rw_problem* p, const rw_spec* spec, const void* d_perms,
+                                   int32_t perm_bytes, int64_t batch, double* d_costs, void* stream,
+                                   uint32_t flags);
+/* Collect asynchronous validation errors raised by *_device calls on p. */
+rw_status rw_sync_errors(const rw_problem* p, void* stream);
+/* schedule_cost(expand_schedule(spec), m, order, mode) (cost_model.hpp:31-36):
+ * transfers are flattened round by round; round_offsets has nrounds+1 entries. */
+rw_status rw_schedule_cost(const rw_problem* p, int32_t semantics, int32_t nrounds, const int32_t* round_offsets,
+                           const int32_t* src, const int32_t* dst, const double* bytes, const int32_t* parent,
+                           int32_t cost_mode, const int32_t* perm, double* cost);
+
+/* ---- exhaustive search (solver.hpp:37-42, solver.cpp:73-105) ----------- */
+rw_status rw_brute_force(const rw_problem* p, const rw_spec* spec, int32_t threshold, int32_t* perm_out,
+                         double* cost_out, uint64_t* evals_out);
+/* Size of the enumerated space ((n-1)! for ring, n! otherwise). */
+rw_status rw_brute_force_space(const rw_spec* spec, uint64_t* count_out);
+/* One shard [first, first+count) of the lexicographic space: (min cost, min
+ * lex index).  Used by the multi-GPU driver; rw_unrank maps an index back. */
+rw_status rw_brute_force_range(const rw_problem* p, const rw_spec* spec, uint64_t first, uint64_t count,
+                               double* cost_out, uint64_t* index_out);
+rw_status rw_unrank(const rw_spec* spec, uint64_t index, int32_t* perm_out);
+
+/* ---- heuristic search (solver.hpp:44-53, solver.cpp:141-202) ----------- */
+rw_status rw_anneal(const rw_problem* p, const rw_spec* spec, const rw_solver_config* cfg,
+                    const rw_gpu_config* gpu, int32_t* perm_out, double* cost_out, uint64_t* evals_out,
+                    rw_search_report* report);
+/* Batched best-improvement local search (2-opt + swap + or-opt for ring):
+ * orders are improved in place; costs_out receives reference-exact costs. */
+rw_status rw_local_search(const rw_problem* p, const rw_spec* spec, int32_t* perms_inout, int64_t batch,
+                          int32_t max_rounds, double* costs_out, uint64_t* evals_out);
+
+/* ---- statistics (stats.hpp:18-28) -------------------------------------- */
+/* sample_orders: deterministic per seed (Philox, not libstdc++ shuffle). */
+rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* perms_out);
+rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed,
+                          double* costs_out);
+
+/* ---- synthetic inputs (topology.hpp:40, out of scope for kernels) ------ */
+/* generate_matrix(TopologySpec): writes n*n doubles; returns n in *n_out. */
+rw_status rw_generate_matrix(int32_t nlevels, const int32_t* fanout, const double* latency_us,
+                             const double* bandwidth, const double* oversub, double jitter, uint64_t seed,
+                             double* out, int64_t out_capacity, int32_t* n_out);
+/* Fixture relabeling: rl = std::shuffle(iota(n), mt19937_64(seed)),
+ * m'[i][j] = m[rl[i]][rl[j]] (in place). */
+rw_status rw_relabel_matrix(double* m, int32_t n, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RANKWEAVE_C_H */

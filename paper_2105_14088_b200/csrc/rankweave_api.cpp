@@ -1,0 +1,774 @@
+// rankweave_api.cpp -- the C++ drop-in layer (include/rankweave/rankweave.hpp)
+// over the C ABI (include/rankweave_c.h).
+//
+// Host-side here: argument validation with the reference's exception types and
+// wording (types.cpp, cost_model.cpp:13-19, solver.cpp:50-55), enum/string
+// conversion, schedule *structure* (expand_schedule), the SMT-LIB text side
+// file and neighbor() (its contract is a caller-supplied std::mt19937_64).
+// Every cost is computed on the GPU.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <list>
+#include <mutex>
+#include <numeric>
+#include <sstream>
+
+#include "rankweave/rankweave.hpp"
+#include "rankweave_c.h"
+
+namespace rankweave {
+
+namespace {
+
+[[noreturn]] void raise(rw_status st) {
+  const std::string msg = rw_last_error();
+  if (st == RW_ERR_DOMAIN) throw domain_error(msg);
+  if (st == RW_ERR_IO) throw io_error(msg);
+  throw std::runtime_error("rankweave-b200: " + msg);
+}
+
+inline void check(rw_status st) {
+  if (st != RW_OK) raise(st);
+}
+
+GpuOptions& options_ref() {
+  static GpuOptions o;
+  return o;
+}
+std::mutex& options_mu() {
+  static std::mutex m;
+  return m;
+}
+
+// Device problems cached by matrix content (exact byte comparison against a
+// shadow copy), so repeated calls on one CostMatrix upload it once.
+class ProblemCache {
+ public:
+  rw_problem* get(const CostMatrix& m, int device) {
+    std::lock_guard<std::mutex> lock(mu_);
+    const std::size_t bytes = m.rtt_us.size() * sizeof(double);
+    for (auto it = entries_.begin(); it != entries_.end(); ++it) {
+      if (it->n == m.n() && it->device == device && it->shadow.size() == m.rtt_us.size() &&
+          std::memcmp(it->shadow.data(), m.rtt_us.data(), bytes) == 0) {
+        entries_.splice(entries_.begin(), entries_, it);
+        return entries_.front().problem;
+      }
+    }
+    rw_problem* p = nullptr;
+    check(rw_problem_create(m.rtt_us.data(), m.n(), RW_STORAGE_AUTO, device, &p));
+    entries_.push_front(Entry{m.n(), device, m.rtt_us, p});
+    total_ += bytes;
+    while (entries_.size() > 16 || (total_ > (std::size_t(1) << 31) && entries_.size() > 1)) {
+      total_ -= entries_.back().shadow.size() * sizeof(double);
+      rw_problem_destroy(entries_.back().problem);
+      entries_.pop_back();
+    }
+    return p;
+  }
+
+ private:
+  struct Entry {
+    int n;
+    int device;
+    std::vector<double> shadow;
+    rw_problem* problem;
+  };
+  std::mutex mu_;
+  std::list<Entry> entries_;
+  std::size_t total_ = 0;
+};
+
+ProblemCache& cache() {
+  static ProblemCache* c = new ProblemCache();  // never destroyed: CUDA may be gone at exit
+  return *c;
+}
+
+rw_problem* device_problem(const CostMatrix& m) {
+  if (m.rtt_us.size() != static_cast<std::size_t>(m.n()) * static_cast<std::size_t>(m.n()))
+    throw domain_error("cost matrix storage is not n*n");
+  return cache().get(m, gpu_options().device);
+}
+
+rw_spec to_c(const CollectiveSpec& s) {
+  rw_spec c{};
+  c.algorithm = static_cast<int32_t>(s.algorithm);
+  c.n = s.n;
+  c.size_bytes = s.size_bytes;
+  c.bcube_b = s.bcube_b;
+  c.cost_mode = static_cast<int32_t>(s.cost_mode);
+  c.hd_pairing = static_cast<int32_t>(s.hd_pairing);
+  return c;
+}
+
+// check_inputs (cost_model.cpp:13-19)
+void check_inputs(const CostMatrix& m, const RankOrder& order, const CollectiveSpec& spec) {
+  validate(spec);
+  if (m.n() != spec.n)
+    throw domain_error("matrix is " + std::to_string(m.n()) + "x" + std::to_string(m.n()) + " but spec has N=" +
+                       std::to_string(spec.n));
+  validate(order, spec.n);
+}
+
+double gpu_evaluate(const CostMatrix& m, const RankOrder& order, const CollectiveSpec& spec) {
+  const rw_spec cs = to_c(spec);
+  double cost = 0.0;
+  check(rw_evaluate(device_problem(m), &cs, order.perm.data(), &cost));
+  return cost;
+}
+
+double model_cost(const CostMatrix& m, const RankOrder& order, const CollectiveSpec& spec, Algorithm want,
+                  const char* name) {
+  check_inputs(m, order, spec);
+  if (spec.algorithm != want) throw domain_error(std::string(name) + ": spec is not " + to_string(want));
+  return gpu_evaluate(m, order, spec);
+}
+
+std::string trim_real(double v) {
+  // SMT-LIB reals have no exponent form: fixed notation, trailing zeros trimmed.
+  char buf[512];
+  std::snprintf(buf, sizeof(buf), "%.15f", v);
+  std::string s(buf);
+  const std::size_t dot = s.find('.');
+  if (dot == std::string::npos) return s + ".0";
+  std::size_t last = s.find_last_not_of('0');
+  if (last == dot) ++last;
+  s.erase(last + 1);
+  return s;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ conversions --
+const char* to_string(Algorithm a) {
+  switch (a) {
+    case Algorithm::Ring: return "ring";
+    case Algorithm::HalvingDoubling: return "hd";
+    case Algorithm::DoubleBinaryTree: return "dbt";
+    case Algorithm::BCube: return "bcube";
+  }
+  return "?";
+}
+const char* to_string(CostMode m) { return m == CostMode::LatencyOnly ? "latency" : "latency-size"; }
+const char* to_string(HdPairing p) { return p == HdPairing::PaperFormula ? "paper" : "xor"; }
+const char* to_string(SolveMethod m) {
+  switch (m) {
+    case SolveMethod::BruteForce: return "BruteForce";
+    case SolveMethod::Anneal: return "Anneal";
+    case SolveMethod::External: return "External";
+  }
+  return "?";
+}
+
+Algorithm algorithm_from_string(const std::string& s) {
+  static const std::pair<const char*, Algorithm> table[] = {{"ring", Algorithm::Ring},
+                                                            {"hd", Algorithm::HalvingDoubling},
+                                                            {"dbt", Algorithm::DoubleBinaryTree},
+                                                            {"bcube", Algorithm::BCube}};
+  for (const auto& [name, value] : table)
+    if (s == name) return value;
+  throw domain_error("unknown algorithm '" + s + "' (expected ring|hd|dbt|bcube)");
+}
+CostMode cost_mode_from_string(const std::string& s) {
+  if (s == "latency") return CostMode::LatencyOnly;
+  if (s == "latency-size") return CostMode::LatencyTimesSize;
+  throw domain_error("unknown cost mode '" + s + "' (expected latency|latency-size)");
+}
+HdPairing hd_pairing_from_string(const std::string& s) {
+  if (s == "paper") return HdPairing::PaperFormula;
+  if (s == "xor") return HdPairing::XorPairing;
+  throw domain_error("unknown pairing '" + s + "' (expected paper|xor)");
+}
+SolveMethod solve_method_from_string(const std::string& s) {
+  for (SolveMethod m : {SolveMethod::BruteForce, SolveMethod::Anneal, SolveMethod::External})
+    if (s == to_string(m)) return m;
+  throw domain_error("unknown solve method '" + s + "'");
+}
+
+// ----------------------------------------------------------- value types --
+CostMatrix::CostMatrix(std::vector<std::string> host_ids, std::vector<std::vector<double>> rows_in)
+    : hosts(std::move(host_ids)) {
+  const std::size_t n = hosts.size();
+  if (rows_in.size() != n)
+    throw domain_error("matrix has " + std::to_string(rows_in.size()) + " rows for " + std::to_string(n) + " hosts");
+  rtt_us.reserve(n * n);
+  for (const auto& r : rows_in) {
+    if (r.size() != n) throw domain_error("matrix is not square");
+    rtt_us.insert(rtt_us.end(), r.begin(), r.end());
+  }
+}
+
+std::vector<std::vector<double>> CostMatrix::rows() const {
+  const std::size_t n = hosts.size();
+  std::vector<std::vector<double>> out(n);
+  for (std::size_t i = 0; i < n; ++i) out[i].assign(rtt_us.begin() + i * n, rtt_us.begin() + (i + 1) * n);
+  return out;
+}
+
+RankOrder RankOrder::identity(int n) {
+  RankOrder o;
+  o.perm.resize(static_cast<std::size_t>(n));
+  std::iota(o.perm.begin(), o.perm.end(), 0);
+  return o;
+}
+
+void validate(const CostMatrix& m) {
+  const std::size_t n = m.hosts.size();
+  if (n == 0) throw domain_error("cost matrix is empty");
+  if (m.rtt_us.size() != n * n) throw domain_error("cost matrix storage is not n*n");
+  for (int i = 0; i < m.n(); ++i)
+    for (int j = 0; j < m.n(); ++j) {
+      const double v = m.at(i, j);
+      if (!std::isfinite(v) || v < 0.0)
+        throw domain_error("rtt[" + std::to_string(i) + "][" + std::to_string(j) +
+                           "] is not a finite nonnegative value");
+      if (i == j && v != 0.0)
+        throw domain_error("rtt[" + std::to_string(i) + "][" + std::to_string(i) + "] must be 0");
+    }
+}
+
+bool is_symmetric(const CostMatrix& m) {
+  const int n = m.n();
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j)
+      if (m.at(i, j) != m.at(j, i)) return false;
+  return true;
+}
+
+void validate(const RankOrder& order, int n) {
+  if (order.size() != n)
+    throw domain_error("rank order has " + std::to_string(order.size()) + " entries, expected " + std::to_string(n));
+  std::vector<unsigned char> seen(static_cast<std::size_t>(n), 0);
+  for (int v : order.perm) {
+    if (v < 0 || v >= n || seen[static_cast<std::size_t>(v)])
+      throw domain_error("rank order is not a permutation of [0, " + std::to_string(n) + ")");
+    seen[static_cast<std::size_t>(v)] = 1;
+  }
+}
+
+RankOrder rotated(const RankOrder& order, int k) {
+  const int n = order.size();
+  RankOrder out;
+  out.perm.resize(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) out.perm[static_cast<std::size_t>(i)] = order.perm[static_cast<std::size_t>(alias_rank(i + k, n))];
+  return out;
+}
+
+RankOrder inverse(const RankOrder& order) {
+  RankOrder out;
+  out.perm.resize(order.perm.size());
+  for (int i = 0; i < order.size(); ++i) out.perm[static_cast<std::size_t>(order.perm[static_cast<std::size_t>(i)])] = i;
+  return out;
+}
+
+bool is_power_of(long long n, long long base) {
+  if (base < 2 || n < 1) return false;
+  for (; n % base == 0; n /= base) {
+  }
+  return n == 1;
+}
+
+int ilog(long long n, long long base) {
+  if (!is_power_of(n, base)) throw domain_error("ilog: n is not a power of base");
+  int k = 0;
+  for (; n > 1; n /= base) ++k;
+  return k;
+}
+
+void validate(const CollectiveSpec& spec) {
+  // The C ABI owns the single copy of the rule set (types.cpp:143-163 wording).
+  const rw_spec cs = to_c(spec);
+  check(rw_validate_spec(&cs));
+}
+
+double total_wire_bytes(const Schedule& s) {
+  double total = 0.0;
+  for (const auto& r : s.rounds)
+    for (const auto& t : r)
+      if (t.src != t.dst) total += t.bytes;
+  return total;
+}
+
+// ------------------------------------------------------------- cost model --
+double round_bytes(double size_bytes, int base, int round) {
+  double divisor = 1.0;
+  for (int k = 0; k <= round; ++k) divisor *= static_cast<double>(base);
+  return size_bytes / divisor;
+}
+
+double transfer_cost(const CostMatrix& m, int i, int j, double bytes, CostMode mode) {
+  const int n = m.n();
+  const double rtt = m.at(alias_rank(i, n), alias_rank(j, n));
+  return mode == CostMode::LatencyOnly ? rtt : rtt * bytes;
+}
+
+double ring_cost(const CostMatrix& m, const RankOrder& o, const CollectiveSpec& s) {
+  return model_cost(m, o, s, Algorithm::Ring, "ring_cost");
+}
+double halving_doubling_cost(const CostMatrix& m, const RankOrder& o, const CollectiveSpec& s) {
+  return model_cost(m, o, s, Algorithm::HalvingDoubling, "halving_doubling_cost");
+}
+double double_binary_tree_cost(const CostMatrix& m, const RankOrder& o, const CollectiveSpec& s) {
+  return model_cost(m, o, s, Algorithm::DoubleBinaryTree, "double_binary_tree_cost");
+}
+double bcube_cost(const CostMatrix& m, const RankOrder& o, const CollectiveSpec& s) {
+  return model_cost(m, o, s, Algorithm::BCube, "bcube_cost");
+}
+
+double evaluate(const CostMatrix& m, const RankOrder& order, const CollectiveSpec& spec) {
+  check_inputs(m, order, spec);
+  return gpu_evaluate(m, order, spec);
+}
+
+std::vector<double> evaluate_batch(const CostMatrix& m, const std::vector<RankOrder>& orders,
+                                   const CollectiveSpec& spec) {
+  validate(spec);
+  if (m.n() != spec.n)
+    throw domain_error("matrix is " + std::to_string(m.n()) + "x" + std::to_string(m.n()) + " but spec has N=" +
+                       std::to_string(spec.n));
+  std::vector<int32_t> flat;
+  flat.reserve(orders.size() * static_cast<std::size_t>(spec.n));
+  for (const auto& o : orders) {
+    if (o.size() != spec.n)
+      throw domain_error("rank order has " + std::to_string(o.size()) + " entries, expected " + std::to_string(spec.n));
+    flat.insert(flat.end(), o.perm.begin(), o.perm.end());
+  }
+  std::vector<double> costs(orders.size());
+  const rw_spec cs = to_c(spec);
+  check(rw_evaluate_batch(device_problem(m), &cs, flat.data(), static_cast<int64_t>(orders.size()), costs.data(),
+                          gpu_options().exact_batch ? static_cast<uint32_t>(RW_EVAL_EXACT) : 0u, nullptr));
+  return costs;
+}
+
+// Schedule structure (matrix independent); semantics per cost_model.cpp:150-236.
+Schedule expand_schedule(const CollectiveSpec& spec) {
+  validate(spec);
+  const int n = spec.n;
+  Schedule s;
+  s.algorithm = spec.algorithm;
+  s.node_count = n;
+  if (n == 1) {
+    s.semantics = ScheduleSemantics::SequentialHops;
+    return s;
+  }
+  switch (spec.algorithm) {
+    case Algorithm::Ring:
+      s.semantics = ScheduleSemantics::SequentialHops;
+      for (int i = 0; i < n; ++i) s.rounds.push_back({Transfer{i, alias_rank(i - 1, n), spec.size_bytes, -1}});
+      break;
+    case Algorithm::HalvingDoubling:
+    case Algorithm::BCube: {
+      s.semantics = ScheduleSemantics::BulkSynchronousRounds;
+      const bool hd = spec.algorithm == Algorithm::HalvingDoubling;
+      const int base = hd ? 2 : spec.bcube_b;
+      const int rounds = ilog(n, base);
+      long long stride = 1;
+      for (int r = 0; r < rounds; ++r, stride *= base) {
+        const double bytes = round_bytes(spec.size_bytes, base, r);
+        std::vector<Transfer> round;
+        if (hd && spec.hd_pairing == HdPairing::XorPairing) {
+          for (int j = 0; j < n; ++j) round.push_back(Transfer{j, j ^ static_cast<int>(stride), bytes, -1});
+        } else if (hd) {
+          for (int j = 0; j < n / 2; ++j)
+            round.push_back(Transfer{j, alias_rank(j + static_cast<int>(stride), n), bytes, -1});
+        } else {
+          for (int j = 0; j < n / base; ++j)
+            for (int k = 1; k < base; ++k)
+              round.push_back(Transfer{j, static_cast<int>((j + k * stride) % n), bytes, -1});
+        }
+        s.rounds.push_back(std::move(round));
+      }
+      break;
+    }
+    case Algorithm::DoubleBinaryTree: {
+      s.semantics = ScheduleSemantics::CriticalPath;
+      const double half = spec.size_bytes / 2.0;
+      // depth-first emission: an edge's children are the two edges of its
+      // sub-interval one depth below (the reference's recursion order)
+      std::function<void(int, int, int, int, int)> walk = [&](int i, int j, int shift, int depth, int parent) {
+        if (i >= j) return;
+        if (static_cast<int>(s.rounds.size()) <= depth) s.rounds.resize(static_cast<std::size_t>(depth) + 1);
+        const int mid = (i + j) / 2;
+        auto& level = s.rounds[static_cast<std::size_t>(depth)];
+        const int li = static_cast<int>(level.size());
+        level.push_back(Transfer{alias_rank(mid + shift, n), alias_rank((3 * i + j) / 2 - 1 + shift, n), half, parent});
+        walk(i, mid - 1, shift, depth + 1, li);
+        auto& level2 = s.rounds[static_cast<std::size_t>(depth)];
+        const int ri = static_cast<int>(level2.size());
+        level2.push_back(Transfer{alias_rank(mid + shift, n), alias_rank((i + 3 * j) / 2 + 1 + shift, n), half, parent});
+        walk(mid + 1, j, shift, depth + 1, ri);
+      };
+      walk(0, n - 1, 0, 0, -1);
+      walk(0, n - 1, -1, 0, -1);
+      break;
+    }
+  }
+  return s;
+}
+
+double schedule_cost(const Schedule& s, const CostMatrix& m, const RankOrder& order, CostMode mode) {
+  if (m.n() != s.node_count) throw domain_error("schedule node count does not match matrix dimension");
+  validate(order, s.node_count);
+  std::vector<int32_t> offs{0}, src, dst, parent;
+  std::vector<double> bytes;
+  for (const auto& r : s.rounds) {
+    for (const auto& t : r) {
+      src.push_back(t.src);
+      dst.push_back(t.dst);
+      parent.push_back(t.parent);
+      bytes.push_back(t.bytes);
+    }
+    offs.push_back(static_cast<int32_t>(src.size()));
+  }
+  double cost = 0.0;
+  check(rw_schedule_cost(device_problem(m), static_cast<int32_t>(s.semantics), static_cast<int32_t>(s.rounds.size()),
+                         offs.data(), src.data(), dst.data(), bytes.data(), parent.data(), static_cast<int32_t>(mode),
+                         order.perm.data(), &cost));
+  return cost;
+}
+
+// ------------------------------------------------------------------ solver --
+void validate(const SolverConfig& cfg) {
+  if (!(cfg.budget.count() > 0.0)) throw domain_error("solver budget must be > 0");
+  if (!(cfg.cooling > 0.0 && cfg.cooling < 1.0)) throw domain_error("cooling factor must be in (0, 1)");
+  if (cfg.restarts < 1) throw domain_error("restarts must be >= 1");
+  if (cfg.brute_force_threshold < 2) throw domain_error("brute-force threshold must be >= 2");
+}
+
+Solution brute_force(const CostMatrix& m, const CollectiveSpec& spec, int threshold) {
+  validate(spec);
+  if (spec.n > threshold)
+    throw domain_error("N=" + std::to_string(spec.n) + " exceeds the brute-force threshold " +
+                       std::to_string(threshold) + "; use anneal");
+  if (m.n() != spec.n)
+    throw domain_error("matrix is " + std::to_string(m.n()) + "x" + std::to_string(m.n()) + " but spec has N=" +
+                       std::to_string(spec.n));
+  const rw_spec cs = to_c(spec);
+  Solution sol;
+  sol.method = SolveMethod::BruteForce;
+  sol.order.perm.resize(static_cast<std::size_t>(spec.n));
+  uint64_t evals = 0;
+  check(rw_brute_force(device_problem(m), &cs, threshold, sol.order.perm.data(), &sol.cost, &evals));
+  sol.evaluations = evals;
+  return sol;
+}
+
+// One random mutation (solver.hpp:44-47): swap two positions, reverse a
+// sub-array, or shuffle a short window -- each with probability 1/3.
+RankOrder neighbor(const RankOrder& order, std::mt19937_64& rng) {
+  const int n = order.size();
+  if (n < 2) return order;
+  RankOrder out = order;
+  auto& v = out.perm;
+  auto uniform = [&rng](int lo, int hi) { return std::uniform_int_distribution<int>(lo, hi)(rng); };
+  const int kind = uniform(0, 2);
+  if (kind == 2) {
+    const int cap = std::min(n, std::max(3, n / 8));
+    const int len = uniform(2, std::max(2, cap));
+    const int first = uniform(0, n - len);
+    std::shuffle(v.begin() + first, v.begin() + first + len, rng);
+    return out;
+  }
+  int a = uniform(0, n - 1);
+  int b = uniform(0, n - 2);
+  b += (b >= a) ? 1 : 0;
+  if (kind == 0) {
+    std::swap(v[static_cast<std::size_t>(a)], v[static_cast<std::size_t>(b)]);
+  } else {
+    if (a > b) std::swap(a, b);
+    std::reverse(v.begin() + a, v.begin() + b + 1);
+  }
+  return out;
+}
+
+Solution anneal(const CostMatrix& m, const CollectiveSpec& spec, const SolverConfig& cfg) {
+  validate(spec);
+  validate(cfg);
+  if (m.n() != spec.n) throw domain_error("matrix dimension does not match spec.n");
+  const rw_spec cs = to_c(spec);
+  rw_solver_config c{};
+  c.budget_s = cfg.budget.count();
+  c.seed = cfg.seed;
+  c.initial_temperature = cfg.initial_temperature;
+  c.cooling = cfg.cooling;
+  c.steps_per_temperature = cfg.steps_per_temperature;
+  c.restarts = cfg.restarts;
+  c.brute_force_threshold = cfg.brute_force_threshold;
+  rw_gpu_config g{};
+  g.chains = gpu_options().chains;
+  Solution sol;
+  sol.method = SolveMethod::Anneal;
+  sol.order.perm.resize(static_cast<std::size_t>(spec.n));
+  uint64_t evals = 0;
+  check(rw_anneal(device_problem(m), &cs, &c, &g, sol.order.perm.data(), &sol.cost, &evals, nullptr));
+  sol.evaluations = evals;
+  return sol;
+}
+
+// Routing and stage-2 side files as in solver.cpp:204-261.
+Solution two_stage_solve(const CostMatrix& m, const CollectiveSpec& spec, const SolverConfig& cfg,
+                         const TwoStageOptions& opts) {
+  validate(spec);
+  validate(cfg);
+  auto log = [&](const std::string& msg) {
+    if (opts.log) opts.log(msg);
+  };
+  Solution stage1;
+  if (spec.n <= 2) {
+    stage1.order = RankOrder::identity(spec.n);
+    stage1.cost = evaluate(m, stage1.order, spec);
+    stage1.method = SolveMethod::BruteForce;
+    stage1.evaluations = 1;
+  } else if (spec.n <= cfg.brute_force_threshold) {
+    stage1 = brute_force(m, spec, cfg.brute_force_threshold);
+    log("stage 1: brute force over " + std::to_string(stage1.evaluations) + " orders, cost " +
+        std::to_string(stage1.cost));
+  } else {
+    stage1 = anneal(m, spec, cfg);
+    log("stage 1: anneal, " + std::to_string(stage1.evaluations) + " evaluations, cost " +
+        std::to_string(stage1.cost));
+  }
+  if (!opts.emit_smt_path.empty()) {
+    const std::string text = emit_smtlib(m, spec, stage1.cost);
+    std::ofstream out(opts.emit_smt_path);
+    if (!out) throw io_error("cannot write SMT file '" + opts.emit_smt_path + "'");
+    out << text;
+    log("stage 2: SMT-LIB encoding with bound cost < " + std::to_string(stage1.cost) + " written to " +
+        opts.emit_smt_path);
+  }
+  if (opts.external_model_path.empty()) return stage1;
+  std::ifstream in(opts.external_model_path);
+  if (!in) {
+    log("warning: cannot read external model '" + opts.external_model_path + "'; keeping the stage-1 solution");
+    return stage1;
+  }
+  std::stringstream text;
+  text << in.rdbuf();
+  try {
+    const RankOrder ext = parse_model_file(text.str(), spec.n);
+    const double c = evaluate(m, ext, spec);
+    if (c < stage1.cost) {
+      log("external model improves cost " + std::to_string(stage1.cost) + " -> " + std::to_string(c));
+      return Solution{ext, c, SolveMethod::External, stage1.evaluations + 1};
+    }
+    log("warning: external model does not improve on the stage-1 cost; keeping stage 1");
+  } catch (const domain_error& e) {
+    log(std::string("warning: invalid external model: ") + e.what() + "; keeping the stage-1 solution");
+  }
+  return stage1;
+}
+
+// ------------------------------------------------------------------- stats --
+namespace {
+std::vector<double> mid_ranks(const std::vector<double>& xs) {
+  std::vector<std::size_t> idx(xs.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a, std::size_t b) { return xs[a] < xs[b]; });
+  std::vector<double> rank(xs.size());
+  for (std::size_t i = 0; i < idx.size();) {
+    std::size_t j = i;
+    while (j + 1 < idx.size() && xs[idx[j + 1]] == xs[idx[i]]) ++j;
+    const double r = 0.5 * static_cast<double>(i + j) + 1.0;
+    for (std::size_t k = i; k <= j; ++k) rank[idx[k]] = r;
+    i = j + 1;
+  }
+  return rank;
+}
+}  // namespace
+
+double spearman(const std::vector<double>& xs, const std::vector<double>& ys) {
+  if (xs.size() != ys.size())
+    throw domain_error("spearman: series lengths differ (" + std::to_string(xs.size()) + " vs " +
+                       std::to_string(ys.size()) + ")");
+  if (xs.size() < 2) throw domain_error("spearman: need at least 2 points");
+  const auto rx = mid_ranks(xs), ry = mid_ranks(ys);
+  const double n = static_cast<double>(rx.size());
+  double mx = 0.0, my = 0.0;
+  for (std::size_t i = 0; i < rx.size(); ++i) {
+    mx += rx[i];
+    my += ry[i];
+  }
+  mx /= n;
+  my /= n;
+  double sxy = 0.0, sxx = 0.0, syy = 0.0;
+  for (std::size_t i = 0; i < rx.size(); ++i) {
+    sxy += (rx[i] - mx) * (ry[i] - my);
+    sxx += (rx[i] - mx) * (rx[i] - mx);
+    syy += (ry[i] - my) * (ry[i] - my);
+  }
+  if (sxx == 0.0 || syy == 0.0) throw domain_error("spearman: constant series, coefficient undefined");
+  return sxy / std::sqrt(sxx * syy);
+}
+
+DistributionStats distribution_stats(const std::vector<double>& values) {
+  if (values.empty()) throw domain_error("distribution_stats: no samples");
+  DistributionStats st;
+  st.count = static_cast<int>(values.size());
+  st.min = st.max = values.front();
+  double sum = 0.0;
+  for (double v : values) {
+    st.min = std::min(st.min, v);
+    st.max = std::max(st.max, v);
+    sum += v;
+  }
+  st.mean = sum / static_cast<double>(st.count);
+  double sq = 0.0;
+  for (double v : values) sq += (v - st.mean) * (v - st.mean);
+  st.stddev = std::sqrt(sq / static_cast<double>(st.count));
+  return st;
+}
+
+std::vector<RankOrder> sample_orders(int n, int n_samples, std::uint64_t seed) {
+  if (n_samples < 1) throw domain_error("sample_orders: need at least 1 sample");
+  std::vector<int32_t> flat(static_cast<std::size_t>(n) * static_cast<std::size_t>(n_samples));
+  check(rw_sample_orders(n, n_samples, seed, flat.data()));
+  std::vector<RankOrder> out(static_cast<std::size_t>(n_samples));
+  for (int k = 0; k < n_samples; ++k)
+    out[static_cast<std::size_t>(k)].perm.assign(flat.begin() + static_cast<std::ptrdiff_t>(k) * n,
+                                                 flat.begin() + static_cast<std::ptrdiff_t>(k + 1) * n);
+  return out;
+}
+
+std::vector<double> sample_costs(const CostMatrix& m, const CollectiveSpec& spec, int n_samples, std::uint64_t seed) {
+  if (n_samples < 1) throw domain_error("sample_orders: need at least 1 sample");
+  validate(spec);
+  if (m.n() != spec.n)
+    throw domain_error("matrix is " + std::to_string(m.n()) + "x" + std::to_string(m.n()) + " but spec has N=" +
+                       std::to_string(spec.n));
+  std::vector<double> costs(static_cast<std::size_t>(n_samples));
+  const rw_spec cs = to_c(spec);
+  check(rw_sample_costs(device_problem(m), &cs, n_samples, seed, costs.data()));
+  return costs;
+}
+
+DistributionStats sample_cost_distribution(const CostMatrix& m, const CollectiveSpec& spec, int n_samples,
+                                           std::uint64_t seed) {
+  return distribution_stats(sample_costs(m, spec, n_samples, seed));
+}
+
+// ------------------------------------------------------------------ smtlib --
+// Stage-2 side file (out of the GPU scope): rank variables r_i in [0, N),
+// pairwise distinct; matrix flattened into an Array(Int, Real) constant; the
+// model's objective over (sel r_i r_j); optional strict bound on the cost.
+std::string emit_smtlib(const CostMatrix& m, const CollectiveSpec& spec, std::optional<double> upper_bound,
+                        int emission_cap) {
+  validate(spec);
+  validate(m);
+  if (m.n() != spec.n) throw domain_error("matrix dimension does not match spec.n");
+  const int n = spec.n;
+  const bool heavy = spec.algorithm == Algorithm::DoubleBinaryTree || spec.algorithm == Algorithm::BCube;
+  if (heavy && n > emission_cap)
+    throw domain_error(std::string("refusing ") + to_string(spec.algorithm) + " emission for N=" + std::to_string(n) +
+                       " > cap " + std::to_string(emission_cap) + " (term blow-up); raise the cap to force");
+  auto var = [n](int i) { return "r_" + std::to_string(alias_rank(i, n)); };
+  auto term = [&](int i, int j, double bytes) {
+    const std::string sel = "(sel " + var(i) + " " + var(j) + ")";
+    return spec.cost_mode == CostMode::LatencyOnly ? sel : "(* " + trim_real(bytes) + " " + sel + ")";
+  };
+  auto fold_max = [](const std::vector<std::string>& ts) {
+    std::string acc = ts.front();
+    for (std::size_t k = 1; k < ts.size(); ++k) acc = "(max2 " + acc + " " + ts[k] + ")";
+    return acc;
+  };
+  std::string objective;
+  if (n == 1) {
+    objective = "0.0";
+  } else if (spec.algorithm == Algorithm::Ring) {
+    objective = "(+";
+    for (int i = 0; i < n; ++i) objective += " " + term(i, i - 1, spec.size_bytes);
+    objective += ")";
+  } else if (spec.algorithm == Algorithm::DoubleBinaryTree) {
+    const double half = spec.size_bytes / 2.0;
+    std::function<std::string(int, int, int)> tree = [&](int i, int j, int sh) -> std::string {
+      if (i >= j) return "0.0";
+      const int mid = (i + j) / 2;
+      return "(max2 (+ " + term(mid + sh, (3 * i + j) / 2 - 1 + sh, half) + " " + tree(i, mid - 1, sh) + ") (+ " +
+             term(mid + sh, (i + 3 * j) / 2 + 1 + sh, half) + " " + tree(mid + 1, j, sh) + "))";
+    };
+    objective = "(max2 " + tree(0, n - 1, 0) + " " + tree(0, n - 1, -1) + ")";
+  } else {
+    const Schedule sch = expand_schedule(spec);
+    objective = "(+";
+    for (const auto& round : sch.rounds) {
+      std::vector<std::string> ts;
+      for (const auto& t : round) ts.push_back(term(t.src, t.dst, t.bytes));
+      objective += " " + fold_max(ts);
+    }
+    objective += ")";
+  }
+  std::ostringstream o;
+  o << "; rank-order cost minimization\n; algorithm=" << to_string(spec.algorithm) << " n=" << n
+    << " size_bytes=" << trim_real(spec.size_bytes) << " mode=" << to_string(spec.cost_mode);
+  if (spec.algorithm == Algorithm::BCube) o << " b=" << spec.bcube_b;
+  if (spec.algorithm == Algorithm::HalvingDoubling) o << " pairing=" << to_string(spec.hd_pairing);
+  o << "\n; solve with an optimizing solver, e.g.: z3 <file>\n(set-option :produce-models true)\n";
+  if (spec.algorithm != Algorithm::Ring) o << "(define-fun max2 ((a Real) (b Real)) Real (ite (>= a b) a b))\n";
+  o << "(declare-const c (Array Int Real))\n";
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) o << "(assert (= (select c " << (i * n + j) << ") " << trim_real(m.at(i, j)) << "))\n";
+  for (int i = 0; i < n; ++i) o << "(declare-const r_" << i << " Int)\n";
+  for (int i = 0; i < n; ++i) o << "(assert (and (>= r_" << i << " 0) (< r_" << i << " " << n << ")))\n";
+  o << "(assert (distinct";
+  for (int i = 0; i < n; ++i) o << " r_" << i;
+  o << "))\n(define-fun sel ((i Int) (j Int)) Real (select c (+ (* " << n << " i) j)))\n";
+  o << "(define-fun cost () Real " << objective << ")\n";
+  if (upper_bound) o << "(assert (< cost " << trim_real(*upper_bound) << "))\n";
+  o << "(minimize cost)\n(check-sat)\n(get-objectives)\n(get-model)\n";
+  return o.str();
+}
+
+RankOrder parse_model_file(const std::string& text, int n) {
+  RankOrder order;
+  order.perm.assign(static_cast<std::size_t>(n), -1);
+  std::istringstream in(text);
+  std::string line;
+  int assigned = 0;
+  while (std::getline(in, line)) {
+    const std::size_t first = line.find_first_not_of(" \t\r");
+    if (first == std::string::npos || line[first] == ';' || line[first] == '#') continue;
+    int idx = -1, value = -1, used = -1;
+    const bool ok = std::sscanf(line.c_str(), " r_%d = %d %n", &idx, &value, &used) == 2 && used >= 0 &&
+                    line.find_first_not_of(" \t\r", static_cast<std::size_t>(used)) == std::string::npos;
+    if (!ok) throw domain_error("model line not of the form 'r_<i> = <int>': '" + line + "'");
+    if (idx < 0 || idx >= n)
+      throw domain_error("model assigns r_" + std::to_string(idx) + " outside [0, " + std::to_string(n) + ")");
+    if (order.perm[static_cast<std::size_t>(idx)] != -1)
+      throw domain_error("model assigns r_" + std::to_string(idx) + " twice");
+    order.perm[static_cast<std::size_t>(idx)] = value;
+    ++assigned;
+  }
+  if (assigned != n)
+    throw domain_error("model assigns " + std::to_string(assigned) + " of " + std::to_string(n) + " rank variables");
+  validate(order, n);
+  return order;
+}
+
+bool balanced_sexpr(const std::string& text) {
+  long depth = 0;
+  bool comment = false;
+  for (char ch : text) {
+    if (comment) {
+      comment = ch != '\n';
+      continue;
+    }
+    if (ch == ';') comment = true;
+    else if (ch == '(') ++depth;
+    else if (ch == ')' && --depth < 0) return false;
+  }
+  return depth == 0;
+}
+
+// ---------------------------------------------------------- GPU options ----
+void set_gpu_options(const GpuOptions& opts) {
+  std::lock_guard<std::mutex> lock(options_mu());
+  options_ref() = opts;
+}
+
+GpuOptions gpu_options() {
+  std::lock_guard<std::mutex> lock(options_mu());
+  return options_ref();
+}
+
+}  // namespace rankweave

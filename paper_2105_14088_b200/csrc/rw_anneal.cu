@@ -1,0 +1,777 @@
+// rw_anneal.cu -- simulated annealing (K4) and batched local search (K3),
+// replacing anneal / neighbor (proj/src/solver.cpp:107-202).
+//
+// Schedule semantics kept from the reference:
+//   * T0 = population stddev of 100 random-order costs when
+//     initial_temperature <= 0 (solver.cpp:152-165), 1.0 if that is <= 0;
+//   * T_floor = T0 * 1e-6 and the level temperatures are produced by the same
+//     repeated multiplication `t *= cooling` (solver.cpp:166-182), computed on
+//     the host and uploaded, so the level count (2757 at 0.995) is identical;
+//   * steps_per_temperature proposals per level (default 4N, solver.cpp:149);
+//   * Metropolis: accept when delta <= 0 or U < exp(-delta / t) (solver.cpp:188);
+//   * chain 0 starts from the identity order, so the result never costs more
+//     than the identity (solver.cpp:172-173); the other chains start from
+//     random orders;
+//   * the wall-clock budget is honoured between kernel launches (each launch
+//     runs a bounded number of temperature levels), so budget = 1e-9 s runs
+//     no annealing at all, as test_solver.cpp:196-213 expects.
+//
+// GPU design: one warp per chain, Philox4x32-10 keyed by (seed, global chain
+// id, lane) so results do not depend on how chains are sharded over GPUs.
+// Ring (the model with O(1) move deltas) uses speculative proposals: all 32
+// lanes price a move against the same state, the lowest-numbered accepting
+// lane wins.  Because rejected proposals leave the state unchanged this is
+// the sequential Metropolis chain; proposals after the winner are discarded
+// and are NOT counted as evaluations.  Other models price each proposal with
+// a warp-cooperative full evaluation (the reference's unit of work).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "rw_device.cuh"
+#include "rw_internal.h"
+#include "rw_models.cuh"
+
+namespace rwb {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kOrWindow = 48;  // or-opt segment displacement window
+
+struct AnnealArgs {
+  int n;
+  int chains;         // chains in this launch
+  int64_t gid0;       // global id of chain 0 of this launch
+  int level_begin;
+  int level_end;
+  int steps;
+  const double* temps;
+  uint64_t seed;
+  double mul;         // ring: kernel units -> real cost
+  int symmetric;
+  int model;
+  double scale;
+  size_t mat_smem;
+  int warp_bytes;     // per-warp shared bytes
+  uint16_t* cur;
+  uint16_t* best;
+  double* cur_cost;   // kernel units (ring) / real cost (others)
+  double* best_cost;
+  unsigned long long* ctr;
+  unsigned long long* proposals;
+  RoundsArgs rounds;
+  DbtArgs dbt;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+template <typename T>
+__device__ __forceinline__ const T* stage_mat(const T* g, size_t bytes, unsigned char* smem) {
+  const uint4* src = reinterpret_cast<const uint4*>(g);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  const size_t vecs = bytes >> 4;
+  for (size_t k = threadIdx.x; k < vecs; k += blockDim.x) dst[k] = __ldg(src + k);
+  const unsigned char* gs = reinterpret_cast<const unsigned char*>(g);
+  for (size_t k = (vecs << 4) + threadIdx.x; k < bytes; k += blockDim.x) smem[k] = gs[k];
+  __syncthreads();
+  return reinterpret_cast<const T*>(smem);
+}
+
+__device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+// Move encoding shared by proposal and application.
+struct Move {
+  int type;  // 0 swap(i, j), 1 reverse [i..j], 2 rotate-left block [i, i+j) by k
+  int i, j, k;
+};
+
+__device__ __forceinline__ Move draw_move(uint4 r, int n, bool symmetric) {
+  Move m;
+  const uint32_t sel = r.x & 7u;
+  m.type = symmetric ? (sel < 4 ? 1 : sel < 6 ? 0 : 2) : (sel < 4 ? 0 : 2);
+  if (n < 6 && m.type == 2) m.type = 0;
+  if (m.type != 2) {
+    int i = (int)(((uint64_t)r.y * (uint32_t)n) >> 32);
+    int j = (int)(((uint64_t)r.z * (uint32_t)(n - 1)) >> 32);
+    if (j >= i) ++j;
+    if (i > j) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    if (m.type == 1 && i == 0 && j == n - 1) j = n - 2;  // full reversal: same cycle
+    m.i = i;
+    m.j = j;
+    m.k = 0;
+  } else {
+    // segment length L in {1,2,3}, displacement d in [1, min(W, n-L-1)],
+    // forward (rotate by L) or backward (rotate by d)
+    const int L = 1 + (int)((r.x >> 3) % 3u);
+    const int dmax = min(kOrWindow, n - L - 1);
+    const int d = 1 + (int)(((uint64_t)r.z * (uint32_t)dmax) >> 32);
+    const int len = L + d;
+    const int s = (int)(((uint64_t)r.y * (uint32_t)(n - len + 1)) >> 32);
+    m.i = s;
+    m.j = len;
+    m.k = ((r.x >> 6) & 1u) ? L : d;
+  }
+  return m;
+}
+
+// Ring delta in kernel units for a move against the current order.
+template <typename T, bool kSmem, typename Acc>
+__device__ __forceinline__ Acc ring_delta(const uint16_t* p, int n, const T* mat, const Move& m) {
+  auto D = [&](int a, int b) -> Acc { return (Acc)mat_at<T, kSmem>(mat, n, a, b); };
+  if (m.type == 1) {  // reverse [i..j] (symmetric matrices)
+    const int a = p[wrapi(m.i - 1, n)], b = p[m.i], c = p[m.j], d = p[wrapi(m.j + 1, n)];
+    return (D(c, a) + D(d, b)) - (D(b, a) + D(d, c));
+  }
+  if (m.type == 0) {  // swap positions i < j
+    int h[4] = {m.i, wrapi(m.i + 1, n), m.j, wrapi(m.j + 1, n)};
+    Acc oldc = 0, newc = 0;
+    for (int q = 0; q < 4; ++q) {
+      bool dup = false;
+      for (int r = 0; r < q; ++r) dup |= (h[r] == h[q]);
+      if (dup) continue;
+      const int pos = h[q], prv = wrapi(h[q] - 1, n);
+      const int cur_o = p[pos], prv_o = p[prv];
+      const int cur_n = pos == m.i ? p[m.j] : pos == m.j ? p[m.i] : cur_o;
+      const int prv_n = prv == m.i ? p[m.j] : prv == m.j ? p[m.i] : prv_o;
+      oldc += D(cur_o, prv_o);
+      newc += D(cur_n, prv_n);
+    }
+    return newc - oldc;
+  }
+  // rotate-left block [s, s+len) by k: A = p[s..s+k), B = p[s+k..s+len)
+  const int s = m.i, len = m.j, k = m.k;
+  const int x = p[wrapi(s - 1, n)], w = p[wrapi(s + len, n)];
+  const int a0 = p[s], al = p[s + k - 1], b0 = p[s + k], bl = p[s + len - 1];
+  return (D(b0, x) + D(a0, bl) + D(w, al)) - (D(a0, x) + D(b0, al) + D(w, bl));
+}
+
+// Apply a move to the warp's order (all lanes participate).
+__device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, int lane) {
+  if (m.type == 0) {
+    if (lane == 0) {
+      const uint16_t t = p[m.i];
+      p[m.i] = p[m.j];
+      p[m.j] = t;
+    }
+  } else if (m.type == 1) {
+    const int half = (m.j - m.i + 1) >> 1;
+    for (int q = lane; q < half; q += 32) {
+      const uint16_t t = p[m.i + q];
+      p[m.i + q] = p[m.j - q];
+      p[m.j - q] = t;
+    }
+  } else {
+    const int s = m.i, len = m.j, k = m.k;
+    uint16_t v[(kOrWindow + 3 + 31) / 32];
+#pragma unroll
+    for (int q = 0; q < (kOrWindow + 3 + 31) / 32; ++q) {
+      const int e = lane + 32 * q;
+      if (e < len) {
+        int src = e + k;
+        if (src >= len) src -= len;
+        v[q] = p[s + src];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < (kOrWindow + 3 + 31) / 32; ++q) {
+      const int e = lane + 32 * q;
+      if (e < len) p[s + e] = v[q];
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void store_order(uint16_t* g, const uint16_t* s, int n, int lane) {
+  for (int i = lane; i < n; i += 32) g[i] = s[i];
+}
+
+// ------------------------------------------------------------- init -----
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_anneal_init(AnnealArgs a, const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (chain >= a.chains) return;
+  const int n = a.n;
+  unsigned char* wbase = smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes;
+  uint16_t* p = reinterpret_cast<uint16_t*>(wbase);
+  const int64_t gid = a.gid0 + chain;
+  for (int i = lane; i < n; i += 32) p[i] = (uint16_t)i;
+  __syncwarp();
+  if (gid != 0 && lane == 0) {  // Fisher-Yates from a dedicated Philox stream
+    Philox rng;
+    rng.init(a.seed ^ 0x5eed5eed5eed5eedull, (uint64_t)gid);
+    for (int i = n - 1; i > 0; --i) {
+      const int j = (int)rng.below((uint32_t)(i + 1));
+      const uint16_t t = p[i];
+      p[i] = p[j];
+      p[j] = t;
+    }
+  }
+  __syncwarp();
+  double c;
+  if (a.model == kRing) {
+    c = warp_ring_raw<T, kSmem>(p, n, mat, lane);
+  } else if (a.model == kDoubleBinaryTree) {
+    double* vals = reinterpret_cast<double*>(wbase + 2 * al16((size_t)n * 2));
+    if (a.dbt.gvals) vals = a.dbt.gvals + (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * a.dbt.edges;
+    c = warp_dbt_cost<T, kSmem>(p, n, mat, a.dbt, a.scale, vals, lane);
+  } else {
+    c = warp_rounds_cost<T, kSmem>(p, n, mat, a.rounds, a.scale, lane);
+  }
+  store_order(a.cur + (size_t)chain * n, p, n, lane);
+  store_order(a.best + (size_t)chain * n, p, n, lane);
+  if (lane == 0) {
+    a.cur_cost[chain] = c;
+    a.best_cost[chain] = c;
+    a.ctr[chain] = 0;
+    a.proposals[chain] = 0;
+  }
+}
+
+// ------------------------------------------------------- ring anneal -----
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (chain >= a.chains) return;
+  const int n = a.n;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes);
+  const uint16_t* gcur = a.cur + (size_t)chain * n;
+  for (int i = lane; i < n; i += 32) p[i] = gcur[i];
+  __syncwarp();
+  using Acc = typename std::conditional<std::is_same<T, uint16_t>::value, long long, double>::type;
+  double cur = a.cur_cost[chain];
+  double best = a.best_cost[chain];
+  unsigned long long ctr = a.ctr[chain];
+  unsigned long long props = a.proposals[chain];
+  const int64_t gid = a.gid0 + chain;
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint64_t stream = ((uint64_t)gid << 5) | (uint64_t)lane;
+  const bool sym = a.symmetric != 0;
+  for (int level = a.level_begin; level < a.level_end; ++level) {
+    const double t = a.temps[level];
+    const double inv_t = a.mul / t;  // real delta / t = units * mul / t
+    int remaining = a.steps;
+    while (remaining > 0) {
+      const int active = min(32, remaining);
+      Philox rng;
+      rng.key = key;
+      rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+      const uint4 r = rng.block();
+      ++ctr;
+      const Move m = draw_move(r, n, sym);
+      const Acc delta = ring_delta<T, kSmem, Acc>(p, n, mat, m);
+      bool acc = false;
+      if (lane < active) {
+        if (delta <= (Acc)0) acc = true;
+        else {
+          const float u = (float)(r.w >> 8) * 0x1.0p-24f;
+          acc = u < __expf(-(float)((double)delta * inv_t));
+        }
+      }
+      const unsigned mask = __ballot_sync(kFull, acc);
+      if (mask) {
+        const int w = __ffs(mask) - 1;
+        Move mw;
+        mw.type = __shfl_sync(kFull, m.type, w);
+        mw.i = __shfl_sync(kFull, m.i, w);
+        mw.j = __shfl_sync(kFull, m.j, w);
+        mw.k = __shfl_sync(kFull, m.k, w);
+        const Acc dw = __shfl_sync(kFull, delta, w);
+        apply_move(p, n, mw, lane);
+        cur += (double)dw;
+        props += (unsigned long long)(w + 1);
+        remaining -= w + 1;
+        if (cur < best) {
+          best = cur;
+          store_order(a.best + (size_t)chain * n, p, n, lane);
+        }
+      } else {
+        props += (unsigned long long)active;
+        remaining -= active;
+      }
+    }
+    if constexpr (!std::is_same<T, uint16_t>::value) cur = warp_ring_raw<T, kSmem>(p, n, mat, lane);  // drift resync
+  }
+  __syncwarp();
+  store_order(a.cur + (size_t)chain * n, p, n, lane);
+  if (lane == 0) {
+    a.cur_cost[chain] = cur;
+    a.best_cost[chain] = best;
+    a.ctr[chain] = ctr;
+    a.proposals[chain] = props;
+  }
+}
+
+// --------------------------------------------- full-evaluation anneal -----
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_anneal_full(AnnealArgs a, const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (chain >= a.chains) return;
+  const int n = a.n;
+  unsigned char* wbase = smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes;
+  uint16_t* p = reinterpret_cast<uint16_t*>(wbase);
+  uint16_t* q = reinterpret_cast<uint16_t*>(wbase + al16((size_t)n * 2));
+  double* vals = reinterpret_cast<double*>(wbase + 2 * al16((size_t)n * 2));
+  if (a.dbt.gvals) vals = a.dbt.gvals + (size_t)chain * a.dbt.edges;
+  const uint16_t* gcur = a.cur + (size_t)chain * n;
+  for (int i = lane; i < n; i += 32) p[i] = gcur[i];
+  __syncwarp();
+  double cur = a.cur_cost[chain];
+  double best = a.best_cost[chain];
+  unsigned long long ctr = a.ctr[chain];
+  unsigned long long props = a.proposals[chain];
+  const int64_t gid = a.gid0 + chain;
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint64_t stream = ((uint64_t)gid << 5) | 31u;
+  for (int level = a.level_begin; level < a.level_end; ++level) {
+    const double t = a.temps[level];
+    for (int s = 0; s < a.steps; ++s) {
+      Philox rng;
+      rng.key = key;
+      rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+      const uint4 r = rng.block();
+      ++ctr;
+      const Move m = draw_move(r, n, true);
+      for (int i = lane; i < n; i += 32) q[i] = p[i];
+      __syncwarp();
+      apply_move(q, n, m, lane);
+      double c;
+      if (a.model == kDoubleBinaryTree) c = warp_dbt_cost<T, kSmem>(q, n, mat, a.dbt, a.scale, vals, lane);
+      else c = warp_rounds_cost<T, kSmem>(q, n, mat, a.rounds, a.scale, lane);
+      const double delta = c - cur;
+      bool acc = delta <= 0.0;
+      if (!acc) {
+        const float u = (float)(r.w >> 8) * 0x1.0p-24f;
+        acc = u < __expf(-(float)(delta / t));
+      }
+      ++props;
+      if (acc) {
+        uint16_t* tmp = p;
+        p = q;
+        q = tmp;
+        cur = c;
+        if (cur < best) {
+          best = cur;
+          store_order(a.best + (size_t)chain * n, p, n, lane);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  store_order(a.cur + (size_t)chain * n, p, n, lane);
+  if (lane == 0) {
+    a.cur_cost[chain] = cur;
+    a.best_cost[chain] = best;
+    a.ctr[chain] = ctr;
+    a.proposals[chain] = props;
+  }
+}
+
+// Argmin over chains of (exact cost, global chain id).
+__global__ void k_chain_argmin(const double* cost, int chains, int64_t gid0, double* out_cost, long long* out_chain) {
+  __shared__ double sc[1024];
+  __shared__ long long si[1024];
+  double bc = __longlong_as_double(0x7ff0000000000000ll);
+  long long bi = -1;
+  for (int c = threadIdx.x; c < chains; c += blockDim.x) {
+    const double v = cost[c];
+    if (v < bc || bi < 0) {
+      bc = v;
+      bi = gid0 + c;
+    }
+  }
+  sc[threadIdx.x] = bc;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double oc = sc[threadIdx.x + s];
+      const long long oi = si[threadIdx.x + s];
+      if (oi >= 0 && (si[threadIdx.x] < 0 || oc < sc[threadIdx.x] || (oc == sc[threadIdx.x] && oi < si[threadIdx.x]))) {
+        sc[threadIdx.x] = oc;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_cost = sc[0];
+    *out_chain = si[0];
+  }
+}
+
+__global__ void k_sample_orders(int n, int64_t samples, uint64_t seed, uint16_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = w; s < samples; s += nw) {
+    uint16_t* p = out + s * n;
+    for (int i = lane; i < n; i += 32) p[i] = (uint16_t)i;
+    __syncwarp();
+    if (lane == 0) {
+      Philox rng;
+      rng.init(seed, (uint64_t)s);
+      for (int i = n - 1; i > 0; --i) {
+        const int j = (int)rng.below((uint32_t)(i + 1));
+        const uint16_t t = p[i];
+        p[i] = p[j];
+        p[j] = t;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// -------------------------------------------------------- local search -----
+// Best-improvement over all 2-opt (symmetric), swap and windowed or-opt
+// moves of one order per warp; repeats until no move improves or max_rounds.
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_local_search_ring(const T* __restrict__ gmat, size_t mat_smem, int n,
+                                                           int symmetric, int64_t batch, uint16_t* orders,
+                                                           int warp_bytes, int max_rounds,
+                                                           unsigned long long* evals) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, mat_smem, smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t ord = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (ord >= batch) return;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(mat_smem) + (size_t)wib * warp_bytes);
+  uint16_t* g = orders + ord * n;
+  for (int i = lane; i < n; i += 32) p[i] = g[i];
+  __syncwarp();
+  using Acc = typename std::conditional<std::is_same<T, uint16_t>::value, long long, double>::type;
+  unsigned long long ev = 0;
+  const long long pairs = (long long)n * (n - 1) / 2;
+  for (int round = 0; round < max_rounds && n >= 4; ++round) {
+    Acc best_d = 0;
+    Move best_m{-1, 0, 0, 0};
+    // moves indexed by (type, pair index); pair (i<j) from a triangular index
+    for (int type = (symmetric ? 1 : 0); type >= 0; --type) {
+      for (long long t = lane; t < pairs; t += 32) {
+        // unrank t -> (i, j), i < j
+        long long i = (long long)((2.0 * n - 1.0 - sqrt((2.0 * n - 1.0) * (2.0 * n - 1.0) - 8.0 * (double)t)) * 0.5);
+        if (i < 0) i = 0;
+        while (i > 0 && i * (2LL * n - i - 1) / 2 > t) --i;
+        while ((i + 1) * (2LL * n - i - 2) / 2 <= t) ++i;
+        const long long j = t - i * (2LL * n - i - 1) / 2 + i + 1;
+        Move m{type, (int)i, (int)j, 0};
+        if (type == 1 && i == 0 && j == n - 1) continue;
+        const Acc d = ring_delta<T, kSmem, Acc>(p, n, mat, m);
+        ++ev;
+        if (d < best_d) {
+          best_d = d;
+          best_m = m;
+        }
+      }
+    }
+    for (int L = 1; L <= 3; ++L) {
+      const int dmax = min(kOrWindow, n - L - 1);
+      const long long cnt = (long long)(n) * dmax * 2;
+      for (long long t = lane; t < cnt; t += 32) {
+        const int dir = (int)(t & 1);
+        const int d = 1 + (int)((t >> 1) % dmax);
+        const int s = (int)((t >> 1) / dmax);
+        const int len = L + d;
+        if (s + len > n) continue;
+        Move m{2, s, len, dir ? L : d};
+        const Acc dd = ring_delta<T, kSmem, Acc>(p, n, mat, m);
+        ++ev;
+        if (dd < best_d) {
+          best_d = dd;
+          best_m = m;
+        }
+      }
+    }
+    // warp argmin of best_d (ties: lowest lane)
+    Acc v = best_d;
+    int who = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const Acc ov = __shfl_xor_sync(kFull, v, o);
+      const int ow = __shfl_xor_sync(kFull, who, o);
+      if (ov < v || (ov == v && ow < who)) {
+        v = ov;
+        who = ow;
+      }
+    }
+    if (!(v < (Acc)0)) break;
+    Move m;
+    m.type = __shfl_sync(kFull, best_m.type, who);
+    m.i = __shfl_sync(kFull, best_m.i, who);
+    m.j = __shfl_sync(kFull, best_m.j, who);
+    m.k = __shfl_sync(kFull, best_m.k, who);
+    apply_move(p, n, m, lane);
+  }
+  for (int i = lane; i < n; i += 32) g[i] = p[i];
+  ev = warp_sum(ev);
+  if (lane == 0) atomicAdd(evals, ev);
+}
+
+struct DevInfo {
+  int sms;
+  int smem;
+};
+DevInfo dev_info(int dev) {
+  DevInfo d{};
+  RW_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+  RW_CUDA(cudaDeviceGetAttribute(&d.smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  d.smem = std::min(d.smem, 227 * 1024) - 1024;
+  return d;
+}
+
+template <typename K>
+void smem_attr(K k, size_t bytes) {
+  if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+double population_stddev(const std::vector<double>& v) {
+  // distribution_stats (stats.cpp:64-81): serial sums, population stddev
+  double sum = 0.0;
+  for (double x : v) sum += x;
+  const double mean = sum / static_cast<double>(v.size());
+  double sq = 0.0;
+  for (double x : v) sq += (x - mean) * (x - mean);
+  return std::sqrt(sq / static_cast<double>(v.size()));
+}
+
+template <typename T>
+AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_config& cfg, const rw_gpu_config& gpu) {
+  using Clock = std::chrono::steady_clock;
+  const auto start = Clock::now();
+  DeviceGuard g(p.device);
+  ThreadCtx& c = thread_ctx(p.device);
+  cudaStream_t st = c.stream[0];
+  const int n = plan.n;
+  const DevInfo di = dev_info(p.device);
+  AnnealResult res;
+  const int steps = cfg.steps_per_temperature > 0 ? cfg.steps_per_temperature : 4 * n;
+
+  // T0 from 100 random orders (solver.cpp:152-165)
+  double t0 = cfg.initial_temperature;
+  uint64_t evals = 0;
+  if (t0 <= 0.0) {
+    auto* d_o = static_cast<uint16_t*>(c.scratch(0, (size_t)100 * n * 2));
+    auto* d_c = static_cast<double*>(c.scratch(1, 100 * 8));
+    sample_orders_device(n, 100, cfg.seed ^ 0xfeedull, d_o, st);
+    launch_evaluate(p, plan, d_o, 2, 100, d_c, true, false, c.d_err, st);
+    std::vector<double> costs(100);
+    RW_CUDA(cudaMemcpyAsync(costs.data(), d_c, 800, cudaMemcpyDeviceToHost, st));
+    RW_CUDA(cudaStreamSynchronize(st));
+    t0 = population_stddev(costs);
+    evals += 100;
+  }
+  if (t0 <= 0.0) t0 = 1.0;
+  const double t_floor = t0 * 1e-6;
+  std::vector<double> temps;
+  for (double t = t0; t > t_floor; t *= cfg.cooling) temps.push_back(t);
+  const int levels = static_cast<int>(temps.size());
+
+  int chains = gpu.chains > 0 ? gpu.chains : std::max(cfg.restarts, 4 * di.sms);
+  const int64_t gid0 = gpu.chain_begin > 0 ? gpu.chain_begin : 0;
+  int steps_eff = steps;
+  if (gpu.max_proposals > 0) {
+    const long long per_chain = gpu.max_proposals / std::max<long long>(1, (long long)chains * std::max(1, levels));
+    steps_eff = (int)std::max<long long>(1, per_chain);
+  }
+
+  // device state
+  const size_t ord_bytes = (size_t)chains * n * 2;
+  char* base = static_cast<char*>(c.scratch(4, 2 * al16(ord_bytes) + (size_t)chains * 32 + (size_t)levels * 8 + 64));
+  AnnealArgs a{};
+  a.n = n;
+  a.chains = chains;
+  a.gid0 = gid0;
+  a.steps = steps_eff;
+  a.seed = cfg.seed;
+  a.symmetric = p.symmetric ? 1 : 0;
+  a.model = plan.model;
+  a.scale = p.scale;
+  a.mul = plan.model == kRing ? plan.ring_mul : 1.0;
+  a.cur = reinterpret_cast<uint16_t*>(base);
+  a.best = reinterpret_cast<uint16_t*>(base + al16(ord_bytes));
+  a.cur_cost = reinterpret_cast<double*>(base + 2 * al16(ord_bytes));
+  a.best_cost = a.cur_cost + chains;
+  a.ctr = reinterpret_cast<unsigned long long*>(a.best_cost + chains);
+  a.proposals = a.ctr + chains;
+  double* d_temps = reinterpret_cast<double*>(a.proposals + chains);
+  a.temps = d_temps;
+  if (levels) RW_CUDA(cudaMemcpyAsync(d_temps, temps.data(), (size_t)levels * 8, cudaMemcpyHostToDevice, st));
+  if (plan.model == kHalvingDoubling || plan.model == kBCube) {
+    a.rounds.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
+    a.rounds.rounds = plan.rounds;
+    a.rounds.b = plan.bcube_b;
+    a.rounds.mode = plan.mode;
+    for (int r = 0; r < plan.rounds; ++r) a.rounds.bytes[r] = plan.round_bytes[r];
+  }
+  int dbt_edges = 0;
+  if (plan.model == kDoubleBinaryTree && plan.dbt) {
+    dbt_edges = plan.dbt->edges;
+    a.dbt.src = plan.dbt->d_src();
+    a.dbt.dst = plan.dbt->d_dst();
+    a.dbt.c0 = plan.dbt->d_c0();
+    a.dbt.c1 = plan.dbt->d_c1();
+    a.dbt.depth_off = plan.dbt->d_depth_off();
+    a.dbt.depths = plan.dbt->depths;
+    a.dbt.edges = dbt_edges;
+    a.dbt.mode = plan.mode;
+    a.dbt.half = plan.half;
+  }
+  // shared memory plan: two order buffers (+ dbt values) per warp
+  size_t warp_bytes = 2 * al16((size_t)n * 2) + al16((size_t)dbt_edges * 8);
+  const size_t mat_bytes = (size_t)n * n * sizeof(T);
+  int wpb = 8;
+  bool smem_mat = mat_bytes + (size_t)wpb * warp_bytes <= (size_t)di.smem;
+  if (!smem_mat) {
+    while (wpb > 1 && (size_t)wpb * warp_bytes > (size_t)di.smem) wpb >>= 1;
+    if ((size_t)wpb * warp_bytes > (size_t)di.smem) {  // dbt values to global memory
+      warp_bytes = 2 * al16((size_t)n * 2);
+      a.dbt.gvals = static_cast<double*>(c.scratch(5, (size_t)chains * dbt_edges * 8 + 8));
+    }
+  }
+  a.mat_smem = smem_mat ? mat_bytes : 0;
+  a.warp_bytes = (int)warp_bytes;
+  const size_t dyn = al16(a.mat_smem) + (size_t)wpb * warp_bytes;
+  const int grid = (chains + wpb - 1) / wpb;
+  const int threads = wpb * 32;
+
+  auto init = smem_mat ? k_anneal_init<T, true> : k_anneal_init<T, false>;
+  smem_attr(init, dyn);
+  init<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
+  RW_CUDA(cudaGetLastError());
+  evals += (uint64_t)chains;
+
+  auto ring = smem_mat ? k_anneal_ring<T, true> : k_anneal_ring<T, false>;
+  auto full = smem_mat ? k_anneal_full<T, true> : k_anneal_full<T, false>;
+  smem_attr(ring, dyn);
+  smem_attr(full, dyn);
+  const auto deadline = start + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(cfg.budget_s));
+  const int per_launch = std::max(1, (int)std::min<long long>(levels, (1LL << 16) / std::max(1, steps_eff)));
+  int level = 0;
+  while (level < levels && n > 1) {
+    RW_CUDA(cudaStreamSynchronize(st));
+    if (Clock::now() >= deadline) break;
+    a.level_begin = level;
+    a.level_end = std::min(levels, level + per_launch);
+    if (plan.model == kRing) ring<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
+    else full<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
+    RW_CUDA(cudaGetLastError());
+    level = a.level_end;
+  }
+
+  // exact re-score of every chain's best, then (cost, global chain) argmin
+  double* d_exact = static_cast<double*>(c.scratch(1, (size_t)chains * 8 + 16));
+  launch_evaluate(p, plan, a.best, 2, chains, d_exact, true, false, c.d_err, st);
+  double* d_wc = d_exact + chains;
+  long long* d_wi = reinterpret_cast<long long*>(d_exact + chains + 1);
+  k_chain_argmin<<<1, 1024, 0, st>>>(d_exact, chains, gid0, d_wc, d_wi);
+  RW_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> props((size_t)chains);
+  RW_CUDA(cudaMemcpyAsync(props.data(), a.proposals, (size_t)chains * 8, cudaMemcpyDeviceToHost, st));
+  double wc = 0.0;
+  long long wi = 0;
+  RW_CUDA(cudaMemcpyAsync(&wc, d_wc, 8, cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaMemcpyAsync(&wi, d_wi, 8, cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaStreamSynchronize(st));
+  std::vector<uint16_t> w((size_t)n);
+  RW_CUDA(cudaMemcpy(w.data(), a.best + (size_t)(wi - gid0) * n, (size_t)n * 2, cudaMemcpyDeviceToHost));
+  uint64_t total_props = 0;
+  for (unsigned long long x : props) total_props += x;
+  evals += total_props;
+  res.proposals = total_props;
+  res.chains = chains;
+  res.levels = levels;
+  res.t0 = t0;
+  res.order.assign(w.begin(), w.end());
+  res.cost = wc;
+  res.evaluations = evals;
+  res.chain = wi;
+  res.levels_run = level;
+  return res;
+}
+
+template <typename T>
+void local_search_typed(Problem& p, const EvalPlan& plan, int32_t* perms, int64_t batch, int max_rounds,
+                        double* costs, uint64_t* evals) {
+  DeviceGuard g(p.device);
+  ThreadCtx& c = thread_ctx(p.device);
+  cudaStream_t st = c.stream[0];
+  const int n = plan.n;
+  const DevInfo di = dev_info(p.device);
+  std::vector<uint16_t> h((size_t)batch * n);
+  for (size_t k = 0; k < h.size(); ++k) h[k] = (uint16_t)perms[k];
+  char* base = static_cast<char*>(c.scratch(4, al16(h.size() * 2) + (size_t)batch * 8 + 64));
+  auto* d_o = reinterpret_cast<uint16_t*>(base);
+  auto* d_c = reinterpret_cast<double*>(base + al16(h.size() * 2));
+  auto* d_ev = reinterpret_cast<unsigned long long*>(d_c + batch);
+  RW_CUDA(cudaMemcpyAsync(d_o, h.data(), h.size() * 2, cudaMemcpyHostToDevice, st));
+  RW_CUDA(cudaMemsetAsync(d_ev, 0, 8, st));
+  if (plan.model == kRing && n >= 4) {
+    const size_t warp_bytes = al16((size_t)n * 2);
+    const size_t mat_bytes = (size_t)n * n * sizeof(T);
+    const int wpb = 8;
+    const bool smem_mat = mat_bytes + wpb * warp_bytes <= (size_t)di.smem;
+    const size_t dyn = (smem_mat ? al16(mat_bytes) : 0) + wpb * warp_bytes;
+    auto k = smem_mat ? k_local_search_ring<T, true> : k_local_search_ring<T, false>;
+    smem_attr(k, dyn);
+    const int grid = (int)((batch + wpb - 1) / wpb);
+    k<<<grid, wpb * 32, dyn, st>>>(static_cast<const T*>(p.d_mat), smem_mat ? mat_bytes : 0, n, p.symmetric ? 1 : 0,
+                                   batch, d_o, (int)warp_bytes, max_rounds, d_ev);
+    RW_CUDA(cudaGetLastError());
+  }
+  launch_evaluate(p, plan, d_o, 2, batch, d_c, true, false, c.d_err, st);
+  unsigned long long ev = 0;
+  RW_CUDA(cudaMemcpyAsync(h.data(), d_o, h.size() * 2, cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaMemcpyAsync(costs, d_c, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaMemcpyAsync(&ev, d_ev, 8, cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaStreamSynchronize(st));
+  for (size_t k = 0; k < h.size(); ++k) perms[k] = h[k];
+  *evals = ev + (uint64_t)batch;
+}
+
+}  // namespace
+
+void sample_orders_device(int n, int64_t samples, uint64_t seed, uint16_t* d_out, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((samples + 7) / 8, 148 * 16);
+  k_sample_orders<<<(int)std::max<int64_t>(1, blocks), 256, 0, st>>>(n, samples, seed, d_out);
+  RW_CUDA(cudaGetLastError());
+}
+
+AnnealResult anneal_device(Problem& p, const EvalPlan& plan, const rw_solver_config& cfg, const rw_gpu_config& gpu) {
+  switch (p.storage) {
+    case RW_STORAGE_U16: return anneal_typed<uint16_t>(p, plan, cfg, gpu);
+    case RW_STORAGE_F32: return anneal_typed<float>(p, plan, cfg, gpu);
+    default: return anneal_typed<double>(p, plan, cfg, gpu);
+  }
+}
+
+void local_search_device(Problem& p, const EvalPlan& plan, int32_t* perms, int64_t batch, int max_rounds,
+                         double* costs, uint64_t* evals) {
+  if (batch <= 0) return;
+  switch (p.storage) {
+    case RW_STORAGE_U16: local_search_typed<uint16_t>(p, plan, perms, batch, max_rounds, costs, evals); break;
+    case RW_STORAGE_F32: local_search_typed<float>(p, plan, perms, batch, max_rounds, costs, evals); break;
+    default: local_search_typed<double>(p, plan, perms, batch, max_rounds, costs, evals); break;
+  }
+}
+
+}  // namespace rwb

@@ -1,0 +1,377 @@
+// rw_capi.cpp -- the extern "C" boundary (include/rankweave_c.h).  Every
+// entry point validates its arguments with the reference's wording, maps C++
+// exceptions onto rw_status and records the message for rw_last_error().
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rw_internal.h"
+
+namespace rwb {
+Problem* problem_create(const double* rtt, int n, int hint, int device);
+void problem_destroy(Problem* p);
+rw_status generate_matrix(int nlevels, const int32_t* fanout, const double* latency, const double* bw,
+                          const double* oversub, double jitter, uint64_t seed, double* out, int64_t cap, int32_t* n_out);
+void relabel_matrix(double* m, int n, uint64_t seed);
+}  // namespace rwb
+
+struct rw_problem {
+  rwb::Problem* impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+rw_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return RW_OK;
+  } catch (const rwb::Failure& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return RW_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RW_ERR_INTERNAL;
+  }
+}
+
+rwb::Problem& get(const rw_problem* p) {
+  if (!p || !p->impl) rwb::fail_domain("null rw_problem");
+  return *p->impl;
+}
+
+void need(const void* ptr, const char* what) {
+  if (!ptr) rwb::fail_domain(std::string("null pointer argument: ") + what);
+}
+
+// validate(order, n) (types.cpp:100-110) for one host order.
+void validate_host_order(const int32_t* perm, int32_t size, int n) {
+  if (size != n)
+    rwb::fail_domain("rank order has " + std::to_string(size) + " entries, expected " + std::to_string(n));
+  std::vector<char> seen(static_cast<size_t>(n), 0);
+  for (int i = 0; i < n; ++i) {
+    const int v = perm[i];
+    if (v < 0 || v >= n || seen[static_cast<size_t>(v)])
+      rwb::fail_domain("rank order is not a permutation of [0, " + std::to_string(n) + ")");
+    seen[static_cast<size_t>(v)] = 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rw_last_error(void) { return g_last_error.c_str(); }
+int32_t rw_abi_version(void) { return RW_ABI_VERSION; }
+
+int32_t rw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+rw_status rw_validate_spec(const rw_spec* spec) {
+  return guarded([&] {
+    need(spec, "spec");
+    rwb::validate_spec(*spec);
+  });
+}
+
+rw_status rw_problem_create(const double* rtt_us, int32_t n, int32_t storage_hint, int32_t device, rw_problem** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    need(rtt_us, "rtt_us");
+    auto* h = new rw_problem{nullptr};
+    try {
+      h->impl = rwb::problem_create(rtt_us, n, storage_hint, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+rw_status rw_problem_destroy(rw_problem* p) {
+  return guarded([&] {
+    if (!p) return;
+    rwb::problem_destroy(p->impl);
+    delete p;
+  });
+}
+
+rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out) {
+  return guarded([&] {
+    need(out, "out");
+    const rwb::Problem& q = get(p);
+    out->n = q.n;
+    out->device = q.device;
+    out->storage = q.storage;
+    out->frac_bits = q.frac_bits;
+    out->symmetric = q.symmetric ? 1 : 0;
+    out->zero_diagonal = q.zero_diag ? 1 : 0;
+    out->device_bytes = static_cast<int64_t>(q.mat_bytes);
+    out->max_value = q.max_value;
+  });
+}
+
+rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* perm, double* cost) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(perm, "perm");
+    need(cost, "cost");
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    validate_host_order(perm, spec->n, spec->n);
+    rwb::evaluate_host_orders(q, plan, perm, 1, cost, /*exact=*/true, /*validate=*/true, nullptr);
+  });
+}
+
+rw_status rw_evaluate_batch(const rw_problem* p, const rw_spec* spec, const int32_t* perms, int64_t batch,
+                            double* costs, uint32_t flags, rw_eval_report* report) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(perms, "perms");
+      need(costs, "costs");
+    }
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    rwb::evaluate_host_orders(q, plan, perms, batch, costs, (flags & RW_EVAL_EXACT) != 0,
+                              (flags & RW_EVAL_NO_VALIDATE) == 0, report);
+  });
+}
+
+rw_status rw_evaluate_batch_device(const rw_problem* p, const rw_spec* spec, const void* d_perms, int32_t perm_bytes,
+                                   int64_t batch, double* d_costs, void* stream, uint32_t flags) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(d_perms, "d_perms");
+      need(d_costs, "d_costs");
+    }
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    rwb::DeviceGuard g(q.device);
+    rwb::launch_evaluate(q, plan, d_perms, perm_bytes, batch, d_costs, (flags & RW_EVAL_EXACT) != 0,
+                         (flags & RW_EVAL_NO_VALIDATE) == 0, q.d_err, static_cast<cudaStream_t>(stream));
+  });
+}
+
+rw_status rw_sync_errors(const rw_problem* p, void* stream) {
+  return guarded([&] {
+    rwb::Problem& q = get(p);
+    rwb::DeviceGuard g(q.device);
+    rwb::ThreadCtx& c = rwb::thread_ctx(q.device);
+    rwb::raise_order_errors(q.d_err, c.h_err, static_cast<cudaStream_t>(stream));
+  });
+}
+
+rw_status rw_schedule_cost(const rw_problem* p, int32_t semantics, int32_t nrounds, const int32_t* round_offsets,
+                           const int32_t* src, const int32_t* dst, const double* bytes, const int32_t* parent,
+                           int32_t cost_mode, const int32_t* perm, double* cost) {
+  return guarded([&] {
+    need(round_offsets, "round_offsets");
+    need(perm, "perm");
+    need(cost, "cost");
+    rwb::Problem& q = get(p);
+    if (nrounds < 0) rwb::fail_domain("nrounds must be >= 0");
+    if (semantics < RW_SEQUENTIAL_HOPS || semantics > RW_CRITICAL_PATH) rwb::fail_domain("schedule_cost: unknown semantics");
+    const int edges = round_offsets[nrounds];
+    if (edges > 0) {
+      need(src, "src");
+      need(dst, "dst");
+      need(bytes, "bytes");
+    }
+    validate_host_order(perm, q.n, q.n);
+    *cost = rwb::schedule_cost_device(q, semantics, nrounds, round_offsets, src, dst, bytes, parent, cost_mode, perm);
+  });
+}
+
+rw_status rw_brute_force_space(const rw_spec* spec, uint64_t* count_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(count_out, "count_out");
+    rwb::validate_spec(*spec);
+    *count_out = rwb::brute_force_space(*spec);
+  });
+}
+
+rw_status rw_brute_force(const rw_problem* p, const rw_spec* spec, int32_t threshold, int32_t* perm_out,
+                         double* cost_out, uint64_t* evals_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(perm_out, "perm_out");
+    need(cost_out, "cost_out");
+    rwb::validate_spec(*spec);
+    if (spec->n > threshold)
+      rwb::fail_domain("N=" + std::to_string(spec->n) + " exceeds the brute-force threshold " +
+                       std::to_string(threshold) + "; use anneal");
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    const uint64_t space = rwb::brute_force_space(*spec);
+    double cost = 0.0;
+    uint64_t index = 0;
+    rwb::brute_force_range(q, plan, 0, space, &cost, &index);
+    rwb::unrank(*spec, index, perm_out);
+    // Reported cost is the reference-identical evaluation of the winner.
+    rwb::evaluate_host_orders(q, plan, perm_out, 1, cost_out, true, true, nullptr);
+    if (evals_out) *evals_out = space;
+  });
+}
+
+rw_status rw_brute_force_range(const rw_problem* p, const rw_spec* spec, uint64_t first, uint64_t count,
+                               double* cost_out, uint64_t* index_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(cost_out, "cost_out");
+    need(index_out, "index_out");
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    const uint64_t space = rwb::brute_force_space(*spec);
+    if (first > space) first = space;
+    if (count > space - first) count = space - first;
+    rwb::brute_force_range(q, plan, first, count, cost_out, index_out);
+  });
+}
+
+rw_status rw_unrank(const rw_spec* spec, uint64_t index, int32_t* perm_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(perm_out, "perm_out");
+    rwb::validate_spec(*spec);
+    if (index >= rwb::brute_force_space(*spec)) rwb::fail_domain("lexicographic index out of range");
+    rwb::unrank(*spec, index, perm_out);
+  });
+}
+
+rw_status rw_anneal(const rw_problem* p, const rw_spec* spec, const rw_solver_config* cfg, const rw_gpu_config* gpu,
+                    int32_t* perm_out, double* cost_out, uint64_t* evals_out, rw_search_report* report) {
+  return guarded([&] {
+    const auto t_start = std::chrono::steady_clock::now();
+    need(spec, "spec");
+    need(cfg, "cfg");
+    need(perm_out, "perm_out");
+    need(cost_out, "cost_out");
+    rwb::validate_spec(*spec);
+    // validate(SolverConfig) -- solver.cpp:50-55
+    if (!(cfg->budget_s > 0.0)) rwb::fail_domain("solver budget must be > 0");
+    if (!(cfg->cooling > 0.0 && cfg->cooling < 1.0)) rwb::fail_domain("cooling factor must be in (0, 1)");
+    if (cfg->restarts < 1) rwb::fail_domain("restarts must be >= 1");
+    if (cfg->brute_force_threshold < 2) rwb::fail_domain("brute-force threshold must be >= 2");
+    rwb::Problem& q = get(p);
+    if (q.n != spec->n) rwb::fail_domain("matrix dimension does not match spec.n");
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    rw_gpu_config g{};
+    if (gpu) g = *gpu;
+    const rwb::AnnealResult r = rwb::anneal_device(q, plan, *cfg, g);
+    std::copy(r.order.begin(), r.order.end(), perm_out);
+    *cost_out = r.cost;
+    if (evals_out) *evals_out = r.evaluations;
+    if (report) {
+      report->winner_chain = r.chain;
+      report->chains = r.chains;
+      report->proposals = static_cast<int64_t>(r.proposals);
+      report->levels = r.levels;
+      report->levels_run = r.levels_run;
+      report->initial_temperature = r.t0;
+      report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
+  });
+}
+
+rw_status rw_local_search(const rw_problem* p, const rw_spec* spec, int32_t* perms_inout, int64_t batch,
+                          int32_t max_rounds, double* costs_out, uint64_t* evals_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(perms_inout, "perms_inout");
+      need(costs_out, "costs_out");
+    }
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    for (int64_t b = 0; b < batch; ++b) validate_host_order(perms_inout + b * spec->n, spec->n, spec->n);
+    uint64_t ev = 0;
+    rwb::local_search_device(q, plan, perms_inout, batch, max_rounds, costs_out, &ev);
+    if (evals_out) *evals_out = ev;
+  });
+}
+
+rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* perms_out) {
+  return guarded([&] {
+    if (samples < 1) rwb::fail_domain("sample_orders: need at least 1 sample");
+    if (n < 1 || n > 65536) rwb::fail_domain("sample_orders: n out of range");
+    need(perms_out, "perms_out");
+    int dev = 0;
+    RW_CUDA(cudaGetDevice(&dev));
+    rwb::ThreadCtx& c = rwb::thread_ctx(dev);
+    const size_t count = static_cast<size_t>(n) * static_cast<size_t>(samples);
+    auto* d = static_cast<uint16_t*>(c.scratch(0, count * 2));
+    rwb::sample_orders_device(n, samples, seed, d, c.stream[0]);
+    std::vector<uint16_t> h(count);
+    RW_CUDA(cudaMemcpyAsync(h.data(), d, count * 2, cudaMemcpyDeviceToHost, c.stream[0]));
+    RW_CUDA(cudaStreamSynchronize(c.stream[0]));
+    for (size_t k = 0; k < count; ++k) perms_out[k] = h[k];
+  });
+}
+
+rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed, double* costs_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(costs_out, "costs_out");
+    if (samples < 1) rwb::fail_domain("sample_orders: need at least 1 sample");
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    rwb::DeviceGuard g(q.device);
+    rwb::ThreadCtx& c = rwb::thread_ctx(q.device);
+    const size_t count = static_cast<size_t>(spec->n) * static_cast<size_t>(samples);
+    auto* d = static_cast<uint16_t*>(c.scratch(0, count * 2));
+    auto* dc = static_cast<double*>(c.scratch(1, static_cast<size_t>(samples) * 8));
+    rwb::sample_orders_device(spec->n, samples, seed, d, c.stream[0]);
+    // Reported costs are reference-identical (exact ring summation).
+    rwb::launch_evaluate(q, plan, d, 2, samples, dc, /*exact=*/true, /*validate=*/false, c.d_err, c.stream[0]);
+    RW_CUDA(cudaMemcpyAsync(costs_out, dc, static_cast<size_t>(samples) * 8, cudaMemcpyDeviceToHost, c.stream[0]));
+    RW_CUDA(cudaStreamSynchronize(c.stream[0]));
+  });
+}
+
+rw_status rw_generate_matrix(int32_t nlevels, const int32_t* fanout, const double* latency_us, const double* bandwidth,
+                             const double* oversub, double jitter, uint64_t seed, double* out, int64_t out_capacity,
+                             int32_t* n_out) {
+  rw_status st = RW_OK;
+  const rw_status g = guarded([&] {
+    need(fanout, "fanout");
+    need(latency_us, "latency_us");
+    need(bandwidth, "bandwidth");
+    need(oversub, "oversub");
+    need(n_out, "n_out");
+    st = rwb::generate_matrix(nlevels, fanout, latency_us, bandwidth, oversub, jitter, seed, out, out_capacity, n_out);
+  });
+  return g != RW_OK ? g : st;
+}
+
+rw_status rw_relabel_matrix(double* m, int32_t n, uint64_t seed) {
+  return guarded([&] {
+    need(m, "m");
+    if (n < 1) rwb::fail_domain("n must be >= 1");
+    rwb::relabel_matrix(m, n, seed);
+  });
+}
+
+}  // extern "C"

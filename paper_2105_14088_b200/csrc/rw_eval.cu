@@ -1,0 +1,602 @@
+// rw_eval.cu -- batch cost-model scoring on sm_100a (K1), the
+// reference-identical ring re-score (K0) and generic schedule re-costing.
+//
+// Reference semantics followed (paths relative to the reference root):
+//   ring_cost              proj/src/cost_model.cpp:59-69   hop i = rtt[perm[i]][perm[i-1]], sorted FP64 sum
+//   halving_doubling_cost  proj/src/cost_model.cpp:71-92   sum over rounds of the round max
+//   double_binary_tree     proj/src/cost_model.cpp:94-116  max of two critical paths
+//   bcube_cost             proj/src/cost_model.cpp:118-138
+//   schedule_cost          proj/src/cost_model.cpp:238-285
+//   validate(order)        proj/src/types.cpp:100-110      (bijection check on every order)
+//
+// Exactness.  fl(x * b) is monotone in x for b > 0, so a round maximum of
+// fl(rtt * bytes) equals fl(max(rtt) * bytes): the max-of-rounds models take
+// the max of raw matrix codes and do exactly the reference's FP64 multiply /
+// add sequence per round -> identical bits for every matrix.  The double
+// binary tree does the reference's per-edge multiply and add in the same
+// operand order.  Ring sums are order-sensitive: with u16 fixed-point storage
+// the kernel sums integer codes (exact, and equal to the reference whenever
+// its own arithmetic is exact -- EvalPlan::bit_exact); otherwise the fast
+// kernel's FP64 tree sum is within a few ulps, and K0 sorts the hops and sums
+// them serially exactly like sorted_sum (cost_model.cpp:38-43).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <type_traits>
+
+#include "rw_device.cuh"
+#include "rw_internal.h"
+#include "rw_models.cuh"
+
+namespace rwb {
+
+using namespace dev;
+
+namespace {
+
+struct DevProps {
+  int sms = 148;
+  int smem_optin = 227 * 1024;
+};
+
+DevProps device_props(int dev) {
+  static std::mutex mu;
+  static std::map<int, DevProps> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  DevProps p;
+  RW_CUDA(cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev));
+  RW_CUDA(cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cache[dev] = p;
+  return p;
+}
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct KArgs {
+  int64_t batch;
+  int n;
+  int flag_stride;     // bytes of validation flags per warp
+  int perm_stride;     // bytes of staged order per warp (u16)
+  int val_stride;      // bytes of per-warp FP64 scratch (dbt)
+  size_t mat_smem;     // bytes of matrix staged in shared memory (0: global)
+  double scale;        // u16 code scale
+  unsigned long long* err;
+};
+
+// Stage the whole matrix into shared memory (16-byte vector copies).
+template <typename T>
+__device__ __forceinline__ const T* stage_matrix(const T* __restrict__ g, size_t bytes, unsigned char* smem) {
+  const uint4* src = reinterpret_cast<const uint4*>(g);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  const size_t vecs = bytes >> 4;
+  for (size_t k = threadIdx.x; k < vecs; k += blockDim.x) dst[k] = __ldg(src + k);
+  const unsigned char* gs = reinterpret_cast<const unsigned char*>(g);
+  for (size_t k = (vecs << 4) + threadIdx.x; k < bytes; k += blockDim.x) smem[k] = gs[k];
+  __syncthreads();
+  return reinterpret_cast<const T*>(smem);
+}
+
+// ------------------------------------------------------------ K1: ring ----
+// One warp per order.  Lane l handles positions l, l+32, ...; the predecessor
+// of each position comes from the neighbouring lane by shuffle, so the order
+// is read exactly once with coalesced loads.
+template <typename T, typename P, bool kSmem, bool kValidate>
+__global__ void __launch_bounds__(1024) k_ring(KArgs a, const P* __restrict__ perms, const T* __restrict__ gmat,
+                                               double mul, double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_matrix<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint8_t* flags = smem + align16(a.mat_smem) + (size_t)wib * a.flag_stride;
+  const int n = a.n;
+  if constexpr (kValidate)
+    for (int k = lane; k < a.flag_stride; k += 32) flags[k] = 0;
+  __syncwarp();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint8_t marker = 0;
+  constexpr bool kInt = std::is_same<T, uint16_t>::value;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < a.batch; b += nwarps) {
+    marker = marker == 255 ? 1 : marker + 1;
+    const P* pp = perms + b * n;
+    int carry = ld_order<P>(pp, n - 1);
+    bool bad = false;
+    unsigned long long iacc = 0;
+    double dacc = 0.0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const int cur = (i < n) ? ld_order<P>(pp, i) : 0;
+      int prev = __shfl_up_sync(kFull, cur, 1);
+      const int last = __shfl_sync(kFull, cur, 31);
+      if (lane == 0) prev = carry;
+      carry = last;
+      if (i < n) {
+        const bool ok = (unsigned)cur < (unsigned)n && (unsigned)prev < (unsigned)n;
+        if (kValidate && (unsigned)cur < (unsigned)n) flags[cur] = marker;
+        if (ok) {
+          const T v = mat_at<T, kSmem>(mat, n, cur, prev);
+          if constexpr (kInt) iacc += v;
+          else dacc = __dadd_rn(dacc, (double)v);
+        } else {
+          bad = true;
+        }
+      }
+    }
+    double cost;
+    if constexpr (kInt) cost = __dmul_rn((double)warp_sum(iacc), mul);
+    else cost = __dmul_rn(warp_sum(dacc), mul);
+    if constexpr (kValidate) {
+      __syncwarp();
+      bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      costs[b] = (n == 1) ? 0.0 : cost;
+      if (kValidate && bad) report_bad_order(a.err, n, b);
+    }
+  }
+}
+
+// Stage one order into the warp's shared buffer and mark validation flags.
+template <typename P, bool kValidate>
+__device__ __forceinline__ bool stage_order(const P* __restrict__ pp, int n, uint16_t* s_perm, uint8_t* flags,
+                                            uint8_t marker, int lane) {
+  bool bad = false;
+  for (int i = lane; i < n; i += 32) {
+    const int v = ld_order<P>(pp, i);
+    if ((unsigned)v < (unsigned)n) {
+      s_perm[i] = (uint16_t)v;
+      if (kValidate) flags[v] = marker;
+    } else {
+      s_perm[i] = 0;
+      bad = true;
+    }
+  }
+  __syncwarp();
+  return bad;
+}
+
+// ------------------------------------------------- K1: max-of-rounds ----
+template <typename T, typename P, bool kSmem, bool kValidate>
+__global__ void __launch_bounds__(1024) k_rounds(KArgs a, RoundsArgs r, const P* __restrict__ perms,
+                                                 const T* __restrict__ gmat, double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_matrix<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* wbase = smem + align16(a.mat_smem) + (size_t)wib * (a.flag_stride + a.perm_stride);
+  uint16_t* s_perm = reinterpret_cast<uint16_t*>(wbase);
+  uint8_t* flags = wbase + a.perm_stride;
+  const int n = a.n;
+  if constexpr (kValidate)
+    for (int k = lane; k < a.flag_stride; k += 32) flags[k] = 0;
+  __syncwarp();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint8_t marker = 0;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < a.batch; b += nwarps) {
+    marker = marker == 255 ? 1 : marker + 1;
+    bool bad = stage_order<P, kValidate>(perms + b * n, n, s_perm, flags, marker, lane);
+    const double total = warp_rounds_cost<T, kSmem>(s_perm, n, mat, r, a.scale, lane);
+    if constexpr (kValidate) {
+      bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      costs[b] = (n == 1) ? 0.0 : total;
+      if (kValidate && bad) report_bad_order(a.err, n, b);
+    }
+    __syncwarp();
+  }
+}
+
+// -------------------------------------------------- K1: double tree -------
+template <typename T, typename P, bool kSmem, bool kValidate>
+__global__ void __launch_bounds__(1024) k_dbt(KArgs a, DbtArgs d, const P* __restrict__ perms,
+                                              const T* __restrict__ gmat, double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_matrix<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* wbase = smem + align16(a.mat_smem) + (size_t)wib * (a.flag_stride + a.perm_stride + a.val_stride);
+  uint16_t* s_perm = reinterpret_cast<uint16_t*>(wbase);
+  uint8_t* flags = wbase + a.perm_stride;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double* vals = a.val_stride ? reinterpret_cast<double*>(wbase + a.perm_stride + a.flag_stride)
+                              : d.gvals + (size_t)gwarp * d.edges;
+  const int n = a.n;
+  if constexpr (kValidate)
+    for (int k = lane; k < a.flag_stride; k += 32) flags[k] = 0;
+  __syncwarp();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint8_t marker = 0;
+  for (int64_t b = gwarp; b < a.batch; b += nwarps) {
+    marker = marker == 255 ? 1 : marker + 1;
+    bool bad = stage_order<P, kValidate>(perms + b * n, n, s_perm, flags, marker, lane);
+    const double best = warp_dbt_cost<T, kSmem>(s_perm, n, mat, d, a.scale, vals, lane);
+    if constexpr (kValidate) {
+      bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      costs[b] = best;
+      if (kValidate && bad) report_bad_order(a.err, n, b);
+    }
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------- K0: exact (sorted) ring ----
+// One CTA per order: hops fl(rtt * S) into a power-of-two buffer padded with
+// +inf, bitonic sort ascending, then one thread sums serially -- the exact
+// operation sequence of sorted_sum (cost_model.cpp:38-43).
+__device__ void bitonic_sort_block(double* v, int np2) {
+  for (int k = 2; k <= np2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double x = v[i], y = v[ixj];
+          const bool up = (i & k) == 0;
+          if (up ? (x > y) : (x < y)) {
+            v[i] = y;
+            v[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <typename T, typename P, bool kValidate>
+__global__ void __launch_bounds__(256) k_ring_exact(KArgs a, const P* __restrict__ perms, const T* __restrict__ gmat,
+                                                    double size_bytes, int mode, int np2, double* gscratch,
+                                                    uint8_t* gflags, double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  double* vals = gscratch ? gscratch + (size_t)blockIdx.x * np2 : reinterpret_cast<double*>(smem);
+  uint8_t* flags = gflags ? gflags + (size_t)blockIdx.x * a.flag_stride : smem + (size_t)np2 * 8;
+  __shared__ int s_bad;
+  if (kValidate)
+    for (int k = threadIdx.x; k < a.flag_stride; k += blockDim.x) flags[k] = 0;
+  uint8_t marker = 0;
+  for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
+    marker = marker == 255 ? 1 : marker + 1;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    const P* pp = perms + b * n;
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+      double h = __longlong_as_double(0x7ff0000000000000ll);  // +inf padding
+      if (i < n) {
+        const int cur = ld_order<P>(pp, i);
+        const int prev = ld_order<P>(pp, i == 0 ? n - 1 : i - 1);
+        if ((unsigned)cur < (unsigned)n && (unsigned)prev < (unsigned)n) {
+          if (kValidate) flags[cur] = marker;
+          h = to_double(ld_matrix<T>(gmat, (size_t)cur * n + prev), a.scale);
+          if (mode == RW_LATENCY_TIMES_SIZE) h = __dmul_rn(h, size_bytes);
+        } else {
+          s_bad = 1;
+          h = 0.0;
+        }
+      }
+      vals[i] = h;
+    }
+    __syncthreads();
+    bitonic_sort_block(vals, np2);
+    if (kValidate) {
+      for (int k = threadIdx.x; k < n; k += blockDim.x)
+        if (flags[k] != marker) s_bad = 1;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      double total = 0.0;
+      for (int i = 0; i < n; ++i) total = __dadd_rn(total, vals[i]);
+      costs[b] = (n == 1) ? 0.0 : total;
+      if (kValidate && s_bad) report_bad_order(a.err, n, b);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- dispatch ---
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+template <typename T, typename P>
+void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v, int64_t batch, double* d_costs,
+                  bool exact, bool validate, int* err_slot, cudaStream_t st, int slot) {
+  const P* d_perms = static_cast<const P*>(d_perms_v);
+  const T* gmat = static_cast<const T*>(p.d_mat);
+  const DevProps dp = device_props(p.device);
+  const int n = plan.n;
+  KArgs a{};
+  a.batch = batch;
+  a.n = n;
+  a.flag_stride = validate ? (int)align16((size_t)n) : 0;
+  a.scale = p.scale;
+  a.err = reinterpret_cast<unsigned long long*>(err_slot);
+  const size_t budget = (size_t)std::min(dp.smem_optin, 227 * 1024) - 1024;
+  const size_t mat_bytes = (size_t)n * n * sizeof(T);
+
+  if (plan.model == kRing && exact && !plan.bit_exact && n > 1) {
+    const int np2 = 1 << (int)std::ceil(std::log2((double)std::max(n, 2)));
+    const size_t need = (size_t)np2 * 8 + (validate ? a.flag_stride : 0);
+    const int grid = (int)std::min<int64_t>(batch, (int64_t)dp.sms * 8);
+    double* gscratch = nullptr;
+    uint8_t* gflags = nullptr;
+    size_t dyn = need;
+    if (need > budget) {
+      ThreadCtx& c = thread_ctx(p.device);
+      gscratch = static_cast<double*>(c.scratch(slot, (size_t)grid * np2 * 8));
+      gflags = validate ? static_cast<uint8_t*>(c.scratch(slot + 1, (size_t)grid * a.flag_stride)) : nullptr;
+      dyn = 0;
+    }
+    auto kern = validate ? k_ring_exact<T, P, true> : k_ring_exact<T, P, false>;
+    set_smem(kern, dyn);
+    kern<<<grid, 256, dyn, st>>>(a, d_perms, gmat, plan.size_bytes, plan.mode, np2, gscratch, gflags, d_costs);
+    RW_CUDA(cudaGetLastError());
+    return;
+  }
+
+  // per-warp shared bytes and matrix placement
+  size_t per_warp = a.flag_stride;
+  if (plan.model != kRing) {
+    a.perm_stride = (int)align16((size_t)n * 2);
+    per_warp += a.perm_stride;
+  }
+  int edges = 0;
+  if (plan.model == kDoubleBinaryTree) {
+    edges = plan.dbt->edges;
+    a.val_stride = (int)align16((size_t)edges * 8);
+  }
+  int threads = 256;
+  bool smem_mat = mat_bytes + 16 * (per_warp + a.val_stride) <= budget;
+  if (smem_mat) {
+    a.mat_smem = mat_bytes;
+    // as many warps as fit beside the matrix, up to 32 (1024 threads)
+    const size_t room = budget - align16(mat_bytes);
+    const int warps = (int)std::min<size_t>(32, room / std::max<size_t>(1, per_warp + a.val_stride));
+    threads = std::max(1, warps / 4) * 128;
+  } else {
+    a.mat_smem = 0;
+    const size_t w = per_warp + a.val_stride;
+    int warps = 8;
+    while (warps > 1 && (size_t)warps * w > budget) warps >>= 1;
+    if ((size_t)warps * w > budget) a.val_stride = 0;  // dbt scratch goes to global memory
+    threads = warps * 32;
+  }
+  const int warps_per_block = threads / 32;
+  const size_t dyn = align16(a.mat_smem) + (size_t)warps_per_block * (per_warp + a.val_stride);
+  const int blocks_per_sm = smem_mat ? 1 : std::max(1, (int)std::min<size_t>(2048 / threads, budget / std::max<size_t>(dyn, 1)));
+  const int64_t want = (batch + warps_per_block - 1) / warps_per_block;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)dp.sms * blocks_per_sm));
+
+  if (plan.model == kRing) {
+    auto kern = smem_mat ? (validate ? k_ring<T, P, true, true> : k_ring<T, P, true, false>)
+                         : (validate ? k_ring<T, P, false, true> : k_ring<T, P, false, false>);
+    set_smem(kern, dyn);
+    kern<<<grid, threads, dyn, st>>>(a, d_perms, gmat, plan.ring_mul, d_costs);
+  } else if (plan.model == kDoubleBinaryTree) {
+    DbtArgs d{};
+    d.src = plan.dbt->d_src();
+    d.dst = plan.dbt->d_dst();
+    d.c0 = plan.dbt->d_c0();
+    d.c1 = plan.dbt->d_c1();
+    d.depth_off = plan.dbt->d_depth_off();
+    d.depths = plan.dbt->depths;
+    d.edges = edges;
+    d.mode = plan.mode;
+    d.half = plan.half;
+    if (a.val_stride == 0 && n > 1) {
+      ThreadCtx& c = thread_ctx(p.device);
+      d.gvals = static_cast<double*>(c.scratch(slot, (size_t)grid * warps_per_block * edges * 8));
+    }
+    auto kern = smem_mat ? (validate ? k_dbt<T, P, true, true> : k_dbt<T, P, true, false>)
+                         : (validate ? k_dbt<T, P, false, true> : k_dbt<T, P, false, false>);
+    set_smem(kern, dyn);
+    kern<<<grid, threads, dyn, st>>>(a, d, d_perms, gmat, d_costs);
+  } else {
+    RoundsArgs r{};
+    r.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
+    r.rounds = plan.rounds;
+    r.b = plan.bcube_b;
+    r.mode = plan.mode;
+    for (int k = 0; k < plan.rounds; ++k) r.bytes[k] = plan.round_bytes[k];
+    auto kern = smem_mat ? (validate ? k_rounds<T, P, true, true> : k_rounds<T, P, true, false>)
+                         : (validate ? k_rounds<T, P, false, true> : k_rounds<T, P, false, false>);
+    set_smem(kern, dyn);
+    kern<<<grid, threads, dyn, st>>>(a, r, d_perms, gmat, d_costs);
+  }
+  RW_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_storage(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                    double* d_costs, bool exact, bool validate, int* err, cudaStream_t st, int slot) {
+  if (perm_bytes == 2) launch_typed<T, uint16_t>(p, plan, d_perms, batch, d_costs, exact, validate, err, st, slot);
+  else launch_typed<T, int32_t>(p, plan, d_perms, batch, d_costs, exact, validate, err, st, slot);
+}
+
+// ------------------------------------------------------- schedule_cost ----
+template <typename T>
+__global__ void __launch_bounds__(256) k_schedule(const T* __restrict__ mat, double scale, int n, int semantics,
+                                                  int nrounds, const int32_t* __restrict__ roff,
+                                                  const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                                  const double* __restrict__ bytes, const int32_t* __restrict__ parent,
+                                                  int mode, const int32_t* __restrict__ perm, int np2, double* vals,
+                                                  double* value, double* child, double* out) {
+  const int edges = roff[nrounds];
+  auto alias = [n](int r) { return ((r % n) + n) % n; };
+  for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+    double c = __longlong_as_double(0x7ff0000000000000ll);
+    if (t < edges) {
+      const int ra = perm[alias(src[t])], rb = perm[alias(dst[t])];
+      c = to_double(mat[(size_t)ra * n + rb], scale);
+      if (mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, bytes[t]);
+    }
+    vals[t] = c;
+  }
+  __syncthreads();
+  if (semantics == RW_SEQUENTIAL_HOPS) {
+    bitonic_sort_block(vals, np2);
+    if (threadIdx.x == 0) {
+      double total = 0.0;
+      for (int t = 0; t < edges; ++t) total = __dadd_rn(total, vals[t]);
+      *out = total;
+    }
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  if (semantics == RW_BULK_SYNCHRONOUS_ROUNDS) {
+    double total = 0.0;
+    for (int r = 0; r < nrounds; ++r) {
+      double mx = 0.0;
+      for (int t = roff[r]; t < roff[r + 1]; ++t) mx = ref_max(mx, vals[t]);
+      total = __dadd_rn(total, mx);
+    }
+    *out = total;
+    return;
+  }
+  // CriticalPath: leaf-up accumulation, cost_model.cpp:260-281
+  double best = 0.0;
+  for (int r = nrounds - 1; r >= 0; --r) {
+    for (int t = roff[r]; t < roff[r + 1]; ++t) child[t] = 0.0;
+    if (r + 1 < nrounds) {
+      for (int t = roff[r + 1]; t < roff[r + 2]; ++t) {
+        const int pa = parent[t];
+        if (pa >= 0 && roff[r] + pa < roff[r + 1]) child[roff[r] + pa] = ref_max(child[roff[r] + pa], value[t]);
+      }
+    }
+    for (int t = roff[r]; t < roff[r + 1]; ++t) {
+      value[t] = __dadd_rn(vals[t], child[t]);
+      if (r == 0) best = ref_max(best, value[t]);
+    }
+  }
+  *out = best;
+}
+
+}  // namespace
+
+void launch_evaluate(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                     double* d_costs, bool exact, bool validate, int* err_slot, cudaStream_t st, int slot) {
+  if (batch <= 0) return;
+  if (perm_bytes != 2 && perm_bytes != 4) fail_domain("perm_bytes must be 2 or 4");
+  switch (p.storage) {
+    case RW_STORAGE_U16:
+      launch_storage<uint16_t>(p, plan, d_perms, perm_bytes, batch, d_costs, exact, validate, err_slot, st, slot);
+      break;
+    case RW_STORAGE_F32:
+      launch_storage<float>(p, plan, d_perms, perm_bytes, batch, d_costs, exact, validate, err_slot, st, slot);
+      break;
+    default:
+      launch_storage<double>(p, plan, d_perms, perm_bytes, batch, d_costs, exact, validate, err_slot, st, slot);
+      break;
+  }
+}
+
+void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms, int64_t batch, double* costs,
+                          bool exact, bool validate, rw_eval_report* report) {
+  if (batch <= 0) return;
+  DeviceGuard g(p.device);
+  ThreadCtx& c = thread_ctx(p.device);
+  const int n = plan.n;
+  // Chunked double-buffered pipeline: H2D(k+1) overlaps scoring(k) on the
+  // other stream; costs come back per chunk.
+  const int64_t row = (int64_t)n * 4;
+  int64_t chunk = std::max<int64_t>(1, ((int64_t)48 << 20) / row);
+  if (batch <= chunk) chunk = batch;
+  else if (batch < 4 * chunk) chunk = (batch + 3) / 4;
+  int32_t* d_perm[2];
+  double* d_cost[2];
+  for (int s = 0; s < 2; ++s) {
+    d_perm[s] = static_cast<int32_t*>(c.scratch(s, (size_t)chunk * row + (size_t)chunk * 8 + 64));
+    d_cost[s] = reinterpret_cast<double*>(reinterpret_cast<char*>(d_perm[s]) + align16((size_t)chunk * row));
+  }
+  RW_CUDA(cudaEventRecord(c.ev[0], c.stream[0]));
+  RW_CUDA(cudaStreamWaitEvent(c.stream[1], c.ev[0], 0));
+  int k = 0;
+  for (int64_t off = 0; off < batch; off += chunk, ++k) {
+    const int s = k & 1;
+    const int64_t cnt = std::min(chunk, batch - off);
+    cudaStream_t st = c.stream[s];
+    RW_CUDA(cudaMemcpyAsync(d_perm[s], perms + off * n, (size_t)cnt * row, cudaMemcpyHostToDevice, st));
+    launch_evaluate(p, plan, d_perm[s], 4, cnt, d_cost[s], exact, validate, c.d_err, st, 2 + 2 * s);
+    RW_CUDA(cudaMemcpyAsync(costs + off, d_cost[s], (size_t)cnt * 8, cudaMemcpyDeviceToHost, st));
+  }
+  RW_CUDA(cudaEventRecord(c.ev[1], c.stream[1]));
+  RW_CUDA(cudaStreamWaitEvent(c.stream[0], c.ev[1], 0));
+  RW_CUDA(cudaStreamSynchronize(c.stream[0]));
+  if (validate) raise_order_errors(c.d_err, c.h_err, c.stream[0]);
+  if (report) {
+    report->bit_exact = (plan.bit_exact || exact) ? 1 : 0;
+    report->kernel = plan.model;
+    report->lookups = lookups_per_eval(plan) * batch;
+  }
+}
+
+double schedule_cost_device(const Problem& p, int semantics, int nrounds, const int32_t* round_offsets,
+                            const int32_t* src, const int32_t* dst, const double* bytes, const int32_t* parent,
+                            int cost_mode, const int32_t* perm) {
+  DeviceGuard g(p.device);
+  ThreadCtx& c = thread_ctx(p.device);
+  cudaStream_t st = c.stream[0];
+  const int edges = round_offsets[nrounds];
+  const int n = p.n;
+  const int np2 = 1 << (int)std::ceil(std::log2((double)std::max(edges, 2)));
+  // layout: roff | src | dst | parent | perm (int32) then bytes | vals | value | child | out (double)
+  const size_t ints = (size_t)(nrounds + 1) + 3 * (size_t)edges + n;
+  const size_t dbl_off = align16(ints * 4);
+  const size_t total = dbl_off + ((size_t)edges + np2 + 2 * (size_t)edges + 1) * 8;
+  char* base = static_cast<char*>(c.scratch(6, total));
+  int32_t* d_roff = reinterpret_cast<int32_t*>(base);
+  int32_t* d_src = d_roff + nrounds + 1;
+  int32_t* d_dst = d_src + edges;
+  int32_t* d_par = d_dst + edges;
+  int32_t* d_perm = d_par + edges;
+  double* d_bytes = reinterpret_cast<double*>(base + dbl_off);
+  double* d_vals = d_bytes + edges;
+  double* d_value = d_vals + np2;
+  double* d_child = d_value + edges;
+  double* d_out = d_child + edges;
+  std::vector<int32_t> hi;
+  hi.reserve(ints);
+  hi.insert(hi.end(), round_offsets, round_offsets + nrounds + 1);
+  hi.insert(hi.end(), src, src + edges);
+  hi.insert(hi.end(), dst, dst + edges);
+  if (parent) hi.insert(hi.end(), parent, parent + edges);
+  else hi.insert(hi.end(), (size_t)edges, -1);
+  hi.insert(hi.end(), perm, perm + n);
+  RW_CUDA(cudaMemcpyAsync(d_roff, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice, st));
+  if (edges) RW_CUDA(cudaMemcpyAsync(d_bytes, bytes, (size_t)edges * 8, cudaMemcpyHostToDevice, st));
+  switch (p.storage) {
+    case RW_STORAGE_U16:
+      k_schedule<uint16_t><<<1, 256, 0, st>>>(static_cast<const uint16_t*>(p.d_mat), p.scale, n, semantics, nrounds,
+                                              d_roff, d_src, d_dst, d_bytes, d_par, cost_mode, d_perm, np2, d_vals,
+                                              d_value, d_child, d_out);
+      break;
+    case RW_STORAGE_F32:
+      k_schedule<float><<<1, 256, 0, st>>>(static_cast<const float*>(p.d_mat), p.scale, n, semantics, nrounds, d_roff,
+                                           d_src, d_dst, d_bytes, d_par, cost_mode, d_perm, np2, d_vals, d_value,
+                                           d_child, d_out);
+      break;
+    default:
+      k_schedule<double><<<1, 256, 0, st>>>(static_cast<const double*>(p.d_mat), p.scale, n, semantics, nrounds,
+                                            d_roff, d_src, d_dst, d_bytes, d_par, cost_mode, d_perm, np2, d_vals,
+                                            d_value, d_child, d_out);
+      break;
+  }
+  RW_CUDA(cudaGetLastError());
+  double out = 0.0;
+  RW_CUDA(cudaMemcpyAsync(&out, d_out, 8, cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaStreamSynchronize(st));
+  return out;
+}
+
+}  // namespace rwb

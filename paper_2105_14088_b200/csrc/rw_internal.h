@@ -1,0 +1,158 @@
+// rw_internal.h -- private declarations shared by the librankweave_b200
+// translation units (host C++ and CUDA).  Nothing here is part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rankweave_c.h"
+
+namespace rwb {
+
+// ---------------------------------------------------------------- errors ----
+struct Failure : std::runtime_error {
+  rw_status status;
+  Failure(rw_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void fail_domain(const std::string& m) { throw Failure(RW_ERR_DOMAIN, m); }
+[[noreturn]] inline void fail_internal(const std::string& m) { throw Failure(RW_ERR_INTERNAL, m); }
+void cuda_check(cudaError_t e, const char* expr, const char* file, int line);
+#define RW_CUDA(x) ::rwb::cuda_check((x), #x, __FILE__, __LINE__)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+// Model ids (= rw_spec.algorithm).
+enum Model : int { kRing = 0, kHalvingDoubling = 1, kDoubleBinaryTree = 2, kBCube = 3 };
+
+// ----------------------------------------------------------------- problem --
+// Critical-path form of the double binary tree for one n: the transfers of
+// expand_schedule (cost_model.cpp:194-222) in depth order, each with the two
+// transfers of its sub-interval as children.  Device resident.
+struct DbtPlan {
+  int n = 0;
+  int edges = 0;
+  int depths = 0;
+  std::vector<int32_t> h_src, h_dst, h_c0, h_c1, h_depth_off;
+  int32_t* d_all = nullptr;  // [src | dst | c0 | c1 | depth_off]
+  const int32_t* d_src() const { return d_all; }
+  const int32_t* d_dst() const { return d_all + edges; }
+  const int32_t* d_c0() const { return d_all + 2 * edges; }
+  const int32_t* d_c1() const { return d_all + 3 * edges; }
+  const int32_t* d_depth_off() const { return d_all + 4 * edges; }
+};
+
+struct Problem {
+  int n = 0;
+  int device = 0;
+  int storage = RW_STORAGE_F64;
+  int frac_bits = 0;
+  double scale = 1.0;  // u16: value = q * scale
+  bool symmetric = false;
+  bool zero_diag = false;
+  double max_value = 0.0;
+  uint32_t max_q = 0;
+  void* d_mat = nullptr;
+  size_t mat_bytes = 0;
+  int* d_err = nullptr;  // async error slot for *_device calls: {flag, min index}
+  std::mutex mu;
+  std::unique_ptr<DbtPlan> dbt;
+  size_t elem_bytes() const { return storage == RW_STORAGE_U16 ? 2 : storage == RW_STORAGE_F32 ? 4 : 8; }
+};
+
+// ---------------------------------------------------------------- planning --
+constexpr int kMaxRounds = 64;
+
+// Everything a scoring kernel needs for one (problem, spec), computed on the
+// host: per-round byte counts exactly as round_bytes() forms them
+// (cost_model.cpp:47-51), the ring multiplier, and exactness facts.
+struct EvalPlan {
+  int model = kRing;
+  int n = 0;
+  int mode = RW_LATENCY_TIMES_SIZE;
+  int pairing = RW_PAIRING_PAPER;
+  int bcube_b = 2;
+  int rounds = 0;
+  double size_bytes = 0.0;
+  double half = 0.0;                   // dbt: S / 2
+  double round_bytes[kMaxRounds] = {}; // hd / bcube
+  double ring_mul = 1.0;               // ring: cost = sum(raw) * ring_mul
+  bool ring_int = false;               // ring sums raw u16 codes as integers
+  bool bit_exact = false;              // fast path reproduces reference bits
+  const DbtPlan* dbt = nullptr;
+};
+
+void validate_spec(const rw_spec& s);                  // types.cpp:143-163 wording
+EvalPlan make_plan(Problem& p, const rw_spec& s);       // + n / matrix checks
+int64_t lookups_per_eval(const EvalPlan& plan);
+
+// Per-thread, per-device execution context for host-buffer calls.
+struct ThreadCtx {
+  int device = -1;
+  cudaStream_t stream[2] = {nullptr, nullptr};
+  cudaEvent_t ev[4] = {};
+  int* d_err = nullptr;
+  int* h_err = nullptr;  // pinned
+  void* d_buf[8] = {};
+  size_t d_cap[8] = {};
+  void* scratch(int slot, size_t bytes);
+};
+ThreadCtx& thread_ctx(int device);
+
+// Reads and clears an error slot; throws the reference's domain_error text.
+void raise_order_errors(int* d_err, int* h_err, cudaStream_t st);
+
+// ----------------------------------------------------------------- kernels --
+// Batch scoring (K1) of `batch` orders stored row-major (perm_bytes 2 or 4).
+// exact: reference-identical ring summation (K0).  validate: bijection check,
+// failures recorded in err_slot.
+// scratch_slot: first of two ThreadCtx scratch slots this launch may use.
+void launch_evaluate(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                     double* d_costs, bool exact, bool validate, int* err_slot, cudaStream_t st,
+                     int scratch_slot = 2);
+
+// Generic schedule re-costing (schedule_cost, cost_model.cpp:238-285), one order.
+double schedule_cost_device(const Problem& p, int semantics, int nrounds, const int32_t* round_offsets,
+                            const int32_t* src, const int32_t* dst, const double* bytes, const int32_t* parent,
+                            int cost_mode, const int32_t* perm);
+
+// Exhaustive search over lexicographic indices [first, first+count).
+void brute_force_range(const Problem& p, const EvalPlan& plan, uint64_t first, uint64_t count, double* cost_out,
+                       uint64_t* index_out);
+uint64_t brute_force_space(const rw_spec& s);
+void unrank(const rw_spec& s, uint64_t index, int32_t* perm_out);
+
+// Simulated annealing and local search.
+struct AnnealResult {
+  std::vector<int32_t> order;
+  double cost = 0.0;
+  uint64_t evaluations = 0;
+  int64_t chain = 0;     // global id of the winning chain
+  int64_t chains = 0;
+  uint64_t proposals = 0;
+  int levels = 0;
+  int levels_run = 0;    // temperature levels completed within the budget
+  double t0 = 0.0;
+};
+AnnealResult anneal_device(Problem& p, const EvalPlan& plan, const rw_solver_config& cfg, const rw_gpu_config& gpu);
+void local_search_device(Problem& p, const EvalPlan& plan, int32_t* perms, int64_t batch, int max_rounds,
+                         double* costs, uint64_t* evals);
+
+// Random orders (Philox), device side.
+void sample_orders_device(int n, int64_t samples, uint64_t seed, uint16_t* d_out, cudaStream_t st);
+
+// Scores host orders and returns reference-exact costs (used by search code).
+void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms, int64_t batch, double* costs,
+                          bool exact, bool validate, rw_eval_report* report);
+
+}  // namespace rwb

@@ -1,0 +1,116 @@
+// rw_models.cuh -- warp-cooperative cost models over an order staged in
+// shared memory.  Shared by the batch scorer (rw_eval.cu) and the annealer
+// (rw_anneal.cu).  Each function returns the reference-identical FP64 cost
+// (for ring: see the summation note in rw_eval.cu) in every lane.
+#pragma once
+
+#include "rw_device.cuh"
+#include "rw_internal.h"
+
+namespace rwb {
+namespace dev {
+
+template <typename T, bool kSmem>
+__device__ __forceinline__ T mat_at(const T* m, int n, int a, int b) {
+  if constexpr (kSmem) return m[a * n + b];
+  else return ld_matrix<T>(m, (size_t)a * (size_t)n + (size_t)b);
+}
+
+struct RoundsArgs {
+  int kind;  // 0 hd paper, 1 hd xor, 2 bcube
+  int rounds;
+  int b;
+  int mode;
+  double bytes[kMaxRounds];
+};
+
+struct DbtArgs {
+  const int32_t* src;
+  const int32_t* dst;
+  const int32_t* c0;
+  const int32_t* c1;
+  const int32_t* depth_off;
+  int depths;
+  int edges;
+  int mode;
+  double half;
+  double* gvals;  // global per-warp scratch when shared memory is too small
+};
+
+// Sum over rounds of the round maximum (cost_model.cpp:71-92, 118-138).
+template <typename T, bool kSmem>
+__device__ double warp_rounds_cost(const uint16_t* s_perm, int n, const T* mat, const RoundsArgs& r, double scale,
+                                   int lane) {
+  using Acc = typename MaxAcc<T>::type;
+  double total = 0.0;
+  long long stride = 1;
+  for (int rd = 0; rd < r.rounds; ++rd) {
+    Acc mx = Acc(0);
+    if (r.kind == 0) {
+      const int s = 1 << rd;
+      for (int j = lane; j < (n >> 1); j += 32)
+        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
+    } else if (r.kind == 1) {
+      const int s = 1 << rd;
+      for (int j = lane; j < n; j += 32) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+    } else {
+      const int bm1 = r.b - 1;
+      const int pairs = (n / r.b) * bm1;
+      for (int t = lane; t < pairs; t += 32) {
+        const int j = t / bm1;
+        const int k = 1 + (t - j * bm1);
+        const int dst = (int)(((long long)j + (long long)k * stride) % n);
+        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[dst]));
+      }
+      stride *= r.b;
+    }
+    mx = warp_max(mx);
+    double rm = to_double((T)mx, scale);
+    if (r.mode == RW_LATENCY_TIMES_SIZE) rm = __dmul_rn(rm, r.bytes[rd]);
+    total = __dadd_rn(total, rm);
+  }
+  return total;
+}
+
+// Double binary tree critical path (cost_model.cpp:94-116) over the
+// depth-ordered expansion; vals is per-warp scratch of `edges` doubles.
+template <typename T, bool kSmem>
+__device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d, double scale,
+                                double* vals, int lane) {
+  if (n <= 1) return 0.0;
+  for (int depth = d.depths - 1; depth >= 0; --depth) {
+    const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
+    for (int e = lo + lane; e < hi; e += 32) {
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[__ldg(d.src + e)], s_perm[__ldg(d.dst + e)]), scale);
+      if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+      const int ch = __ldg(d.c0 + e);
+      // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
+      const double sub = ch >= 0 ? ref_max(vals[ch], vals[__ldg(d.c1 + e)]) : 0.0;
+      vals[e] = __dadd_rn(c, sub);
+    }
+    __syncwarp();
+  }
+  const int top = __ldg(d.depth_off + 1);
+  double best = vals[0];
+  for (int e = 1; e < top; ++e) best = ref_max(best, vals[e]);
+  __syncwarp();
+  return best;
+}
+
+// Ring: sum of raw codes (integer for u16) -- used for exact resyncs in SA.
+template <typename T, bool kSmem>
+__device__ double warp_ring_raw(const uint16_t* s_perm, int n, const T* mat, int lane) {
+  if constexpr (std::is_same<T, uint16_t>::value) {
+    unsigned long long acc = 0;
+    for (int i = lane; i < n; i += 32) acc += mat_at<T, kSmem>(mat, n, s_perm[i], s_perm[i == 0 ? n - 1 : i - 1]);
+    return (double)warp_sum(acc);
+  } else {
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32)
+      acc = __dadd_rn(acc, (double)mat_at<T, kSmem>(mat, n, s_perm[i], s_perm[i == 0 ? n - 1 : i - 1]));
+    return warp_sum(acc);
+  }
+}
+
+}  // namespace dev
+}  // namespace rwb

@@ -1,0 +1,402 @@
+// rw_problem.cpp -- host side of the device problem object: storage choice,
+// upload, spec validation and evaluation planning.
+//
+// Reference correspondences:
+//   CostMatrix (types.hpp:42-53)          -> rwb::Problem (matrix resident in HBM)
+//   validate(CollectiveSpec) (types.cpp:143-163) -> validate_spec (same wording)
+//   check_inputs (cost_model.cpp:13-19)   -> make_plan (same wording)
+//   round_bytes (cost_model.cpp:47-51)    -> EvalPlan::round_bytes (same FP64 ops)
+//   expand_dbt (cost_model.cpp:194-222)   -> build_dbt_plan (critical-path tree)
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "rw_internal.h"
+
+namespace rwb {
+
+void cuda_check(cudaError_t e, const char* expr, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  throw Failure(RW_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                                 ") at " + file + ":" + std::to_string(line) + ": " + expr);
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  RW_CUDA(cudaGetDevice(&prev));
+  if (prev != dev) RW_CUDA(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+}
+
+// ------------------------------------------------------------ thread ctx --
+void* ThreadCtx::scratch(int slot, size_t bytes) {
+  if (d_cap[slot] < bytes) {
+    if (d_buf[slot]) {
+      RW_CUDA(cudaStreamSynchronize(stream[0]));
+      RW_CUDA(cudaStreamSynchronize(stream[1]));
+      RW_CUDA(cudaFree(d_buf[slot]));
+      d_buf[slot] = nullptr;
+    }
+    size_t cap = bytes + bytes / 2 + 256;
+    RW_CUDA(cudaMalloc(&d_buf[slot], cap));
+    d_cap[slot] = cap;
+  }
+  return d_buf[slot];
+}
+
+ThreadCtx& thread_ctx(int device) {
+  // One context per (thread, device); intentionally never torn down (CUDA
+  // objects must not be destroyed from thread-exit handlers during shutdown).
+  thread_local std::map<int, ThreadCtx*> ctxs;
+  auto it = ctxs.find(device);
+  if (it != ctxs.end()) return *it->second;
+  auto* c = new ThreadCtx();
+  c->device = device;
+  for (auto& s : c->stream) RW_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  for (auto& e : c->ev) RW_CUDA(cudaEventCreate(&e));
+  RW_CUDA(cudaMalloc(&c->d_err, 2 * sizeof(unsigned long long)));
+  const unsigned long long init[2] = {0ull, ~0ull};
+  RW_CUDA(cudaMemcpy(c->d_err, init, sizeof(init), cudaMemcpyHostToDevice));
+  RW_CUDA(cudaMallocHost(&c->h_err, 2 * sizeof(unsigned long long)));
+  ctxs[device] = c;
+  return *c;
+}
+
+void raise_order_errors(int* d_err, int* h_err, cudaStream_t st) {
+  RW_CUDA(cudaMemcpyAsync(h_err, d_err, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaStreamSynchronize(st));
+  auto* h = reinterpret_cast<unsigned long long*>(h_err);
+  if (h[0] != 0) {
+    const unsigned long long bad = h[1];
+    const unsigned long long init[2] = {0ull, ~0ull};
+    RW_CUDA(cudaMemcpyAsync(d_err, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    RW_CUDA(cudaStreamSynchronize(st));
+    throw Failure(RW_ERR_DOMAIN, "rank order is not a permutation of [0, " + std::to_string(h[0] >> 32) +
+                                     ") (batch entry " + std::to_string(bad) + ")");
+  }
+}
+
+// ---------------------------------------------------------- validation ----
+static bool is_power_of(long long n, long long base) {
+  if (base < 2 || n < 1) return false;
+  while (n % base == 0) n /= base;
+  return n == 1;
+}
+
+static int ilog_exact(long long n, long long base) {
+  int k = 0;
+  while (n > 1) {
+    n /= base;
+    ++k;
+  }
+  return k;
+}
+
+static const char* algo_name(int a) {
+  switch (a) {
+    case kRing: return "ring";
+    case kHalvingDoubling: return "hd";
+    case kDoubleBinaryTree: return "dbt";
+    case kBCube: return "bcube";
+  }
+  return "?";
+}
+
+void validate_spec(const rw_spec& s) {
+  if (s.n < 1) fail_domain("node count must be >= 1");
+  if (!(s.size_bytes > 0.0)) fail_domain("data size must be > 0");
+  if (s.algorithm < kRing || s.algorithm > kBCube) fail_domain("evaluate: unknown algorithm");
+  if (s.cost_mode != RW_LATENCY_ONLY && s.cost_mode != RW_LATENCY_TIMES_SIZE) fail_domain("unknown cost mode");
+  if (s.hd_pairing != RW_PAIRING_PAPER && s.hd_pairing != RW_PAIRING_XOR) fail_domain("unknown pairing");
+  if (s.n == 1) return;  // degenerate single-node collective
+  switch (s.algorithm) {
+    case kHalvingDoubling:
+    case kDoubleBinaryTree:
+      if (!is_power_of(s.n, 2))
+        fail_domain(std::string(algo_name(s.algorithm)) + " requires N a power of 2, got " + std::to_string(s.n));
+      break;
+    case kBCube:
+      if (s.bcube_b < 2) fail_domain("BCube group size B must be >= 2");
+      if (!is_power_of(s.n, s.bcube_b))
+        fail_domain("BCube requires N a power of B=" + std::to_string(s.bcube_b) + ", got " + std::to_string(s.n));
+      break;
+    default: break;
+  }
+}
+
+// ------------------------------------------------------------- dbt plan ---
+// Emits the transfers of both trees in the same order as the reference's
+// expansion: per depth, left edge then its subtree, then right edge.
+static void build_dbt_plan(DbtPlan& plan, int n) {
+  struct E {
+    int src, dst, parent;
+  };
+  std::vector<std::vector<E>> rounds;
+  auto alias = [n](int r) { return ((r % n) + n) % n; };
+  // explicit recursion on a small stack (depth <= log2 n + 1)
+  struct Frame {
+    int i, j, shift, depth, parent, stage, mid;
+  };
+  for (int shift : {0, -1}) {
+    std::vector<Frame> st;
+    st.push_back({0, n - 1, shift, 0, -1, 0, 0});
+    while (!st.empty()) {
+      Frame& f = st.back();
+      if (f.stage == 0) {
+        if (f.i >= f.j) {
+          st.pop_back();
+          continue;
+        }
+        if (static_cast<int>(rounds.size()) <= f.depth) rounds.resize(f.depth + 1);
+        f.mid = (f.i + f.j) / 2;
+        const int left_peer = (3 * f.i + f.j) / 2 - 1;
+        const int idx = static_cast<int>(rounds[f.depth].size());
+        rounds[f.depth].push_back({alias(f.mid + f.shift), alias(left_peer + f.shift), f.parent});
+        f.stage = 1;
+        const Frame child{f.i, f.mid - 1, f.shift, f.depth + 1, idx, 0, 0};
+        st.push_back(child);
+      } else if (f.stage == 1) {
+        const int right_peer = (f.i + 3 * f.j) / 2 + 1;
+        const int idx = static_cast<int>(rounds[f.depth].size());
+        rounds[f.depth].push_back({alias(f.mid + f.shift), alias(right_peer + f.shift), f.parent});
+        f.stage = 2;
+        const Frame child{f.mid + 1, f.j, f.shift, f.depth + 1, idx, 0, 0};
+        st.push_back(child);
+      } else {
+        st.pop_back();
+      }
+    }
+  }
+  plan.n = n;
+  plan.depths = static_cast<int>(rounds.size());
+  plan.h_depth_off.assign(plan.depths + 1, 0);
+  for (int d = 0; d < plan.depths; ++d)
+    plan.h_depth_off[d + 1] = plan.h_depth_off[d] + static_cast<int>(rounds[d].size());
+  plan.edges = plan.h_depth_off[plan.depths];
+  plan.h_src.resize(plan.edges);
+  plan.h_dst.resize(plan.edges);
+  plan.h_c0.assign(plan.edges, -1);
+  plan.h_c1.assign(plan.edges, -1);
+  for (int d = 0; d < plan.depths; ++d) {
+    for (size_t t = 0; t < rounds[d].size(); ++t) {
+      const int g = plan.h_depth_off[d] + static_cast<int>(t);
+      plan.h_src[g] = rounds[d][t].src;
+      plan.h_dst[g] = rounds[d][t].dst;
+      if (d > 0) {
+        const int parent = plan.h_depth_off[d - 1] + rounds[d][t].parent;
+        if (plan.h_c0[parent] < 0) plan.h_c0[parent] = g;
+        else plan.h_c1[parent] = g;
+      }
+    }
+  }
+  std::vector<int32_t> all;
+  all.reserve(4 * plan.edges + plan.depths + 1);
+  for (auto* v : {&plan.h_src, &plan.h_dst, &plan.h_c0, &plan.h_c1}) all.insert(all.end(), v->begin(), v->end());
+  all.insert(all.end(), plan.h_depth_off.begin(), plan.h_depth_off.end());
+  RW_CUDA(cudaMalloc(&plan.d_all, all.size() * sizeof(int32_t)));
+  RW_CUDA(cudaMemcpy(plan.d_all, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+}
+
+// ------------------------------------------------------------- planning ---
+static double round_bytes(double size_bytes, int base, int round) {
+  double divisor = 1.0;
+  for (int k = 0; k <= round; ++k) divisor *= static_cast<double>(base);
+  return size_bytes / divisor;
+}
+
+// Odd integer mantissa of a positive finite double (x = m * 2^e, m odd).
+static double odd_mantissa(double x) {
+  int e = 0;
+  double m = std::frexp(x, &e);  // x = m * 2^e, m in [0.5, 1)
+  double mi = std::ldexp(m, 53);  // exact integer < 2^53
+  while (mi != 0.0 && std::fmod(mi, 2.0) == 0.0) mi /= 2.0;
+  return mi;
+}
+
+EvalPlan make_plan(Problem& p, const rw_spec& s) {
+  validate_spec(s);
+  if (p.n != s.n)
+    fail_domain("matrix is " + std::to_string(p.n) + "x" + std::to_string(p.n) + " but spec has N=" +
+                std::to_string(s.n));
+  EvalPlan plan;
+  plan.model = s.algorithm;
+  plan.n = s.n;
+  plan.mode = s.cost_mode;
+  plan.pairing = s.hd_pairing;
+  plan.bcube_b = s.bcube_b;
+  plan.size_bytes = s.size_bytes;
+  plan.half = s.size_bytes / 2.0;
+  plan.bit_exact = true;
+  if (s.n == 1) return plan;
+  switch (s.algorithm) {
+    case kRing: {
+      const bool times = s.cost_mode == RW_LATENCY_TIMES_SIZE;
+      if (p.storage == RW_STORAGE_U16) {
+        plan.ring_int = true;
+        plan.ring_mul = times ? p.scale * s.size_bytes : p.scale;
+        // Every product and partial sum of the reference is exact when
+        // n * max_q * odd(S) < 2^53; then sum(q) * scale * S is its value.
+        const double odd = times ? odd_mantissa(s.size_bytes) : 1.0;
+        const double bound = static_cast<double>(s.n) * static_cast<double>(p.max_q) * odd;
+        plan.bit_exact = std::isfinite(plan.ring_mul) && bound < 9007199254740992.0;
+      } else {
+        plan.ring_int = false;
+        plan.ring_mul = times ? s.size_bytes : 1.0;
+        plan.bit_exact = false;
+      }
+      break;
+    }
+    case kHalvingDoubling: {
+      plan.rounds = ilog_exact(s.n, 2);
+      for (int r = 0; r < plan.rounds; ++r) plan.round_bytes[r] = round_bytes(s.size_bytes, 2, r);
+      break;
+    }
+    case kBCube: {
+      plan.rounds = ilog_exact(s.n, s.bcube_b);
+      if (plan.rounds > kMaxRounds) fail_domain("BCube round count exceeds the supported maximum");
+      for (int r = 0; r < plan.rounds; ++r) plan.round_bytes[r] = round_bytes(s.size_bytes, s.bcube_b, r);
+      break;
+    }
+    case kDoubleBinaryTree: {
+      std::lock_guard<std::mutex> lock(p.mu);
+      if (!p.dbt) {
+        DeviceGuard g(p.device);
+        auto d = std::make_unique<DbtPlan>();
+        build_dbt_plan(*d, s.n);
+        p.dbt = std::move(d);
+      }
+      plan.dbt = p.dbt.get();
+      break;
+    }
+  }
+  return plan;
+}
+
+int64_t lookups_per_eval(const EvalPlan& plan) {
+  const int64_t n = plan.n;
+  if (n <= 1) return 0;
+  switch (plan.model) {
+    case kRing: return n;
+    case kHalvingDoubling: return (plan.pairing == RW_PAIRING_PAPER ? n / 2 : n) * plan.rounds;
+    case kBCube: return (n / plan.bcube_b) * (plan.bcube_b - 1) * plan.rounds;
+    case kDoubleBinaryTree: return plan.dbt ? plan.dbt->edges : 2 * n;
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------ creation ----
+// Smallest f such that every entry is q * 2^-f with integer q (or -1).
+static int needed_frac_bits(double v) {
+  if (v == 0.0) return 0;
+  int e = 0;
+  const double m = std::frexp(v, &e);
+  double mi = std::ldexp(m, 53);
+  int tz = 0;
+  while (std::fmod(mi, 2.0) == 0.0) {
+    mi /= 2.0;
+    ++tz;
+  }
+  const int f = 53 - e - tz;
+  return f < 0 ? 0 : f;
+}
+
+static Problem* create_problem(const double* rtt, int n, int hint, int device) {
+  if (n < 1) fail_domain("cost matrix is empty");
+  if (n > 65536) fail_domain("n > 65536 is not supported (orders are stored as uint16 on the device)");
+  int ndev = 0;
+  RW_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0) RW_CUDA(cudaGetDevice(&device));
+  if (device >= ndev) fail_domain("device " + std::to_string(device) + " does not exist");
+  auto p = std::make_unique<Problem>();
+  p->n = n;
+  p->device = device;
+  const size_t nn = static_cast<size_t>(n) * static_cast<size_t>(n);
+
+  bool finite_nonneg = true, f32_exact = true, sym = true, zdiag = true;
+  int frac = 0;
+  double vmax = 0.0;
+  for (size_t k = 0; k < nn; ++k) {
+    const double v = rtt[k];
+    if (!(std::isfinite(v) && v >= 0.0) || std::signbit(v)) finite_nonneg = false;
+    if (static_cast<double>(static_cast<float>(v)) != v) f32_exact = false;
+    if (finite_nonneg) {
+      const int f = needed_frac_bits(v);
+      if (f > frac) frac = f;
+      if (v > vmax) vmax = v;
+    }
+  }
+  for (int i = 0; i < n && (sym || zdiag); ++i) {
+    if (rtt[static_cast<size_t>(i) * n + i] != 0.0) zdiag = false;
+    for (int j = i + 1; j < n && sym; ++j)
+      if (rtt[static_cast<size_t>(i) * n + j] != rtt[static_cast<size_t>(j) * n + i]) sym = false;
+  }
+  const bool u16_ok = finite_nonneg && frac <= 30 && std::ldexp(vmax, frac) <= 65535.0;
+  int storage = RW_STORAGE_F64;
+  switch (hint) {
+    case RW_STORAGE_AUTO: storage = u16_ok ? RW_STORAGE_U16 : f32_exact ? RW_STORAGE_F32 : RW_STORAGE_F64; break;
+    case RW_STORAGE_U16:
+      if (!u16_ok) fail_domain("matrix is not representable as 16-bit fixed point");
+      storage = RW_STORAGE_U16;
+      break;
+    case RW_STORAGE_F32:
+      if (!f32_exact) fail_domain("matrix is not exactly representable in FP32");
+      storage = RW_STORAGE_F32;
+      break;
+    case RW_STORAGE_F64: storage = RW_STORAGE_F64; break;
+    default: fail_domain("unknown storage hint");
+  }
+  p->storage = storage;
+  p->symmetric = sym;
+  p->zero_diag = zdiag;
+  p->max_value = vmax;
+  if (storage == RW_STORAGE_U16) {
+    p->frac_bits = frac;
+    p->scale = std::ldexp(1.0, -frac);
+  }
+
+  DeviceGuard g(device);
+  p->mat_bytes = nn * p->elem_bytes();
+  RW_CUDA(cudaMalloc(&p->d_mat, p->mat_bytes));
+  std::vector<unsigned char> staged(p->mat_bytes);
+  if (storage == RW_STORAGE_U16) {
+    auto* q = reinterpret_cast<uint16_t*>(staged.data());
+    uint32_t mq = 0;
+    for (size_t k = 0; k < nn; ++k) {
+      q[k] = static_cast<uint16_t>(std::ldexp(rtt[k], frac));
+      if (q[k] > mq) mq = q[k];
+    }
+    p->max_q = mq;
+  } else if (storage == RW_STORAGE_F32) {
+    auto* f = reinterpret_cast<float*>(staged.data());
+    for (size_t k = 0; k < nn; ++k) f[k] = static_cast<float>(rtt[k]);
+  } else {
+    std::memcpy(staged.data(), rtt, p->mat_bytes);
+  }
+  RW_CUDA(cudaMemcpy(p->d_mat, staged.data(), p->mat_bytes, cudaMemcpyHostToDevice));
+  RW_CUDA(cudaMalloc(&p->d_err, 2 * sizeof(unsigned long long)));
+  const unsigned long long init[2] = {0ull, ~0ull};
+  RW_CUDA(cudaMemcpy(p->d_err, init, sizeof(init), cudaMemcpyHostToDevice));
+  return p.release();
+}
+
+static void destroy_problem(Problem* p) {
+  if (!p) return;
+  {
+    DeviceGuard g(p->device);
+    cudaDeviceSynchronize();
+    if (p->d_mat) cudaFree(p->d_mat);
+    if (p->d_err) cudaFree(p->d_err);
+    if (p->dbt && p->dbt->d_all) cudaFree(p->dbt->d_all);
+  }
+  delete p;
+}
+
+}  // namespace rwb
+
+// Exposed to rw_capi.cpp
+namespace rwb {
+Problem* problem_create(const double* rtt, int n, int hint, int device) { return create_problem(rtt, n, hint, device); }
+void problem_destroy(Problem* p) { destroy_problem(p); }
+}  // namespace rwb

@@ -1,0 +1,31 @@
+"""The reference's own doctest suites, compiled UNCHANGED against this
+repository's drop-in C++ API (include/rankweave/*.hpp -> librankweave_b200.so).
+
+oracle/Makefile `suites` builds two binaries from proj/tests/test_cost_model.cpp,
+test_solver.cpp and test_stats.cpp with a from-scratch doctest shim:
+  _ref/suite_on_reference  -- linked with the reference library (sanity)
+  _ref/suite_on_b200       -- linked with librankweave_b200.so (GPU-backed)
+The binaries are built in the build container and travel to the GPU box.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+ON_REF = os.path.join(ROOT, "oracle", "_ref", "suite_on_reference")
+ON_B200 = os.path.join(ROOT, "oracle", "_ref", "suite_on_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(ON_REF), reason="reference suites not built")
+def test_reference_suites_pass_on_reference():
+    r = subprocess.run([ON_REF], capture_output=True, text=True, timeout=300, cwd="/tmp")
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(ON_B200), reason="reference suites not built")
+def test_reference_suites_pass_on_b200_library():
+    r = subprocess.run([ON_B200], capture_output=True, text=True, timeout=900, cwd="/tmp")
+    print(r.stdout[-2000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
