@@ -316,6 +316,9 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   const T* gmat = static_cast<const T*>(p.d_mat);
   const DevProps dp = device_props(p.device);
   const int n = plan.n;
+  // n == 1: every model costs 0 (cost_model.cpp:63,76,99,122); the ring kernel
+  // still runs the order validation.
+  const int model = n <= 1 ? kRing : plan.model;
   KArgs a{};
   a.batch = batch;
   a.n = n;
@@ -347,12 +350,12 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
 
   // per-warp shared bytes and matrix placement
   size_t per_warp = a.flag_stride;
-  if (plan.model != kRing) {
+  if (model != kRing) {
     a.perm_stride = (int)align16((size_t)n * 2);
     per_warp += a.perm_stride;
   }
   int edges = 0;
-  if (plan.model == kDoubleBinaryTree) {
+  if (model == kDoubleBinaryTree) {
     edges = plan.dbt->edges;
     a.val_stride = (int)align16((size_t)edges * 8);
   }
@@ -378,12 +381,12 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   const int64_t want = (batch + warps_per_block - 1) / warps_per_block;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)dp.sms * blocks_per_sm));
 
-  if (plan.model == kRing) {
+  if (model == kRing) {
     auto kern = smem_mat ? (validate ? k_ring<T, P, true, true> : k_ring<T, P, true, false>)
                          : (validate ? k_ring<T, P, false, true> : k_ring<T, P, false, false>);
     set_smem(kern, dyn);
     kern<<<grid, threads, dyn, st>>>(a, d_perms, gmat, plan.ring_mul, d_costs);
-  } else if (plan.model == kDoubleBinaryTree) {
+  } else if (model == kDoubleBinaryTree) {
     DbtArgs d{};
     d.src = plan.dbt->d_src();
     d.dst = plan.dbt->d_dst();

@@ -169,6 +169,26 @@ def anneal_goldens(ref: Reference):
               open(os.path.join(HERE, "anneal.json"), "w"), indent=1)
 
 
+def anneal_c4_goldens(ref: Reference, seeds=(0, 1, 2, 3)):
+    """C4 (N=1024 ring) reference anneal, full schedule (45,170,792 evaluations, ~1 h per seed)."""
+    from concurrent.futures import ThreadPoolExecutor
+    m = fixtures.config_matrix("C4", "fixed")
+    s = make_spec(0, 1024, fixtures.SIZE_FIXED, 2, 1, 0)
+
+    def run(seed):
+        t = time.time()
+        perm, cost, ev = ref.anneal(m, s, budget_s=1e6, seed=seed)
+        return {"config": "C4", "variant": "fixed", "model": "ring", "seed": seed, "n": 1024, "cost": cost,
+                "evaluations": ev, "order": perm.tolist(), "seconds": time.time() - t,
+                "identity_cost": float(ref.evaluate_batch(m, np.arange(1024, dtype=np.int32)[None, :], s)[0])}
+
+    with ThreadPoolExecutor(len(seeds)) as ex:
+        results = list(ex.map(run, seeds))
+    for r in results:
+        print("anneal C4", r["seed"], r["cost"], r["evaluations"], f"{r['seconds']:.1f}s", flush=True)
+    json.dump({"results": results, "budget_s": 1e6}, open(os.path.join(HERE, "anneal_c4.json"), "w"), indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true")
@@ -184,6 +204,8 @@ def main():
         brute_goldens(ref, a.slow)
     if "anneal" in steps:
         anneal_goldens(ref)
+    if "anneal_c4" in steps:
+        anneal_c4_goldens(ref)
 
 
 if __name__ == "__main__":
