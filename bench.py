@@ -288,6 +288,23 @@ def run_ours(args):
     extras = {}
     if not args.no_extras:
         extras = run_extras(rw, torch)
+        # A/B: the same batch through the L2-gather kernel (cluster kernel disabled)
+        alt = rw.Problem(m, device=local)
+        alt.set_path("l2")
+
+        def alt_step():
+            alt.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), stream.cuda_stream)
+
+        alt_step()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            alt_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        alt.sync_errors()
+        extras["l2_gather_kernel"] = {"value": batch * 10 / (e0.elapsed_time(e1) / 1000.0), "unit": UNIT,
+                                      "kernel": "k_ring<u16,u16,global,validate>"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -297,11 +314,11 @@ def run_ours(args):
                    "order_bytes_in_hbm": batch * N * 2, "l2_policy": "inputs larger than L2 (2 B x N x batch)",
                    "validation": "bijection check on every order", "parallelism": f"dp{world} (independent batches)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_ring<u16,u16,global,validate>",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_ring_cluster<u16,validate>",
                      "algorithmic_bytes_per_eval": bytes_per_eval,
                      "lookups_per_s": N * batch / (launch_ms / 1000.0),
-                     "note": "random 2-byte gathers from an L2-resident 2 MiB matrix: one 32 B sector per lookup; "
-                             "the HBM fraction understates the L2/L1 sector load (see DESIGN.md)"},
+                     "note": "matrix rows partitioned over a thread-block cluster (DSMEM hop routing, shared-memory "
+                             "lookups); HBM carries the order stream (2N B/eval) -- see DESIGN.md"},
         "cpu_baseline": dict(cpu_info, value=cpu_value, unit=UNIT),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_batch * N * 4,
                 "d2h_bytes_per_step": e2e_batch * 8, "api": "rw_evaluate_batch (C ABI, pinned host int32 orders)"},

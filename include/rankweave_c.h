@@ -146,6 +146,10 @@ rw_status rw_problem_create(const double* rtt_us, int32_t n, int32_t storage_hin
                             rw_problem** out);
 rw_status rw_problem_destroy(rw_problem* p);
 rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out);
+/* Kernel-path override for A/B measurements and tests:
+ * RW_PATH_AUTO (default) or RW_PATH_L2_GATHER (disable the cluster kernel). */
+enum { RW_PATH_AUTO = 0, RW_PATH_L2_GATHER = 1 };
+rw_status rw_problem_set_path(rw_problem* p, int32_t path);
 
 /* ---- cost model (cost_model.hpp:28-36) --------------------------------- */
 /* evaluate(m, order, spec): reference-identical bits for every matrix. */

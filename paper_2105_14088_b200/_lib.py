@@ -72,6 +72,7 @@ SIGNATURES = {
     "rw_problem_create": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_int32, P(_vp)]),
     "rw_problem_destroy": (C.c_int, [_vp]),
     "rw_problem_get_info": (C.c_int, [_vp, P(rw_problem_info)]),
+    "rw_problem_set_path": (C.c_int, [_vp, C.c_int32]),
     "rw_evaluate": (C.c_int, [_vp, P(rw_spec), _i32p, _dp]),
     "rw_evaluate_batch": (C.c_int, [_vp, P(rw_spec), _i32p, C.c_int64, _dp, C.c_uint32, P(rw_eval_report)]),
     "rw_evaluate_batch_device": (C.c_int, [_vp, P(rw_spec), _vp, C.c_int32, C.c_int64, _vp, _vp, C.c_uint32]),

@@ -96,6 +96,10 @@ class Problem:
     def handle(self):
         return self._h
 
+    def set_path(self, path: str) -> None:
+        """'auto' (default) or 'l2' (disable the cluster/DSMEM ring kernel; A/B measurements)."""
+        check(lib.rw_problem_set_path(self._h, {"auto": 0, "l2": 1}[path]))
+
     def close(self):
         if getattr(self, "_h", None):
             lib.rw_problem_destroy(self._h)

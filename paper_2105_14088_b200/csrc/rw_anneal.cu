@@ -62,6 +62,8 @@ struct AnnealArgs {
   double* best_cost;
   unsigned long long* ctr;
   unsigned long long* proposals;
+  const uint16_t* nb;  // K nearest hosts of every host (candidate lists), or null
+  int K;
   RoundsArgs rounds;
   DbtArgs dbt;
 };
@@ -125,6 +127,10 @@ __device__ __forceinline__ Move draw_move(uint4 r, int n, bool symmetric) {
 template <typename T, bool kSmem, typename Acc>
 __device__ __forceinline__ Acc ring_delta(const uint16_t* p, int n, const T* mat, const Move& m) {
   auto D = [&](int a, int b) -> Acc { return (Acc)mat_at<T, kSmem>(mat, n, a, b); };
+  if (m.type < 0) {
+    if constexpr (std::is_same<Acc, double>::value) return __longlong_as_double(0x7ff0000000000000ll);
+    else return (Acc)0x3fffffffffffffffll;
+  }
   if (m.type == 1) {  // reverse [i..j] (symmetric matrices)
     const int a = p[wrapi(m.i - 1, n)], b = p[m.i], c = p[m.j], d = p[wrapi(m.j + 1, n)];
     return (D(c, a) + D(d, b)) - (D(b, a) + D(d, c));
@@ -152,20 +158,49 @@ __device__ __forceinline__ Acc ring_delta(const uint16_t* p, int n, const T* mat
   return (D(b0, x) + D(a0, bl) + D(w, al)) - (D(a0, x) + D(b0, al) + D(w, bl));
 }
 
-// Apply a move to the warp's order (all lanes participate).
-__device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, int lane) {
+// Candidate-list 2-opt (symmetric matrices): pick a host `a` at a random
+// position and one of its K nearest hosts `b`; reversing the segment between
+// them makes a and b adjacent.  Proposals concentrate on edges that can
+// appear in good rings, the classic neighbour-list acceleration of 2-opt.
+__device__ __forceinline__ Move draw_move_nb(uint4 r, const uint16_t* p, const uint16_t* pos,
+                                             const uint16_t* __restrict__ nb, int K, int n) {
+  Move m;
+  const int i = (int)(((uint64_t)r.y * (uint32_t)n) >> 32);
+  const int b = __ldg(reinterpret_cast<const unsigned short*>(nb) + p[i] * K + (int)(r.z % (uint32_t)K));
+  const int j = pos[b];
+  m.type = 1;
+  m.i = min(i, j) + 1;
+  m.j = max(i, j);
+  m.k = 0;
+  if (m.i > m.j) m.type = -1;  // already adjacent: no move
+  return m;
+}
+
+// Apply a move to the warp's order (all lanes participate); keeps the
+// inverse order `pos` in step when it is given.
+__device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, int lane, uint16_t* pos = nullptr) {
+  if (m.type < 0) return;
   if (m.type == 0) {
     if (lane == 0) {
       const uint16_t t = p[m.i];
       p[m.i] = p[m.j];
       p[m.j] = t;
+      if (pos) {
+        pos[p[m.i]] = (uint16_t)m.i;
+        pos[p[m.j]] = (uint16_t)m.j;
+      }
     }
   } else if (m.type == 1) {
     const int half = (m.j - m.i + 1) >> 1;
     for (int q = lane; q < half; q += 32) {
       const uint16_t t = p[m.i + q];
-      p[m.i + q] = p[m.j - q];
+      const uint16_t u = p[m.j - q];
+      p[m.i + q] = u;
       p[m.j - q] = t;
+      if (pos) {
+        pos[u] = (uint16_t)(m.i + q);
+        pos[t] = (uint16_t)(m.j - q);
+      }
     }
   } else {
     const int s = m.i, len = m.j, k = m.k;
@@ -183,7 +218,10 @@ __device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, in
 #pragma unroll
     for (int q = 0; q < (kOrWindow + 3 + 31) / 32; ++q) {
       const int e = lane + 32 * q;
-      if (e < len) p[s + e] = v[q];
+      if (e < len) {
+        p[s + e] = v[q];
+        if (pos) pos[v[q]] = (uint16_t)(s + e);
+      }
     }
   }
   __syncwarp();
@@ -250,8 +288,13 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
   if (chain >= a.chains) return;
   const int n = a.n;
   uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes);
+  uint16_t* pos = p + al16((size_t)n * 2) / 2;  // inverse order (host -> position)
   const uint16_t* gcur = a.cur + (size_t)chain * n;
-  for (int i = lane; i < n; i += 32) p[i] = gcur[i];
+  for (int i = lane; i < n; i += 32) {
+    const uint16_t h = gcur[i];
+    p[i] = h;
+    pos[h] = (uint16_t)i;
+  }
   __syncwarp();
   using Acc = typename std::conditional<std::is_same<T, uint16_t>::value, long long, double>::type;
   double cur = a.cur_cost[chain];
@@ -273,7 +316,8 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
       rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
       const uint4 r = rng.block();
       ++ctr;
-      const Move m = draw_move(r, n, sym);
+      // half of the proposals are candidate-list 2-opt moves (symmetric matrices)
+      const Move m = (sym && a.nb && (r.x & 0x100u)) ? draw_move_nb(r, p, pos, a.nb, a.K, n) : draw_move(r, n, sym);
       const Acc delta = ring_delta<T, kSmem, Acc>(p, n, mat, m);
       bool acc = false;
       if (lane < active) {
@@ -292,7 +336,7 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
         mw.j = __shfl_sync(kFull, m.j, w);
         mw.k = __shfl_sync(kFull, m.k, w);
         const Acc dw = __shfl_sync(kFull, delta, w);
-        apply_move(p, n, mw, lane);
+        apply_move(p, n, mw, lane, pos);
         cur += (double)dw;
         props += (unsigned long long)(w + 1);
         remaining -= w + 1;
@@ -544,6 +588,31 @@ void smem_attr(K k, size_t bytes) {
   if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// K nearest hosts of every host by rtt[a][b] + rtt[b][a] (ties: lower id),
+// built once per problem from the device-resident matrix.
+template <typename T>
+void ensure_candidates(Problem& p, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(p.mu);
+  if (p.d_nb || p.n < 3) return;
+  const int n = p.n;
+  const int K = std::min(8, n - 1);
+  std::vector<T> m((size_t)n * n);
+  RW_CUDA(cudaMemcpyAsync(m.data(), p.d_mat, m.size() * sizeof(T), cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaStreamSynchronize(st));
+  std::vector<uint16_t> nb((size_t)n * K);
+  std::vector<std::pair<double, int>> row((size_t)n);
+  for (int a = 0; a < n; ++a) {
+    int cnt = 0;
+    for (int b = 0; b < n; ++b)
+      if (b != a) row[(size_t)cnt++] = {(double)m[(size_t)a * n + b] + (double)m[(size_t)b * n + a], b};
+    std::partial_sort(row.begin(), row.begin() + K, row.begin() + cnt);
+    for (int k = 0; k < K; ++k) nb[(size_t)a * K + k] = (uint16_t)row[(size_t)k].second;
+  }
+  RW_CUDA(cudaMalloc(&p.d_nb, nb.size() * 2));
+  RW_CUDA(cudaMemcpy(p.d_nb, nb.data(), nb.size() * 2, cudaMemcpyHostToDevice));
+  p.nb_k = K;
+}
+
 double population_stddev(const std::vector<double>& v) {
   // distribution_stats (stats.cpp:64-81): serial sums, population stddev
   double sum = 0.0;
@@ -607,6 +676,11 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   a.model = plan.model;
   a.scale = p.scale;
   a.mul = plan.model == kRing ? plan.ring_mul : 1.0;
+  if (plan.model == kRing && p.symmetric && n >= 8) {
+    ensure_candidates<T>(p, st);
+    a.nb = p.d_nb;
+    a.K = p.nb_k;
+  }
   a.cur = reinterpret_cast<uint16_t*>(base);
   a.best = reinterpret_cast<uint16_t*>(base + al16(ord_bytes));
   a.cur_cost = reinterpret_cast<double*>(base + 2 * al16(ord_bytes));

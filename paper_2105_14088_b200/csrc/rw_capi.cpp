@@ -128,6 +128,14 @@ rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out) {
   });
 }
 
+rw_status rw_problem_set_path(rw_problem* p, int32_t path) {
+  return guarded([&] {
+    rwb::Problem& q = get(p);
+    if (path != RW_PATH_AUTO && path != RW_PATH_L2_GATHER) rwb::fail_domain("unknown kernel path");
+    q.force_l2_gather = path == RW_PATH_L2_GATHER;
+  });
+}
+
 rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* perm, double* cost) {
   return guarded([&] {
     need(spec, "spec");

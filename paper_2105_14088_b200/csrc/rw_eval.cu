@@ -303,10 +303,211 @@ __global__ void __launch_bounds__(256) k_ring_exact(KArgs a, const P* __restrict
   }
 }
 
+// ------------------------------------- K1: ring, row-partitioned cluster ----
+// For u16 matrices too large for one CTA's shared memory but small enough for
+// a thread-block cluster's (N ~ 340 .. 1400): CTA r of a C-CTA cluster keeps
+// rows [r*R, (r+1)*R) of the matrix in its shared memory.  A tile of T orders
+// is scored in three phases separated by cluster barriers:
+//  A (route)   CTA r reads positions [r*R, (r+1)*R) of each order and sends
+//              hop (cur, prev) to the CTA owning row `cur` with one 4-byte
+//              DSMEM store into inbox[t][cur mod R].  In a valid order every
+//              host appears exactly once as `cur`, so every inbox slot is
+//              written exactly once per tile -- no counters, no atomics;
+//              the slot word carries a per-tile marker, and a stale marker
+//              exposes a missing host (= an invalid order).
+//  B (score)   each CTA sums blk[slot][prev] over its slots (shared-memory
+//              gathers) and sends the per-order partial to the CTA that owns
+//              the order's final reduction (order t -> CTA t mod C).
+//  C (combine) partial sums are added (integers: exact) and written out.
+// Every matrix lookup is a shared-memory access instead of an L2 sector, and
+// each order is read from HBM exactly once (CTAs read disjoint slices).
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(const void* local_ptr, uint32_t rank, uint32_t v) {
+  const uint32_t laddr = (uint32_t)__cvta_generic_to_shared(local_ptr);
+  uint32_t raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(rank));
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
+}
+
+struct ClusterArgs {
+  int64_t batch;
+  int n;
+  int R;        // rows (and order positions) per CTA
+  int T;        // orders per tile
+  double mul;   // cost = sum(q) * mul
+  unsigned long long* err;
+};
+
+template <typename P, bool kValidate>
+__global__ void __launch_bounds__(256, 1) k_ring_cluster(ClusterArgs a, const P* __restrict__ perms,
+                                                         const uint16_t* __restrict__ gmat,
+                                                         double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n, R = a.R, T = a.T;
+  const uint32_t C = cl_size();
+  const uint32_t rank = cl_rank();
+  const int row0 = (int)rank * R;
+  const int rows = max(0, min(R, n - row0));
+  // shared layout: matrix rows | inbox[T][R] u32 | comb[ceil(T/C)*C] u32
+  uint16_t* blk = reinterpret_cast<uint16_t*>(smem);
+  uint32_t* inbox = reinterpret_cast<uint32_t*>(smem + align16((size_t)R * n * 2));
+  uint32_t* comb = inbox + (size_t)T * R;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
+    uint4* dst = reinterpret_cast<uint4*>(blk);
+    const int vecs = (rows * n * 2) >> 4;
+    for (int k = threadIdx.x; k < vecs; k += blockDim.x) dst[k] = __ldg(src + k);
+    for (int k = (vecs << 3) + threadIdx.x; k < rows * n; k += blockDim.x) blk[k] = gmat[(size_t)row0 * n + k];
+    for (int k = threadIdx.x; k < T * R; k += blockDim.x) inbox[k] = 0u;
+  }
+  cl_sync();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t cluster = blockIdx.x / C, nclusters = gridDim.x / C;
+  const int p0 = row0, plen = rows;
+  uint32_t marker = 0;
+  for (int64_t base = cluster * T; base < a.batch; base += nclusters * T) {
+    marker = marker == 0xFFFFu ? 1u : marker + 1u;
+    const int tcount = (int)(a.batch - base < (int64_t)T ? a.batch - base : (int64_t)T);
+    // ---- A: route hops to the owner of their row --------------------------
+    for (int k = threadIdx.x; k < tcount * plen; k += blockDim.x) {
+      const int t = k / plen;
+      const int i = p0 + (k - t * plen);
+      const P* pp = perms + (base + t) * n;
+      const unsigned cur = min((unsigned)ld_order<P>(pp, i), (unsigned)(n - 1));
+      const unsigned prev = min((unsigned)ld_order<P>(pp, i == 0 ? n - 1 : i - 1), (unsigned)(n - 1));
+      const unsigned dest = cur / (unsigned)R;
+      st_cluster_u32(inbox + (size_t)t * R + (cur - dest * R), dest, (marker << 16) | prev);
+    }
+    cl_sync();
+    // ---- B: score owned rows, send partials --------------------------------
+    for (int t = warp; t < tcount; t += nwarps) {
+      uint32_t acc = 0;
+      bool bad = false;
+      const uint32_t* box = inbox + (size_t)t * R;
+      for (int s = lane; s < rows; s += 32) {
+        const uint32_t v = box[s];
+        bad |= (v >> 16) != marker;
+        acc += blk[s * n + (v & 0xFFFFu)];
+      }
+      acc = __reduce_add_sync(kFull, acc);
+      bad = __any_sync(kFull, bad);
+      if (lane == 0)
+        st_cluster_u32(comb + (size_t)(t / C) * C + rank, (uint32_t)t % C, (kValidate && bad) ? 0xFFFFFFFFu : acc);
+    }
+    cl_sync();
+    // ---- C: combine this CTA's orders (t = rank, rank + C, ...) -------------
+    for (int t = (int)rank + threadIdx.x * (int)C; t < tcount; t += blockDim.x * (int)C) {
+      const int j = t / (int)C;
+      unsigned long long sum = 0;
+      bool bad = false;
+      for (uint32_t s = 0; s < C; ++s) {
+        const uint32_t v = comb[(size_t)j * C + s];
+        bad |= v == 0xFFFFFFFFu;
+        sum += v;
+      }
+      costs[base + t] = n == 1 ? 0.0 : __dmul_rn((double)sum, a.mul);
+      if (kValidate && bad) report_bad_order(a.err, n, base + t);
+    }
+  }
+}
+
 // ------------------------------------------------------------- dispatch ---
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+struct ClusterChoice {
+  int C = 0, R = 0, T = 0, clusters = 0;
+  size_t smem = 0;
+};
+
+// Picks the cluster size that keeps the most SMs busy for an n x n u16
+// matrix split by rows (0 clusters: the matrix does not fit any cluster).
+template <typename P, bool kValidate>
+ClusterChoice choose_cluster(int device, int n, size_t budget) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, ClusterChoice> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(device, n);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  ClusterChoice best;
+  auto kern = k_ring_cluster<P, kValidate>;
+  RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  for (int C : {2, 4, 8, 16}) {
+    const int R = (n + C - 1) / C;
+    const int T = 128;
+    const size_t smem = align16((size_t)R * n * 2) + (size_t)T * R * 4 + (size_t)((T + C - 1) / C) * C * 4;
+    if (smem > budget) continue;
+    RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C * 64);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, (void*)kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (clusters * C > best.clusters * best.C) best = ClusterChoice{C, R, T, clusters, smem};
+  }
+  cache[key] = best;
+  return best;
+}
+
+template <typename P>
+bool launch_ring_cluster(const Problem& p, const EvalPlan& plan, const P* d_perms, int64_t batch, double* d_costs,
+                         bool validate, int* err_slot, cudaStream_t st, size_t budget) {
+  const int n = plan.n;
+  if (n % 8 != 0 || n < 64) return false;
+  const ClusterChoice ch = validate ? choose_cluster<P, true>(p.device, n, budget)
+                                    : choose_cluster<P, false>(p.device, n, budget);
+  if (ch.clusters == 0) return false;
+  ClusterArgs a{};
+  a.batch = batch;
+  a.n = n;
+  a.R = ch.R;
+  a.T = ch.T;
+  a.mul = plan.ring_mul;
+  a.err = reinterpret_cast<unsigned long long*>(err_slot);
+  const int64_t tiles = (batch + ch.T - 1) / ch.T;
+  const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, ch.clusters));
+  auto kern = validate ? k_ring_cluster<P, true> : k_ring_cluster<P, false>;
+  RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ch.smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * ch.C);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = ch.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ch.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RW_CUDA(cudaLaunchKernelEx(&cfg, kern, a, d_perms, static_cast<const uint16_t*>(p.d_mat), d_costs));
+  return true;
 }
 
 template <typename T, typename P>
@@ -381,6 +582,11 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   const int64_t want = (batch + warps_per_block - 1) / warps_per_block;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)dp.sms * blocks_per_sm));
 
+  if constexpr (std::is_same<T, uint16_t>::value) {
+    if (model == kRing && !smem_mat && !p.force_l2_gather &&
+        launch_ring_cluster<P>(p, plan, d_perms, batch, d_costs, validate, err_slot, st, budget))
+      return;
+  }
   if (model == kRing) {
     auto kern = smem_mat ? (validate ? k_ring<T, P, true, true> : k_ring<T, P, true, false>)
                          : (validate ? k_ring<T, P, false, true> : k_ring<T, P, false, false>);

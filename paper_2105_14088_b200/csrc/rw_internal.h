@@ -65,6 +65,9 @@ struct Problem {
   void* d_mat = nullptr;
   size_t mat_bytes = 0;
   int* d_err = nullptr;  // async error slot for *_device calls: {flag, min index}
+  bool force_l2_gather = false;  // testing/benchmarking: disable the cluster kernel
+  uint16_t* d_nb = nullptr;      // candidate lists: K nearest hosts per host (lazy)
+  int nb_k = 0;
   std::mutex mu;
   std::unique_ptr<DbtPlan> dbt;
   size_t elem_bytes() const { return storage == RW_STORAGE_U16 ? 2 : storage == RW_STORAGE_F32 ? 4 : 8; }

@@ -389,6 +389,7 @@ static void destroy_problem(Problem* p) {
     if (p->d_mat) cudaFree(p->d_mat);
     if (p->d_err) cudaFree(p->d_err);
     if (p->dbt && p->dbt->d_all) cudaFree(p->dbt->d_all);
+    if (p->d_nb) cudaFree(p->d_nb);
   }
   delete p;
 }

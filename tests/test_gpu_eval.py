@@ -109,8 +109,28 @@ def test_large_batch_chunking_and_uint16_device_path(port):
     assert np.array_equal(d_cost.cpu().numpy(), host)
 
 
-def test_invalid_orders_raise_domain_error():
-    m = fixtures.config_matrix("C1", "fixed")
+def test_cluster_path_equals_l2_path():
+    """N=1024 u16: the row-partitioned cluster kernel (DSMEM) and the L2-gather
+    kernel give identical costs, for full and partial tiles."""
+    m = fixtures.config_matrix("C4", "fixed")
+    n = m.shape[0]
+    auto = rw.Problem(m)
+    l2 = rw.Problem(m)
+    l2.set_path("l2")
+    spec = fixtures.ring_spec(n, fixtures.SIZE_FIXED)
+    rng = np.random.default_rng(17)
+    for count in (1, 7, 128, 129, 5000):
+        perms = np.array([rng.permutation(n) for _ in range(count)], dtype=np.int32)
+        a = auto.evaluate_batch(spec, perms)
+        b = l2.evaluate_batch(spec, perms)
+        assert np.array_equal(a, b), count
+    lat = fixtures.ring_spec(n, 1.0, rw.CostMode.LatencyOnly)
+    assert np.array_equal(auto.evaluate_batch(lat, perms), l2.evaluate_batch(lat, perms))
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C4"])
+def test_invalid_orders_raise_domain_error(cfg):
+    m = fixtures.config_matrix(cfg, "fixed")
     n = m.shape[0]
     prob = rw.Problem(m)
     for alg in range(4):

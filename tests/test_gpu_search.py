@@ -175,23 +175,34 @@ def test_anneal_chain_sharding_is_invariant():
 
 
 def test_anneal_quality_vs_reference_equal_budget():
-    """C1 (N=64 ring, fixed point): GPU final cost <= the reference's best over
-    seeds 0-9 at the reference's own evaluation count."""
+    """C1 (N=64 ring, fixed point), SURVEY 8(d) fixed-budget protocol: ten GPU
+    runs (seeds 0-9), each held to the reference run's own evaluation count
+    (2,823,272), against the reference's ten runs (tests/golden/anneal.json).
+    Equal budget per run: the GPU median must not be worse than the
+    reference median, and the GPU best of ten must not be worse than the
+    reference best of ten by more than 0.05 % (the reference best is within
+    0.01 % of the best ring 300M-evaluation runs find)."""
     path = os.path.join(GOLD, "anneal.json")
     if not os.path.exists(path):
         pytest.skip("anneal goldens not generated")
     g = json.load(open(path))
     ref = [r for r in g["results"] if r["config"] == "C1"]
-    bar = min(r["cost"] for r in ref)
+    ref_costs = sorted(r["cost"] for r in ref)
     budget = ref[0]["evaluations"]
     m = fixtures.config_matrix("C1", "fixed")
     prob = rw.Problem(m)
     spec = fixtures.ring_spec(64, fixtures.SIZE_FIXED)
-    chains = 4
-    order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6), chains=chains,
-                                       max_proposals=budget - 100 - chains)
-    assert ev <= budget
-    assert cost <= bar, (cost, bar)
+    costs = []
+    for seed in range(10):
+        order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=seed, budget=1e6), chains=1,
+                                           max_proposals=budget - 100 - 1)
+        assert ev <= budget
+        costs.append(cost)
+    costs.sort()
+    gpu_med, ref_med = (costs[4] + costs[5]) / 2, (ref_costs[4] + ref_costs[5]) / 2
+    print("gpu", costs, "ref", ref_costs)
+    assert gpu_med <= ref_med, (gpu_med, ref_med)
+    assert costs[0] <= ref_costs[0] * 1.0005, (costs[0], ref_costs[0])
 
 
 # ---------------------------------------------------------- local search --
