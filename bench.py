@@ -355,15 +355,18 @@ def run_extras(rw, torch):
         spec = rw.fixtures.ring_spec(64, rw.fixtures.SIZE_FIXED)
         best = None
         t = time.perf_counter()
-        for steps in (8, 32, 128, 256):
-            order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps))
-            best = (cost, steps, ev)
+        for steps in (16, 64, 256, 1024):
+            t1 = time.perf_counter()
+            order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps),
+                                               schedule="calibrated")
+            best = (cost, steps, ev, time.perf_counter() - t1, rep["chains"])
             if cost <= target:
                 break
-        out["time_to_best_ring_c1"] = {"seconds": time.perf_counter() - t, "target_reference_min_seeds0_9": target,
-                                       "reached": best[0] <= target, "cost": best[0], "steps_per_level": best[1],
-                                       "evaluations": best[2],
-                                       "reference_seconds_container": statistics.median(r["seconds"] for r in ref)}
+        out["time_to_best_ring_c1"] = {"seconds_cumulative": time.perf_counter() - t, "seconds_last_run": best[3],
+                                       "target_reference_min_seeds0_9": target, "reached": best[0] <= target,
+                                       "cost": best[0], "steps_per_level": best[1], "evaluations": best[2],
+                                       "chains": best[4],
+                                       "reference_seconds_per_run_container": statistics.median(r["seconds"] for r in ref)}
     return out
 
 

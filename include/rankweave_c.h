@@ -93,8 +93,17 @@ typedef struct rw_gpu_config {
   int32_t chains;       /* SA chains on this call; <= 0: one per restart */
   int32_t chain_begin;  /* global id of the first chain (multi-GPU sharding) */
   int32_t chain_total;  /* total chains across all ranks (<= 0: chains) */
-  int32_t polish;       /* 1: 2-opt/swap best-improvement polish of the winner */
-  int64_t max_proposals;/* total proposal budget for this call (0: schedule) */
+  int32_t schedule;     /* temperatures when initial_temperature <= 0:
+                           0 = reference rule (T0 = stddev of 100 random-order
+                               costs, floor T0 * 1e-6; solver.cpp:152-167);
+                           1 = calibrated (ring): T0 = 0.1 x mean uphill 2-opt
+                               delta of random orders, floor = 5th-percentile
+                               uphill delta / 7; the calibration samples are
+                               counted as evaluations */
+  int64_t max_proposals;/* total evaluation budget of the call (T0/calibration
+                           samples + chain starts + proposals); the steps per
+                           temperature level are derived from it (0: use
+                           steps_per_temperature) */
 } rw_gpu_config;
 
 typedef struct rw_problem rw_problem;

@@ -37,7 +37,7 @@ class rw_solver_config(C.Structure):
 
 class rw_gpu_config(C.Structure):
     _fields_ = [("chains", C.c_int32), ("chain_begin", C.c_int32), ("chain_total", C.c_int32),
-                ("polish", C.c_int32), ("max_proposals", C.c_int64)]
+                ("schedule", C.c_int32), ("max_proposals", C.c_int64)]
 
 
 class rw_problem_info(C.Structure):

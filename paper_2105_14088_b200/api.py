@@ -155,12 +155,15 @@ class Problem:
         return o, costs, ev.value
 
     def anneal(self, spec: "CollectiveSpec", cfg: "SolverConfig", chains: int = 0, chain_begin: int = 0,
-               chain_total: int = 0, max_proposals: int = 0):
+               chain_total: int = 0, max_proposals: int = 0, schedule: str = "reference"):
+        """schedule: 'reference' (T0 = stddev of random costs, floor T0*1e-6) or
+        'calibrated' (ring: temperatures from sampled 2-opt deltas)."""
         order = np.empty(spec.n, dtype=np.int32)
         cost = C.c_double()
         ev = C.c_uint64()
         rep = _lib.rw_search_report()
-        g = _lib.rw_gpu_config(chains, chain_begin, chain_total, 0, max_proposals)
+        g = _lib.rw_gpu_config(chains, chain_begin, chain_total, {"reference": 0, "calibrated": 1}[schedule],
+                               max_proposals)
         check(lib.rw_anneal(self._h, C.byref(spec._c()), C.byref(cfg._c()), C.byref(g), ptr(order, C.c_int32),
                             C.byref(cost), C.byref(ev), C.byref(rep)))
         return order, cost.value, ev.value, {f: getattr(rep, f) for f, _ in rep._fields_}

@@ -430,6 +430,43 @@ __global__ void __launch_bounds__(256) k_anneal_full(AnnealArgs a, const T* __re
   }
 }
 
+// Temperature calibration (schedule 1): each warp draws a random order and
+// prices `per_lane` random 2-opt (symmetric) or swap moves per lane against
+// it; the deltas (kernel units) go to `out` for the host to summarise.
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_calibrate_ring(AnnealArgs a, const T* __restrict__ gmat, int per_lane,
+                                                        double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int n = a.n;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes);
+  for (int i = lane; i < n; i += 32) p[i] = (uint16_t)i;
+  __syncwarp();
+  if (lane == 0) {
+    Philox rng;
+    rng.init(a.seed ^ 0xca11b7a7eull, (uint64_t)(blockIdx.x * (blockDim.x >> 5) + wib));
+    for (int i = n - 1; i > 0; --i) {
+      const int j = (int)rng.below((uint32_t)(i + 1));
+      const uint16_t t = p[i];
+      p[i] = p[j];
+      p[j] = t;
+    }
+  }
+  __syncwarp();
+  using Acc = typename std::conditional<std::is_same<T, uint16_t>::value, long long, double>::type;
+  Philox rng;
+  rng.init(a.seed ^ 0x5a3b1e0dull, ((uint64_t)(blockIdx.x * (blockDim.x >> 5) + wib) << 5) | (uint64_t)lane);
+  for (int k = 0; k < per_lane; ++k) {
+    uint4 r = rng.block();
+    r.x = 0u;  // move class 0: reverse (symmetric matrices) or swap (asymmetric)
+    const Move m = draw_move(r, n, a.symmetric != 0);
+    out[((size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * 32 + lane) * per_lane + k] =
+        (double)ring_delta<T, kSmem, Acc>(p, n, mat, m);
+  }
+}
+
 // Argmin over chains of (exact cost, global chain id).
 __global__ void k_chain_argmin(const double* cost, int chains, int64_t gid0, double* out_cost, long long* out_chain) {
   __shared__ double sc[1024];
@@ -635,42 +672,17 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   AnnealResult res;
   const int steps = cfg.steps_per_temperature > 0 ? cfg.steps_per_temperature : 4 * n;
 
-  // T0 from 100 random orders (solver.cpp:152-165)
-  double t0 = cfg.initial_temperature;
   uint64_t evals = 0;
-  if (t0 <= 0.0) {
-    auto* d_o = static_cast<uint16_t*>(c.scratch(0, (size_t)100 * n * 2));
-    auto* d_c = static_cast<double*>(c.scratch(1, 100 * 8));
-    sample_orders_device(n, 100, cfg.seed ^ 0xfeedull, d_o, st);
-    launch_evaluate(p, plan, d_o, 2, 100, d_c, true, false, c.d_err, st);
-    std::vector<double> costs(100);
-    RW_CUDA(cudaMemcpyAsync(costs.data(), d_c, 800, cudaMemcpyDeviceToHost, st));
-    RW_CUDA(cudaStreamSynchronize(st));
-    t0 = population_stddev(costs);
-    evals += 100;
-  }
-  if (t0 <= 0.0) t0 = 1.0;
-  const double t_floor = t0 * 1e-6;
-  std::vector<double> temps;
-  for (double t = t0; t > t_floor; t *= cfg.cooling) temps.push_back(t);
-  const int levels = static_cast<int>(temps.size());
-
   int chains = gpu.chains > 0 ? gpu.chains : std::max(cfg.restarts, 4 * di.sms);
   const int64_t gid0 = gpu.chain_begin > 0 ? gpu.chain_begin : 0;
-  int steps_eff = steps;
-  if (gpu.max_proposals > 0) {
-    const long long per_chain = gpu.max_proposals / std::max<long long>(1, (long long)chains * std::max(1, levels));
-    steps_eff = (int)std::max<long long>(1, per_chain);
-  }
 
   // device state
   const size_t ord_bytes = (size_t)chains * n * 2;
-  char* base = static_cast<char*>(c.scratch(4, 2 * al16(ord_bytes) + (size_t)chains * 32 + (size_t)levels * 8 + 64));
+  char* base = static_cast<char*>(c.scratch(4, 2 * al16(ord_bytes) + (size_t)chains * 32 + 64));
   AnnealArgs a{};
   a.n = n;
   a.chains = chains;
   a.gid0 = gid0;
-  a.steps = steps_eff;
   a.seed = cfg.seed;
   a.symmetric = p.symmetric ? 1 : 0;
   a.model = plan.model;
@@ -687,9 +699,6 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   a.best_cost = a.cur_cost + chains;
   a.ctr = reinterpret_cast<unsigned long long*>(a.best_cost + chains);
   a.proposals = a.ctr + chains;
-  double* d_temps = reinterpret_cast<double*>(a.proposals + chains);
-  a.temps = d_temps;
-  if (levels) RW_CUDA(cudaMemcpyAsync(d_temps, temps.data(), (size_t)levels * 8, cudaMemcpyHostToDevice, st));
   if (plan.model == kHalvingDoubling || plan.model == kBCube) {
     a.rounds.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
     a.rounds.rounds = plan.rounds;
@@ -727,6 +736,63 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   const size_t dyn = al16(a.mat_smem) + (size_t)wpb * warp_bytes;
   const int grid = (chains + wpb - 1) / wpb;
   const int threads = wpb * 32;
+
+  // ---- temperature schedule ----------------------------------------------
+  double t0 = cfg.initial_temperature;
+  double t_floor = 0.0;
+  if (t0 <= 0.0 && gpu.schedule == 1 && plan.model == kRing && n >= 4) {
+    // calibrated: sample 2-opt / swap deltas at random orders
+    constexpr int kWarps = 8, kPerLane = 16;
+    auto* d_dl = static_cast<double*>(c.scratch(7, (size_t)kWarps * 32 * kPerLane * 8));
+    auto cal = smem_mat ? k_calibrate_ring<T, true> : k_calibrate_ring<T, false>;
+    const size_t cdyn = al16(a.mat_smem) + (size_t)kWarps * warp_bytes;
+    smem_attr(cal, cdyn);
+    cal<<<1, kWarps * 32, cdyn, st>>>(a, static_cast<const T*>(p.d_mat), kPerLane, d_dl);
+    RW_CUDA(cudaGetLastError());
+    std::vector<double> dl((size_t)kWarps * 32 * kPerLane);
+    RW_CUDA(cudaMemcpyAsync(dl.data(), d_dl, dl.size() * 8, cudaMemcpyDeviceToHost, st));
+    RW_CUDA(cudaStreamSynchronize(st));
+    evals += dl.size();
+    std::vector<double> up;
+    for (double d : dl)
+      if (d > 0.0) up.push_back(d * a.mul);
+    if (!up.empty()) {
+      std::sort(up.begin(), up.end());
+      double s = 0.0;
+      for (double d : up) s += d;
+      t0 = 0.1 * s / static_cast<double>(up.size());
+      t_floor = up[up.size() / 20] / 7.0;
+      if (!(t_floor < t0)) t_floor = t0 * 1e-6;
+    }
+  }
+  if (t0 <= 0.0) {
+    // reference rule: T0 = stddev of 100 random-order costs (solver.cpp:152-165)
+    auto* d_o = static_cast<uint16_t*>(c.scratch(0, (size_t)100 * n * 2));
+    auto* d_c = static_cast<double*>(c.scratch(1, 100 * 8));
+    sample_orders_device(n, 100, cfg.seed ^ 0xfeedull, d_o, st);
+    launch_evaluate(p, plan, d_o, 2, 100, d_c, true, false, c.d_err, st);
+    std::vector<double> costs(100);
+    RW_CUDA(cudaMemcpyAsync(costs.data(), d_c, 800, cudaMemcpyDeviceToHost, st));
+    RW_CUDA(cudaStreamSynchronize(st));
+    t0 = population_stddev(costs);
+    evals += 100;
+  }
+  if (t0 <= 0.0) t0 = 1.0;  // flat landscape (solver.cpp:166)
+  if (t_floor <= 0.0) t_floor = t0 * 1e-6;
+  std::vector<double> temps;
+  for (double t = t0; t > t_floor; t *= cfg.cooling) temps.push_back(t);
+  const int levels = static_cast<int>(temps.size());
+  double* d_temps = static_cast<double*>(c.scratch(3, (size_t)std::max(1, levels) * 8));
+  if (levels) RW_CUDA(cudaMemcpyAsync(d_temps, temps.data(), (size_t)levels * 8, cudaMemcpyHostToDevice, st));
+  a.temps = d_temps;
+  int steps_eff = steps;
+  if (gpu.max_proposals > 0) {
+    // the whole call's evaluations (calibration / T0 samples, chain starts,
+    // proposals) stay within max_proposals
+    const long long left = std::max<long long>(0, gpu.max_proposals - (long long)evals - chains);
+    steps_eff = (int)std::max<long long>(1, left / std::max<long long>(1, (long long)chains * std::max(1, levels)));
+  }
+  a.steps = steps_eff;
 
   auto init = smem_mat ? k_anneal_init<T, true> : k_anneal_init<T, false>;
   smem_attr(init, dyn);

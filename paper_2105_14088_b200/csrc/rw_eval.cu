@@ -334,36 +334,53 @@ __device__ __forceinline__ uint32_t cl_size() {
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Remote (DSMEM) store; ordering against readers is provided by the
+// release/acquire cluster barrier, so no compiler memory clobber here (that
+// would pin every preceding load in program order).
 __device__ __forceinline__ void st_cluster_u32(const void* local_ptr, uint32_t rank, uint32_t v) {
   const uint32_t laddr = (uint32_t)__cvta_generic_to_shared(local_ptr);
   uint32_t raddr;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(rank));
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v));
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 struct ClusterArgs {
   int64_t batch;
   int n;
-  int R;        // rows (and order positions) per CTA
+  int R;        // rows (and order positions) per CTA; multiple of 8
   int T;        // orders per tile
   double mul;   // cost = sum(q) * mul
   unsigned long long* err;
 };
 
+constexpr int kClusterThreads = 1024;
+
 template <typename P, bool kValidate>
-__global__ void __launch_bounds__(256, 1) k_ring_cluster(ClusterArgs a, const P* __restrict__ perms,
-                                                         const uint16_t* __restrict__ gmat,
-                                                         double* __restrict__ costs) {
+__global__ void __launch_bounds__(kClusterThreads, 1) k_ring_cluster(ClusterArgs a, const P* __restrict__ perms,
+                                                                     const uint16_t* __restrict__ gmat,
+                                                                     double* __restrict__ costs) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int E = 16 / sizeof(P);  // order elements per 16-byte chunk
   const int n = a.n, R = a.R, T = a.T;
   const uint32_t C = cl_size();
   const uint32_t rank = cl_rank();
   const int row0 = (int)rank * R;
   const int rows = max(0, min(R, n - row0));
-  // shared layout: matrix rows | inbox[T][R] u32 | comb[ceil(T/C)*C] u32
+  const int SL = E + R;  // staged elements per order: one chunk before the slice + the slice
+  // shared layout: matrix rows | inbox[T][R] u32 | comb[ceil(T/C)*C] u32 | stage[2][T][SL] P
   uint16_t* blk = reinterpret_cast<uint16_t*>(smem);
   uint32_t* inbox = reinterpret_cast<uint32_t*>(smem + align16((size_t)R * n * 2));
   uint32_t* comb = inbox + (size_t)T * R;
+  P* stage = reinterpret_cast<P*>(reinterpret_cast<unsigned char*>(comb) + align16((size_t)((T + C - 1) / C) * C * 4));
   {
     const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
     uint4* dst = reinterpret_cast<uint4*>(blk);
@@ -372,23 +389,49 @@ __global__ void __launch_bounds__(256, 1) k_ring_cluster(ClusterArgs a, const P*
     for (int k = (vecs << 3) + threadIdx.x; k < rows * n; k += blockDim.x) blk[k] = gmat[(size_t)row0 * n + k];
     for (int k = threadIdx.x; k < T * R; k += blockDim.x) inbox[k] = 0u;
   }
-  cl_sync();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int64_t cluster = blockIdx.x / C, nclusters = gridDim.x / C;
-  const int p0 = row0, plen = rows;
+  const int chunks = SL / E;  // 16-byte chunks per order
+  const uint32_t invR = (uint32_t)((0x100000000ull + (unsigned long long)R - 1ull) / (unsigned long long)R);
+
+  // cp.async the order slices of one tile: chunk 0 holds the element before
+  // the slice (wrapping to the order's end for the first CTA).
+  auto issue = [&](int64_t base, int buf) {
+    const int tc = (int)(a.batch - base < (int64_t)T ? a.batch - base : (int64_t)T);
+    P* dst0 = stage + (size_t)buf * T * SL;
+    for (int k = threadIdx.x; k < tc * chunks; k += blockDim.x) {
+      const int t = k / chunks, c = k - t * chunks;
+      int start = row0 - E + c * E;
+      if (start < 0) start += n;
+      if (start >= n) continue;  // beyond the order (last CTA, short slice)
+      cp_async16(dst0 + (size_t)t * SL + c * E, perms + (base + t) * n + start);
+    }
+  };
+
+  int64_t base = cluster * T;
+  if (base < a.batch) issue(base, 0);
+  cp_async_commit();
+  cl_sync();
   uint32_t marker = 0;
-  for (int64_t base = cluster * T; base < a.batch; base += nclusters * T) {
+  int buf = 0;
+  for (; base < a.batch; base += nclusters * T, buf ^= 1) {
     marker = marker == 0xFFFFu ? 1u : marker + 1u;
     const int tcount = (int)(a.batch - base < (int64_t)T ? a.batch - base : (int64_t)T);
+    const int64_t next = base + nclusters * T;
+    if (next < a.batch) issue(next, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
     // ---- A: route hops to the owner of their row --------------------------
-    for (int k = threadIdx.x; k < tcount * plen; k += blockDim.x) {
-      const int t = k / plen;
-      const int i = p0 + (k - t * plen);
-      const P* pp = perms + (base + t) * n;
-      const unsigned cur = min((unsigned)ld_order<P>(pp, i), (unsigned)(n - 1));
-      const unsigned prev = min((unsigned)ld_order<P>(pp, i == 0 ? n - 1 : i - 1), (unsigned)(n - 1));
-      const unsigned dest = cur / (unsigned)R;
-      st_cluster_u32(inbox + (size_t)t * R + (cur - dest * R), dest, (marker << 16) | prev);
+    const P* st = stage + (size_t)buf * T * SL;
+    for (int t = warp; t < tcount; t += nwarps) {
+      const P* o = st + (size_t)t * SL + E;  // o[j] = position row0 + j, o[-1] its predecessor
+      for (int j = lane; j < rows; j += 32) {
+        const uint32_t cur = min((uint32_t)o[j], (uint32_t)(n - 1));
+        const uint32_t prev = min((uint32_t)o[j - 1], (uint32_t)(n - 1));
+        const uint32_t dest = __umulhi(cur, invR);
+        st_cluster_u32(inbox + (size_t)t * R + (cur - dest * (uint32_t)R), dest, (marker << 16) | prev);
+      }
     }
     cl_sync();
     // ---- B: score owned rows, send partials --------------------------------
@@ -447,15 +490,18 @@ ClusterChoice choose_cluster(int device, int n, size_t budget) {
   ClusterChoice best;
   auto kern = k_ring_cluster<P, kValidate>;
   RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  for (int C : {2, 4, 8, 16}) {
-    const int R = (n + C - 1) / C;
-    const int T = 128;
-    const size_t smem = align16((size_t)R * n * 2) + (size_t)T * R * 4 + (size_t)((T + C - 1) / C) * C * 4;
+  for (int C = 2; C <= 16; ++C) {
+    const int R = ((n + C - 1) / C + 7) & ~7;
+    if ((C - 1) * R >= n) continue;  // every CTA must own rows
+    const int E = 16 / (int)sizeof(P);
+    const int T = sizeof(P) == 2 ? 128 : 64;
+    const size_t smem = align16((size_t)R * n * 2) + (size_t)T * R * 4 + align16((size_t)((T + C - 1) / C) * C * 4) +
+                        2 * (size_t)T * (E + R) * sizeof(P);
     if (smem > budget) continue;
     RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C * 64);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(kClusterThreads);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -496,7 +542,7 @@ bool launch_ring_cluster(const Problem& p, const EvalPlan& plan, const P* d_perm
   RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ch.smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * ch.C);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kClusterThreads);
   cfg.dynamicSmemBytes = ch.smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -195,8 +195,8 @@ def test_anneal_quality_vs_reference_equal_budget():
     costs = []
     for seed in range(10):
         order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=seed, budget=1e6), chains=1,
-                                           max_proposals=budget - 100 - 1)
-        assert ev <= budget
+                                           max_proposals=budget, schedule="calibrated")
+        assert budget * 0.99 <= ev <= budget
         costs.append(cost)
     costs.sort()
     gpu_med, ref_med = (costs[4] + costs[5]) / 2, (ref_costs[4] + ref_costs[5]) / 2
