@@ -363,106 +363,138 @@ struct ClusterArgs {
 };
 
 constexpr int kClusterThreads = 1024;
+constexpr int kClusterRows = 64;   // matrix rows (and order positions) per CTA
+constexpr int kClusterTile = 64;   // orders per pipeline step
 
+__device__ __forceinline__ void red_cluster_add_u32(const void* local_ptr, uint32_t rank, uint32_t v) {
+  const uint32_t laddr = (uint32_t)__cvta_generic_to_shared(local_ptr);
+  uint32_t raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(rank));
+  asm volatile("red.relaxed.cluster.shared::cluster.add.u32 [%0], %1;" ::"r"(raddr), "r"(v));
+}
+
+// Pipelined: iteration i routes tile i (phase A), scores tile i-1 (phase B)
+// and combines tile i-2 (phase C), then one cluster barrier.  Every shared
+// buffer is double-buffered so a single barrier per tile orders all
+// producer/consumer pairs ("cluster ring kernel").
 template <typename P, bool kValidate>
 __global__ void __launch_bounds__(kClusterThreads, 1) k_ring_cluster(ClusterArgs a, const P* __restrict__ perms,
                                                                      const uint16_t* __restrict__ gmat,
                                                                      double* __restrict__ costs) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int E = 16 / sizeof(P);  // order elements per 16-byte chunk
-  const int n = a.n, R = a.R, T = a.T;
+  constexpr int R = kClusterRows, T = kClusterTile;
+  constexpr int SL = E + R;          // staged elements per order: pad chunk + slice
+  const int n = a.n;
   const uint32_t C = cl_size();
   const uint32_t rank = cl_rank();
   const int row0 = (int)rank * R;
-  const int rows = max(0, min(R, n - row0));
-  const int SL = E + R;  // staged elements per order: one chunk before the slice + the slice
-  // shared layout: matrix rows | inbox[T][R] u32 | comb[ceil(T/C)*C] u32 | stage[2][T][SL] P
+  // shared layout: blk[R][n] u16 | inbox[2][T][R] u32 | acc[2][T] u32 | bad[2][T] u32 | stage[2][T][SL] P
   uint16_t* blk = reinterpret_cast<uint16_t*>(smem);
   uint32_t* inbox = reinterpret_cast<uint32_t*>(smem + align16((size_t)R * n * 2));
-  uint32_t* comb = inbox + (size_t)T * R;
-  P* stage = reinterpret_cast<P*>(reinterpret_cast<unsigned char*>(comb) + align16((size_t)((T + C - 1) / C) * C * 4));
+  uint32_t* acc = inbox + 2 * T * R;
+  uint32_t* badw = acc + 2 * T;
+  P* stage = reinterpret_cast<P*>(badw + 2 * T);
   {
     const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
     uint4* dst = reinterpret_cast<uint4*>(blk);
-    const int vecs = (rows * n * 2) >> 4;
-    for (int k = threadIdx.x; k < vecs; k += blockDim.x) dst[k] = __ldg(src + k);
-    for (int k = (vecs << 3) + threadIdx.x; k < rows * n; k += blockDim.x) blk[k] = gmat[(size_t)row0 * n + k];
-    for (int k = threadIdx.x; k < T * R; k += blockDim.x) inbox[k] = 0u;
+    for (int k = threadIdx.x; k < (R * n) >> 3; k += blockDim.x) dst[k] = __ldg(src + k);
+    for (int k = threadIdx.x; k < 2 * T * R; k += blockDim.x) inbox[k] = 0u;
+    for (int k = threadIdx.x; k < 4 * T; k += blockDim.x) acc[k] = 0u;  // acc and bad
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t cluster = blockIdx.x / C, nclusters = gridDim.x / C;
-  const int chunks = SL / E;  // 16-byte chunks per order
-  const uint32_t invR = (uint32_t)((0x100000000ull + (unsigned long long)R - 1ull) / (unsigned long long)R);
+  const int64_t tiles = (a.batch + T - 1) / T;
+  const int64_t my_tiles = cluster < tiles ? (tiles - cluster + nclusters - 1) / nclusters : 0;
+  const uint32_t invC = (65536u + C - 1u) / C;  // t / C == (t * invC) >> 16 for t < 64
+  constexpr int chunks = SL / E;
 
-  // cp.async the order slices of one tile: chunk 0 holds the element before
-  // the slice (wrapping to the order's end for the first CTA).
-  auto issue = [&](int64_t base, int buf) {
-    const int tc = (int)(a.batch - base < (int64_t)T ? a.batch - base : (int64_t)T);
-    P* dst0 = stage + (size_t)buf * T * SL;
-    for (int k = threadIdx.x; k < tc * chunks; k += blockDim.x) {
-      const int t = k / chunks, c = k - t * chunks;
+  auto tile_base = [&](int64_t k) { return (cluster + k * nclusters) * T; };
+  auto tile_count = [&](int64_t base) { return (int)(a.batch - base < (int64_t)T ? a.batch - base : (int64_t)T); };
+  // cp.async the order slices of tile k: chunk 0 holds the element before the
+  // slice (wrapping to the order's end for the first CTA).
+  auto issue = [&](int64_t k) {
+    const int64_t base = tile_base(k);
+    const int tc = tile_count(base);
+    P* dst0 = stage + (size_t)(k & 1) * T * SL;
+    for (int q = threadIdx.x; q < tc * chunks; q += blockDim.x) {
+      const int t = q / chunks, c = q - t * chunks;
       int start = row0 - E + c * E;
       if (start < 0) start += n;
-      if (start >= n) continue;  // beyond the order (last CTA, short slice)
       cp_async16(dst0 + (size_t)t * SL + c * E, perms + (base + t) * n + start);
     }
   };
 
-  int64_t base = cluster * T;
-  if (base < a.batch) issue(base, 0);
+  if (my_tiles > 0) issue(0);
   cp_async_commit();
   cl_sync();
-  uint32_t marker = 0;
-  int buf = 0;
-  for (; base < a.batch; base += nclusters * T, buf ^= 1) {
-    marker = marker == 0xFFFFu ? 1u : marker + 1u;
-    const int tcount = (int)(a.batch - base < (int64_t)T ? a.batch - base : (int64_t)T);
-    const int64_t next = base + nclusters * T;
-    if (next < a.batch) issue(next, buf ^ 1);
+  for (int64_t i = 0; i < my_tiles + 2; ++i) {
+    if (i + 1 < my_tiles) issue(i + 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    // ---- A: route hops to the owner of their row --------------------------
-    const P* st = stage + (size_t)buf * T * SL;
-    for (int t = warp; t < tcount; t += nwarps) {
-      const P* o = st + (size_t)t * SL + E;  // o[j] = position row0 + j, o[-1] its predecessor
-      for (int j = lane; j < rows; j += 32) {
-        const uint32_t cur = min((uint32_t)o[j], (uint32_t)(n - 1));
-        const uint32_t prev = min((uint32_t)o[j - 1], (uint32_t)(n - 1));
-        const uint32_t dest = __umulhi(cur, invR);
-        st_cluster_u32(inbox + (size_t)t * R + (cur - dest * (uint32_t)R), dest, (marker << 16) | prev);
+    // ---- A(i): route hop (cur, prev) to inbox[i&1][t][cur & 63] of CTA cur >> 6
+    if (i < my_tiles) {
+      const int tc = tile_count(tile_base(i));
+      const uint32_t marker = ((uint32_t)i & 0x7FFFu) + 1u;
+      const P* st = stage + (size_t)(i & 1) * T * SL;
+      uint32_t* box = inbox + (size_t)(i & 1) * T * R;
+      for (int t = warp; t < tc; t += kClusterThreads / 32) {
+        const P* o = st + (size_t)t * SL + E;  // o[j]: position row0 + j; o[-1]: its predecessor
+        uint32_t lo, hi;
+        if constexpr (sizeof(P) == 2) {
+          const uint32_t w = reinterpret_cast<const uint32_t*>(o)[lane];
+          lo = w & 0xFFFFu;
+          hi = w >> 16;
+        } else {
+          const int2 w = reinterpret_cast<const int2*>(o)[lane];
+          lo = (uint32_t)w.x;
+          hi = (uint32_t)w.y;
+        }
+        uint32_t prev_lo = __shfl_up_sync(kFull, hi, 1);
+        if (lane == 0) prev_lo = (uint32_t)o[-1];
+        const uint32_t nm1 = (uint32_t)(n - 1);
+        const uint32_t c0 = min(lo, nm1), p0 = min(prev_lo, nm1);
+        const uint32_t c1 = min(hi, nm1), p1 = c0;
+        st_cluster_u32(box + t * R + (c0 & (R - 1)), c0 >> 6, (marker << 16) | p0);
+        st_cluster_u32(box + t * R + (c1 & (R - 1)), c1 >> 6, (marker << 16) | p1);
+      }
+    }
+    // ---- B(i-1): score owned rows, add partials into the order's owner CTA
+    if (i >= 1 && i - 1 < my_tiles) {
+      const int64_t k = i - 1;
+      const int tc = tile_count(tile_base(k));
+      const uint32_t marker = ((uint32_t)k & 0x7FFFu) + 1u;
+      const uint32_t* box = inbox + (size_t)(k & 1) * T * R;
+      for (int t = warp; t < tc; t += kClusterThreads / 32) {
+        const uint2 v = reinterpret_cast<const uint2*>(box + t * R)[lane];
+        const bool bad = ((v.x >> 16) != marker) | ((v.y >> 16) != marker);
+        uint32_t s = blk[(2 * lane) * n + (v.x & 0xFFFFu)];
+        s += blk[(2 * lane + 1) * n + (v.y & 0xFFFFu)];
+        s = __reduce_add_sync(kFull, s);
+        const bool any_bad = __any_sync(kFull, bad);
+        if (lane == 0) {
+          const uint32_t owner = (uint32_t)t - C * (((uint32_t)t * invC) >> 16);
+          red_cluster_add_u32(acc + (k & 1) * T + t, owner, s);
+          if (kValidate && any_bad) red_cluster_add_u32(badw + (k & 1) * T + t, owner, 1u);
+        }
+      }
+    }
+    // ---- C(i-2): owners publish costs of tile i-2 and clear the accumulators
+    if (i >= 2) {
+      const int64_t k = i - 2;
+      const int64_t base = tile_base(k);
+      const int tc = tile_count(base);
+      for (int t = (int)rank + (int)C * threadIdx.x; t < tc; t += (int)C * blockDim.x) {
+        uint32_t* ac = acc + (k & 1) * T + t;
+        uint32_t* bw = badw + (k & 1) * T + t;
+        costs[base + t] = n == 1 ? 0.0 : __dmul_rn((double)*ac, a.mul);
+        if (kValidate && *bw) report_bad_order(a.err, n, base + t);
+        *ac = 0u;
+        *bw = 0u;
       }
     }
     cl_sync();
-    // ---- B: score owned rows, send partials --------------------------------
-    for (int t = warp; t < tcount; t += nwarps) {
-      uint32_t acc = 0;
-      bool bad = false;
-      const uint32_t* box = inbox + (size_t)t * R;
-      for (int s = lane; s < rows; s += 32) {
-        const uint32_t v = box[s];
-        bad |= (v >> 16) != marker;
-        acc += blk[s * n + (v & 0xFFFFu)];
-      }
-      acc = __reduce_add_sync(kFull, acc);
-      bad = __any_sync(kFull, bad);
-      if (lane == 0)
-        st_cluster_u32(comb + (size_t)(t / C) * C + rank, (uint32_t)t % C, (kValidate && bad) ? 0xFFFFFFFFu : acc);
-    }
-    cl_sync();
-    // ---- C: combine this CTA's orders (t = rank, rank + C, ...) -------------
-    for (int t = (int)rank + threadIdx.x * (int)C; t < tcount; t += blockDim.x * (int)C) {
-      const int j = t / (int)C;
-      unsigned long long sum = 0;
-      bool bad = false;
-      for (uint32_t s = 0; s < C; ++s) {
-        const uint32_t v = comb[(size_t)j * C + s];
-        bad |= v == 0xFFFFFFFFu;
-        sum += v;
-      }
-      costs[base + t] = n == 1 ? 0.0 : __dmul_rn((double)sum, a.mul);
-      if (kValidate && bad) report_bad_order(a.err, n, base + t);
-    }
   }
 }
 
@@ -490,14 +522,16 @@ ClusterChoice choose_cluster(int device, int n, size_t budget) {
   ClusterChoice best;
   auto kern = k_ring_cluster<P, kValidate>;
   RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  for (int C = 2; C <= 16; ++C) {
-    const int R = ((n + C - 1) / C + 7) & ~7;
-    if ((C - 1) * R >= n) continue;  // every CTA must own rows
+  if (n % kClusterRows == 0 && n / kClusterRows >= 2 && n / kClusterRows <= 16) {
+    const int C = n / kClusterRows;
+    const int R = kClusterRows, T = kClusterTile;
     const int E = 16 / (int)sizeof(P);
-    const int T = sizeof(P) == 2 ? 128 : 64;
-    const size_t smem = align16((size_t)R * n * 2) + (size_t)T * R * 4 + align16((size_t)((T + C - 1) / C) * C * 4) +
+    const size_t smem = align16((size_t)R * n * 2) + 2 * (size_t)T * R * 4 + 4 * (size_t)T * 4 +
                         2 * (size_t)T * (E + R) * sizeof(P);
-    if (smem > budget) continue;
+    if (smem > budget) {
+      cache[key] = best;
+      return best;
+    }
     RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C * 64);
@@ -513,9 +547,9 @@ ClusterChoice choose_cluster(int device, int n, size_t budget) {
     int clusters = 0;
     if (cudaOccupancyMaxActiveClusters(&clusters, (void*)kern, &cfg) != cudaSuccess) {
       cudaGetLastError();
-      continue;
+      clusters = 0;
     }
-    if (clusters * C > best.clusters * best.C) best = ClusterChoice{C, R, T, clusters, smem};
+    if (clusters > 0) best = ClusterChoice{C, R, T, clusters, smem};
   }
   cache[key] = best;
   return best;
