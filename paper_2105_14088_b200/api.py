@@ -97,8 +97,8 @@ class Problem:
         return self._h
 
     def set_path(self, path: str) -> None:
-        """'auto' (default) or 'l2' (disable the cluster/DSMEM ring kernel; A/B measurements)."""
-        check(lib.rw_problem_set_path(self._h, {"auto": 0, "l2": 1}[path]))
+        """'auto' (default), 'l2' or 'cluster' (DSMEM row-partitioned ring kernel; A/B measurements)."""
+        check(lib.rw_problem_set_path(self._h, {"auto": 0, "l2": 1, "cluster": 2}[path]))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -140,6 +140,74 @@ __global__ void __launch_bounds__(1024) k_ring(KArgs a, const P* __restrict__ pe
   }
 }
 
+// Vectorised variant for uint16 orders with n % 256 == 0: each lane loads 8
+// consecutive positions with one 16-byte load per 256-position chunk, so the
+// 8 matrix lookups of a lane are independent (ILP 8) and the order costs one
+// L1 wavefront per 512 B instead of one per 64 B.
+template <typename T, bool kSmem, bool kValidate>
+__global__ void __launch_bounds__(1024) k_ring_vec(KArgs a, const uint16_t* __restrict__ perms,
+                                                   const T* __restrict__ gmat, double mul,
+                                                   double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_matrix<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint8_t* flags = smem + align16(a.mat_smem) + (size_t)wib * a.flag_stride;
+  const int n = a.n;
+  if constexpr (kValidate)
+    for (int k = lane; k < a.flag_stride; k += 32) flags[k] = 0;
+  __syncwarp();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint8_t marker = 0;
+  constexpr bool kInt = std::is_same<T, uint16_t>::value;
+  const int chunks = n >> 8;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < a.batch; b += nwarps) {
+    marker = marker == 255 ? 1 : marker + 1;
+    const uint16_t* pp = perms + b * n;
+    const uint4* pv = reinterpret_cast<const uint4*>(pp);
+    uint32_t carry = ld_order<uint16_t>(pp, n - 1);
+    unsigned long long iacc = 0;
+    double dacc = 0.0;
+    bool bad = false;
+#pragma unroll 2
+    for (int c = 0; c < chunks; ++c) {
+      const uint4 v = __ldg(pv + c * 32 + lane);
+      uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                       v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+      uint32_t prev = __shfl_up_sync(kFull, e[7], 1);
+      const uint32_t last = __shfl_sync(kFull, e[7], 31);
+      if (lane == 0) prev = carry;
+      carry = last;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t cur = e[k];
+        const uint32_t pr = k == 0 ? prev : e[k - 1];
+        if (cur < (uint32_t)n && pr < (uint32_t)n) {
+          if (kValidate) flags[cur] = marker;
+          const T val = mat_at<T, kSmem>(mat, n, (int)cur, (int)pr);
+          if constexpr (kInt) iacc += val;
+          else dacc = __dadd_rn(dacc, (double)val);
+        } else {
+          bad = true;
+        }
+      }
+    }
+    double cost;
+    if constexpr (kInt) cost = __dmul_rn((double)warp_sum(iacc), mul);
+    else cost = __dmul_rn(warp_sum(dacc), mul);
+    if constexpr (kValidate) {
+      __syncwarp();
+      bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      costs[b] = cost;
+      if (kValidate && bad) report_bad_order(a.err, n, b);
+    }
+  }
+}
+
 // Stage one order into the warp's shared buffer and mark validation flags.
 template <typename P, bool kValidate>
 __device__ __forceinline__ bool stage_order(const P* __restrict__ pp, int n, uint16_t* s_perm, uint8_t* flags,
@@ -663,9 +731,19 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)dp.sms * blocks_per_sm));
 
   if constexpr (std::is_same<T, uint16_t>::value) {
-    if (model == kRing && !smem_mat && !p.force_l2_gather &&
+    if (model == kRing && !smem_mat && p.use_cluster &&
         launch_ring_cluster<P>(p, plan, d_perms, batch, d_costs, validate, err_slot, st, budget))
       return;
+  }
+  if constexpr (std::is_same<P, uint16_t>::value) {
+    if (model == kRing && n % 256 == 0 && (reinterpret_cast<uintptr_t>(d_perms) & 15) == 0) {
+      auto kern = smem_mat ? (validate ? k_ring_vec<T, true, true> : k_ring_vec<T, true, false>)
+                           : (validate ? k_ring_vec<T, false, true> : k_ring_vec<T, false, false>);
+      set_smem(kern, dyn);
+      kern<<<grid, threads, dyn, st>>>(a, d_perms, gmat, plan.ring_mul, d_costs);
+      RW_CUDA(cudaGetLastError());
+      return;
+    }
   }
   if (model == kRing) {
     auto kern = smem_mat ? (validate ? k_ring<T, P, true, true> : k_ring<T, P, true, false>)

@@ -65,7 +65,7 @@ struct Problem {
   void* d_mat = nullptr;
   size_t mat_bytes = 0;
   int* d_err = nullptr;  // async error slot for *_device calls: {flag, min index}
-  bool force_l2_gather = false;  // testing/benchmarking: disable the cluster kernel
+  bool use_cluster = false;  // RW_PATH_CLUSTER: row-partitioned cluster ring kernel
   uint16_t* d_nb = nullptr;      // candidate lists: K nearest hosts per host (lazy)
   int nb_k = 0;
   std::mutex mu;

@@ -56,6 +56,32 @@ def test_config_goldens(cfg, kind):
             assert np.max(np.abs(fast - want) / want) < 1e-12  # what the FP64 tree sum actually achieves
 
 
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_config_goldens_uint16_device_path(cfg):
+    """uint16 orders in device memory take the vectorised ring kernel (n % 256 == 0)."""
+    import torch
+    m = fixtures.config_matrix(cfg, "fixed")
+    z = np.load(os.path.join(GOLD, f"batch_{cfg}_fixed.npz"))
+    perms = z["perms"]
+    prob = rw.Problem(m)
+    spec = spec_from(z["spec_ring"], float(z["size_ring"][0]))
+    d = torch.from_numpy(perms.astype(np.uint16).view(np.int16)).cuda()
+    c = torch.empty(perms.shape[0], dtype=torch.float64, device="cuda")
+    prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    prob.sync_errors()
+    assert np.array_equal(c.cpu().numpy(), z["cost_ring"])
+    bad = perms.copy()
+    bad[1, 7] = bad[1, 8]
+    d.copy_(torch.from_numpy(bad.astype(np.uint16).view(np.int16)))
+    prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    with pytest.raises(rw.DomainError, match="batch entry 1"):
+        prob.sync_errors()
+
+
 def test_random_small_goldens():
     """Generic FP64 (non-f32, asymmetric too) matrices, N=1..32, every model and mode."""
     z = np.load(os.path.join(GOLD, "random_small.npz"))
@@ -115,6 +141,7 @@ def test_cluster_path_equals_l2_path():
     m = fixtures.config_matrix("C4", "fixed")
     n = m.shape[0]
     auto = rw.Problem(m)
+    auto.set_path("cluster")
     l2 = rw.Problem(m)
     l2.set_path("l2")
     spec = fixtures.ring_spec(n, fixtures.SIZE_FIXED)
@@ -128,11 +155,12 @@ def test_cluster_path_equals_l2_path():
     assert np.array_equal(auto.evaluate_batch(lat, perms), l2.evaluate_batch(lat, perms))
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C4"])
-def test_invalid_orders_raise_domain_error(cfg):
+@pytest.mark.parametrize("cfg,path", [("C1", "auto"), ("C4", "auto"), ("C4", "cluster")])
+def test_invalid_orders_raise_domain_error(cfg, path):
     m = fixtures.config_matrix(cfg, "fixed")
     n = m.shape[0]
     prob = rw.Problem(m)
+    prob.set_path(path)
     for alg in range(4):
         spec = rw.CollectiveSpec(rw.Algorithm(alg), n, 1.0)
         good = np.tile(np.arange(n, dtype=np.int32), (40, 1))
