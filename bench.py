@@ -200,8 +200,8 @@ def run_ours(args):
     costs = torch.empty(batch, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def step():
-        prob.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), stream.cuda_stream)
+    def step(p=prob):
+        p.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), stream.cuda_stream)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -215,13 +215,25 @@ def run_ours(args):
         want = Port().evaluate_batch(m, rows, make_spec(0, N, rw.fixtures.SIZE_FIXED))
         assert np.array_equal(costs[:8].cpu().numpy(), want), "GPU costs differ from the oracle"
 
+    # One step (the route/score kernel pairs of every chunk) captured as a CUDA
+    # graph; the timed loop replays it.
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        cap = torch.cuda.current_stream()
+        prob.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), cap.cuda_stream)
+    graph.replay()
+    torch.cuda.synchronize()
+    prob.sync_errors()
+    chunk = max(4096, (48 << 20) // (N * 2))
+    launches_per_step = 2 * ((batch + chunk - 1) // chunk)
+
     # ---- timed region: device-resident orders (value) ----
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
     with ClockSampler(local) as clocks:
         ev[0].record(stream)
         for k in range(args.steps):
-            step()
+            graph.replay()
             ev[k + 1].record(stream)
         barrier()
     prob.sync_errors()
@@ -232,6 +244,19 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     value = world * batch * args.steps / (max_ms / 1000.0)
+
+    def time_path(path, reps=10):
+        alt = rw.Problem(m, device=local)
+        alt.set_path(path)
+        step(alt)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            step(alt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        alt.sync_errors()
+        return batch * reps / (e0.elapsed_time(e1) / 1000.0)
 
     # ---- e2e: host int32 orders through rw_evaluate_batch (H2D + D2H inside) ----
     e2e_batch = args.e2e_batch
@@ -288,23 +313,15 @@ def run_ours(args):
     extras = {}
     if not args.no_extras:
         extras = run_extras(rw, torch)
-        # A/B: the same batch through the thread-block-cluster (DSMEM routing) ring kernel
-        alt = rw.Problem(m, device=local)
-        alt.set_path("cluster")
-
-        def alt_step():
-            alt.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), stream.cuda_stream)
-
-        alt_step()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(10):
-            alt_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        alt.sync_errors()
-        extras["cluster_dsmem_kernel"] = {"value": batch * 10 / (e0.elapsed_time(e1) / 1000.0), "unit": UNIT,
-                                          "kernel": "k_ring_cluster<u16,validate> (A/B, not the default path)"}
+        # A/B: the same batch through the alternative ring kernels (not the default path)
+        extras["ring_kernel_ab"] = {
+            "unit": UNIT,
+            "transpose_default": value / world,
+            "l2_gather": time_path("l2"),
+            "cluster_dsmem": time_path("cluster"),
+            "note": "l2_gather: one warp per order, random sector gathers (L1TEX-wavefront bound); "
+                    "cluster_dsmem: rows split over a 16-CTA cluster, hops routed by DSMEM stores "
+                    "(DSMEM-transaction bound) -- DESIGN.md 4"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -314,26 +331,20 @@ def run_ours(args):
                    "order_bytes_in_hbm": batch * N * 2, "l2_policy": "inputs larger than L2 (2 B x N x batch)",
                    "validation": "bijection check on every order", "parallelism": f"dp{world} (independent batches)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "k_ring<u16,u16,global,validate>",
+                     "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "k_ring_route + k_ring_score (transpose ring path, one pair per chunk)",
                      "algorithmic_bytes_per_eval": bytes_per_eval,
                      "lookups_per_s": N * batch / (launch_ms / 1000.0),
-                     "l1tex_wavefront_bound": {
-                         "evals_per_s": 148 * 1.965e9 / (N + 2 * N // 64 + 8),
-                         "frac": None,
-                         "note": "each random 2-byte lookup into the L2-resident 2 MiB matrix costs one L1TEX "
-                                 "wavefront (a distinct 128 B line per lane); ~N+N/32+8 wavefronts per order "
-                                 "(lookups, order loads, validation) at one per cycle per SM"},
-                     "note": "the kernel is bound by L1TEX wavefronts of random gathers, not HBM bytes: the HBM "
-                             "fraction understates its load (ncu: l1tex ~96%, DRAM = algorithmic) -- DESIGN.md 4"},
+                     "note": "achieved = SURVEY 8(d) algorithmic bytes (2N order + N x 2 B lookups + 8) x evals/s "
+                             "over the step's CUDA-event time; the path streams the orders from HBM once and "
+                             "keeps its predecessor exchange buffer in L2 -- DESIGN.md 4"},
         "cpu_baseline": dict(cpu_info, value=cpu_value, unit=UNIT),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_batch * N * 4,
                 "d2h_bytes_per_step": e2e_batch * 8, "api": "rw_evaluate_batch (C ABI, pinned host int32 orders)"},
         "clocks": clock,
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * launches_per_step,
         "extras": extras,
     }
-    wb = line["roofline"]["l1tex_wavefront_bound"]
-    wb["frac"] = (batch / (launch_ms / 1000.0)) / wb["evals_per_s"]
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -155,12 +155,15 @@ rw_status rw_problem_create(const double* rtt_us, int32_t n, int32_t storage_hin
                             rw_problem** out);
 rw_status rw_problem_destroy(rw_problem* p);
 rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out);
-/* Kernel-path override for A/B measurements and tests:
- * RW_PATH_AUTO (default: L2-gather ring kernel when the matrix exceeds one
- * CTA's shared memory), RW_PATH_L2_GATHER (same, explicit) or
- * RW_PATH_CLUSTER (row-partitioned thread-block-cluster ring kernel with
- * DSMEM hop routing; u16 matrices with N = 64*C, C <= 16). */
-enum { RW_PATH_AUTO = 0, RW_PATH_L2_GATHER = 1, RW_PATH_CLUSTER = 2 };
+/* Ring kernel-path override for A/B measurements and tests, used when the
+ * matrix exceeds one CTA's shared memory:
+ *   RW_PATH_AUTO       default: RW_PATH_TRANSPOSE when supported, else L2 gather
+ *   RW_PATH_L2_GATHER  one warp per order, random gathers from the L2-resident matrix
+ *   RW_PATH_CLUSTER    row-partitioned thread-block cluster, DSMEM hop routing
+ *                      (u16 matrices, N = 64*C, C <= 16)
+ *   RW_PATH_TRANSPOSE  two passes through an L2-resident predecessor buffer;
+ *                      lookups from a shared-memory row block (N % 8 == 0, 256 <= N <= 8192) */
+enum { RW_PATH_AUTO = 0, RW_PATH_L2_GATHER = 1, RW_PATH_CLUSTER = 2, RW_PATH_TRANSPOSE = 3 };
 rw_status rw_problem_set_path(rw_problem* p, int32_t path);
 
 /* ---- cost model (cost_model.hpp:28-36) --------------------------------- */

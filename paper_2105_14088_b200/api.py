@@ -97,8 +97,9 @@ class Problem:
         return self._h
 
     def set_path(self, path: str) -> None:
-        """'auto' (default), 'l2' or 'cluster' (DSMEM row-partitioned ring kernel; A/B measurements)."""
-        check(lib.rw_problem_set_path(self._h, {"auto": 0, "l2": 1, "cluster": 2}[path]))
+        """Ring kernel path for matrices beyond one CTA's shared memory (A/B measurements):
+        'auto' (default), 'l2' (random L2 gathers), 'cluster' (DSMEM routing), 'transpose'."""
+        check(lib.rw_problem_set_path(self._h, {"auto": 0, "l2": 1, "cluster": 2, "transpose": 3}[path]))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -131,9 +131,9 @@ rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out) {
 rw_status rw_problem_set_path(rw_problem* p, int32_t path) {
   return guarded([&] {
     rwb::Problem& q = get(p);
-    if (path != RW_PATH_AUTO && path != RW_PATH_L2_GATHER && path != RW_PATH_CLUSTER)
+    if (path != RW_PATH_AUTO && path != RW_PATH_L2_GATHER && path != RW_PATH_CLUSTER && path != RW_PATH_TRANSPOSE)
       rwb::fail_domain("unknown kernel path");
-    q.use_cluster = path == RW_PATH_CLUSTER;
+    q.path = path;
   });
 }
 

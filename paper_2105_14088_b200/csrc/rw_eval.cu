@@ -731,10 +731,13 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)dp.sms * blocks_per_sm));
 
   if constexpr (std::is_same<T, uint16_t>::value) {
-    if (model == kRing && !smem_mat && p.use_cluster &&
+    if (model == kRing && !smem_mat && p.path == RW_PATH_CLUSTER &&
         launch_ring_cluster<P>(p, plan, d_perms, batch, d_costs, validate, err_slot, st, budget))
       return;
   }
+  if (model == kRing && !smem_mat && (p.path == RW_PATH_AUTO || p.path == RW_PATH_TRANSPOSE) &&
+      launch_ring_transpose(p, plan, d_perms, (int)sizeof(P), batch, d_costs, validate, err_slot, st, slot))
+    return;
   if constexpr (std::is_same<P, uint16_t>::value) {
     if (model == kRing && n % 256 == 0 && (reinterpret_cast<uintptr_t>(d_perms) & 15) == 0) {
       auto kern = smem_mat ? (validate ? k_ring_vec<T, true, true> : k_ring_vec<T, true, false>)

@@ -65,7 +65,7 @@ struct Problem {
   void* d_mat = nullptr;
   size_t mat_bytes = 0;
   int* d_err = nullptr;  // async error slot for *_device calls: {flag, min index}
-  bool use_cluster = false;  // RW_PATH_CLUSTER: row-partitioned cluster ring kernel
+  int path = RW_PATH_AUTO;   // kernel-path override (rw_problem_set_path)
   uint16_t* d_nb = nullptr;      // candidate lists: K nearest hosts per host (lazy)
   int nb_k = 0;
   std::mutex mu;
@@ -123,6 +123,11 @@ void raise_order_errors(int* d_err, int* h_err, cudaStream_t st);
 void launch_evaluate(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
                      double* d_costs, bool exact, bool validate, int* err_slot, cudaStream_t st,
                      int scratch_slot = 2);
+
+// Two-pass ring scoring through an L2-resident predecessor buffer
+// (rw_ring_transpose.cu); false when the shape is not supported.
+bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                           double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot);
 
 // Generic schedule re-costing (schedule_cost, cost_model.cpp:238-285), one order.
 double schedule_cost_device(const Problem& p, int semantics, int nrounds, const int32_t* round_offsets,

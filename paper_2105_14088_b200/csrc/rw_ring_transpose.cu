@@ -1,0 +1,264 @@
+// rw_ring_transpose.cu -- ring scoring for matrices that do not fit one CTA's
+// shared memory (N=1024 fixed point is 2 MiB, N=4096 is 32 MiB), without
+// random L2 gathers.
+//
+// The L2-gather kernel (k_ring / k_ring_vec) issues one random 2-byte load per
+// hop; each costs a full L1TEX wavefront (32 lanes hit 32 different 128-byte
+// lines), and ncu shows it at ~96% of L1TEX throughput -- one sector per cycle
+// per SM.  This path changes the access pattern instead of the kernel:
+//
+//   pass 1 (k_ring_route)  one warp per order scatters hop (cur, prev) into a
+//       shared-memory "predecessor by host" array, pred[cur] = prev, then
+//       writes it out in 16-byte chunks grouped by row block of the matrix:
+//       predbuf[block][order][row-in-block].  Every global access is
+//       coalesced; the per-chunk buffer (tens of MB) stays in the 126 MB L2.
+//       The same pass validates the order: a host that is never `cur` keeps
+//       the 0xFFFF sentinel (duplicates imply a missing host).
+//   pass 2 (k_ring_score)  a CTA holds a row block of the matrix in shared
+//       memory and scores a range of orders against it: it reads that block's
+//       predecessor slice (contiguous) and does shared-memory lookups
+//       blk[row][pred[row]].  Per-(order, block) partial sums are combined by
+//       the last-arriving CTA in block order (deterministic, exact for
+//       integer codes).
+//
+// Reference semantics: ring_cost (proj/src/cost_model.cpp:59-69), hop i =
+// rtt[perm[i]][perm[i-1]]; every host is `cur` of exactly one hop, so
+// sum over hosts h of rtt[h][pred(h)] is the same multiset of hops.
+#include <algorithm>
+#include <cmath>
+
+#include "rw_device.cuh"
+#include "rw_internal.h"
+
+namespace rwb {
+
+using namespace dev;
+
+namespace {
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct RouteArgs {
+  int64_t count;  // orders in this chunk
+  int64_t base;   // batch index of the chunk's first order (error reports)
+  int n;
+  int R;          // rows per block (multiple of 8)
+  int nblocks;
+  unsigned long long* err;
+};
+
+template <typename P, bool kValidate>
+__global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __restrict__ perms,
+                                                    uint16_t* __restrict__ pred) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint16_t* buf = reinterpret_cast<uint16_t*>(smem + (size_t)wib * al16((size_t)n * 2));
+  uint4* buf4 = reinterpret_cast<uint4*>(buf);
+  const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  const int chunks8 = n >> 3;  // n % 8 == 0 on this path
+  for (int c = lane; c < chunks8; c += 32) buf4[c] = ones;
+  __syncwarp();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < a.count; o += nwarps) {
+    const P* pp = perms + o * n;
+    bool bad = false;
+    if constexpr (sizeof(P) == 2) {
+      if ((n & 255) == 0) {
+        const uint4* pv = reinterpret_cast<const uint4*>(pp);
+        uint32_t carry = ld_order<P>(pp, n - 1);
+        for (int c = 0; c < (n >> 8); ++c) {
+          const uint4 v = __ldg(pv + c * 32 + lane);
+          const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                                 v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+          uint32_t prev = __shfl_up_sync(kFull, e[7], 1);
+          const uint32_t last = __shfl_sync(kFull, e[7], 31);
+          if (lane == 0) prev = carry;
+          carry = last;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t cur = e[k];
+            if (cur < (uint32_t)n) buf[cur] = (uint16_t)(k == 0 ? prev : e[k - 1]);
+            else bad = true;
+          }
+        }
+      } else {
+        for (int i = lane; i < n; i += 32) {
+          const uint32_t cur = (uint32_t)ld_order<P>(pp, i);
+          const uint32_t prev = (uint32_t)ld_order<P>(pp, i == 0 ? n - 1 : i - 1);
+          if (cur < (uint32_t)n) buf[cur] = (uint16_t)prev;
+          else bad = true;
+        }
+      }
+    } else {
+      for (int i = lane; i < n; i += 32) {
+        const uint32_t cur = (uint32_t)ld_order<P>(pp, i);
+        const uint32_t prev = (uint32_t)ld_order<P>(pp, i == 0 ? n - 1 : i - 1);
+        if (cur < (uint32_t)n && prev < (uint32_t)n) buf[cur] = (uint16_t)prev;
+        else bad = true;
+      }
+    }
+    __syncwarp();
+    // write pred by row block (16-byte chunks), check the sentinel, reset
+    for (int c = lane; c < chunks8; c += 32) {
+      const uint4 v = buf4[c];
+      const int h0 = c << 3;
+      const int b = h0 / a.R;
+      const int s0 = h0 - b * a.R;
+      *reinterpret_cast<uint4*>(pred + ((size_t)b * a.count + o) * a.R + s0) = v;
+      if (kValidate) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bad |= (w[k] & 0xFFFFu) == 0xFFFFu || (w[k] >> 16) == 0xFFFFu;
+      }
+      buf4[c] = ones;
+    }
+    __syncwarp();
+    if (kValidate && __any_sync(kFull, bad) && lane == 0) report_bad_order(a.err, n, a.base + o);
+  }
+}
+
+struct ScoreArgs {
+  int64_t count;
+  int n;
+  int R;
+  int nblocks;
+  double mul;      // final multiplier (ring_mul)
+  double* costs;   // chunk-relative output
+};
+
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint16_t* __restrict__ pred,
+                                                        const T* __restrict__ gmat, double* __restrict__ part,
+                                                        unsigned int* __restrict__ cnt) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* blk = reinterpret_cast<T*>(smem);
+  const int n = a.n, R = a.R, nb = a.nblocks;
+  const int G = gridDim.x;
+  // CTA -> (row block, order range); consecutive CTAs share a block
+  const int b = (int)(((int64_t)blockIdx.x * nb) / G);
+  int first = 0;
+  while (((int64_t)(first)*nb) / G < b) ++first;  // first CTA of block b
+  int last = first;
+  while (last + 1 < G && ((int64_t)(last + 1) * nb) / G == b) ++last;
+  const int cpb = last - first + 1, j = (int)blockIdx.x - first;
+  const int64_t o0 = a.count * j / cpb, o1 = a.count * (j + 1) / cpb;
+  const int row0 = b * R;
+  const int rows = min(R, n - row0);
+  {
+    const size_t bytes = (size_t)rows * n * sizeof(T);
+    const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
+    uint4* dst = reinterpret_cast<uint4*>(blk);
+    for (size_t k = threadIdx.x; k < (bytes >> 4); k += blockDim.x) dst[k] = __ldg(src + k);
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  constexpr bool kInt = std::is_same<T, uint16_t>::value;
+  const uint32_t nm1 = (uint32_t)(n - 1);
+  for (int64_t o = o0 + warp; o < o1; o += nwarps) {
+    const uint16_t* src = pred + ((size_t)b * a.count + o) * R;
+    unsigned long long iacc = 0;
+    double dacc = 0.0;
+    for (int s = 2 * lane; s < rows; s += 64) {  // R % 8 == 0: pairs never straddle
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
+      const uint32_t p0 = min(w & 0xFFFFu, nm1), p1 = min(w >> 16, nm1);
+      const T v0 = blk[s * n + p0];
+      const T v1 = blk[(s + 1) * n + p1];
+      if constexpr (kInt) iacc += (unsigned long long)v0 + v1;
+      else dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
+    }
+    double partial;
+    if constexpr (kInt) partial = (double)warp_sum(iacc);  // < 2^53: exact
+    else partial = warp_sum(dacc);
+    if (lane == 0) {
+      part[o * nb + b] = partial;
+      __threadfence();
+      const unsigned prev = atomicAdd(cnt + o, 1u);
+      if (prev == (unsigned)(nb - 1)) {  // last block of this order: combine in block order
+        __threadfence();
+        const volatile double* pv = part + o * nb;
+        double sum = 0.0;
+        for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, pv[k]);
+        a.costs[o] = __dmul_rn(sum, a.mul);
+        cnt[o] = 0u;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                           double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot) {
+  const int n = plan.n;
+  if (n % 8 != 0 || n < 256 || n > 8192 || batch <= 0) return false;
+  int sms = 148, optin = 227 * 1024;
+  RW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+  RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
+  const size_t budget = (size_t)std::min(optin, 227 * 1024) - 1024;
+  const size_t esz = p.elem_bytes();
+  int rmax = (int)(budget / ((size_t)n * esz)) & ~7;
+  if (rmax < 8) return false;
+  const int nblocks = (n + rmax - 1) / rmax;
+  const int R = ((n + nblocks - 1) / nblocks + 7) & ~7;
+  if (nblocks > sms) return false;
+  // chunk so the predecessor buffer (~2n bytes per order) stays L2-resident
+  const int64_t chunk = std::max<int64_t>(4096, ((int64_t)48 << 20) / ((int64_t)n * 2));
+  ThreadCtx& c = thread_ctx(p.device);
+  const int64_t kmax = std::min(batch, chunk);
+  uint16_t* predbuf = static_cast<uint16_t*>(c.scratch(slot, (size_t)nblocks * kmax * R * 2));
+  char* aux = static_cast<char*>(c.scratch(slot + 1, (size_t)kmax * nblocks * 8 + (size_t)kmax * 4 + 64));
+  double* part = reinterpret_cast<double*>(aux);
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(aux + al16((size_t)kmax * nblocks * 8));
+  RW_CUDA(cudaMemsetAsync(cnt, 0, (size_t)kmax * 4, st));
+
+  const size_t route_smem = 8 * al16((size_t)n * 2);
+  const size_t score_smem = al16((size_t)R * n * esz);
+  auto set = [](auto kern, size_t bytes) {
+    if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  };
+  for (int64_t off = 0; off < batch; off += kmax) {
+    const int64_t cnt_o = std::min(kmax, batch - off);
+    RouteArgs ra{cnt_o, off, n, R, nblocks, reinterpret_cast<unsigned long long*>(err_slot)};
+    const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt_o + 7) / 8, (int64_t)sms * 8));
+    if (perm_bytes == 2) {
+      auto k = validate ? k_ring_route<uint16_t, true> : k_ring_route<uint16_t, false>;
+      set(k, route_smem);
+      k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const uint16_t*>(d_perms) + off * n, predbuf);
+    } else {
+      auto k = validate ? k_ring_route<int32_t, true> : k_ring_route<int32_t, false>;
+      set(k, route_smem);
+      k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
+    }
+    RW_CUDA(cudaGetLastError());
+    ScoreArgs sa{cnt_o, n, R, nblocks, plan.ring_mul, d_costs + off};
+    const int sgrid = (int)std::min<int64_t>(sms, std::max<int64_t>(nblocks, cnt_o / 256 * nblocks));
+    switch (p.storage) {
+      case RW_STORAGE_U16: {
+        auto k = k_ring_score<uint16_t>;
+        set(k, score_smem);
+        k<<<std::max(sgrid, nblocks), 1024, score_smem, st>>>(sa, predbuf, static_cast<const uint16_t*>(p.d_mat),
+                                                               part, cnt);
+        break;
+      }
+      case RW_STORAGE_F32: {
+        auto k = k_ring_score<float>;
+        set(k, score_smem);
+        k<<<std::max(sgrid, nblocks), 1024, score_smem, st>>>(sa, predbuf, static_cast<const float*>(p.d_mat),
+                                                               part, cnt);
+        break;
+      }
+      default: {
+        auto k = k_ring_score<double>;
+        set(k, score_smem);
+        k<<<std::max(sgrid, nblocks), 1024, score_smem, st>>>(sa, predbuf, static_cast<const double*>(p.d_mat),
+                                                               part, cnt);
+        break;
+      }
+    }
+    RW_CUDA(cudaGetLastError());
+  }
+  return true;
+}
+
+}  // namespace rwb

@@ -135,27 +135,46 @@ def test_large_batch_chunking_and_uint16_device_path(port):
     assert np.array_equal(d_cost.cpu().numpy(), host)
 
 
-def test_cluster_path_equals_l2_path():
-    """N=1024 u16: the row-partitioned cluster kernel (DSMEM) and the L2-gather
-    kernel give identical costs, for full and partial tiles."""
-    m = fixtures.config_matrix("C4", "fixed")
+@pytest.mark.parametrize("cfg,kind", [("C4", "fixed"), ("C4", "f32"), ("C5", "fixed")])
+def test_ring_paths_agree(cfg, kind):
+    """Matrices beyond one CTA's shared memory: the L2-gather, transpose and
+    (u16, N=1024) cluster kernels give identical costs on full and partial
+    chunks, through int32 host orders and uint16 device orders."""
+    import torch
+    m = fixtures.config_matrix(cfg, kind)
     n = m.shape[0]
-    auto = rw.Problem(m)
-    auto.set_path("cluster")
-    l2 = rw.Problem(m)
-    l2.set_path("l2")
-    spec = fixtures.ring_spec(n, fixtures.SIZE_FIXED)
+    paths = ["l2", "transpose"] + (["cluster"] if (kind == "fixed" and n == 1024) else [])
+    probs = {}
+    for pth in paths:
+        probs[pth] = rw.Problem(m)
+        probs[pth].set_path(pth)
+    spec = fixtures.ring_spec(n, fixtures.size_for(kind))
     rng = np.random.default_rng(17)
-    for count in (1, 7, 128, 129, 5000):
+    for count in (1, 7, 129, 3000):
         perms = np.array([rng.permutation(n) for _ in range(count)], dtype=np.int32)
-        a = auto.evaluate_batch(spec, perms)
-        b = l2.evaluate_batch(spec, perms)
-        assert np.array_equal(a, b), count
+        ref = probs["l2"].evaluate_batch(spec, perms)
+        for pth in paths[1:]:
+            got = probs[pth].evaluate_batch(spec, perms)
+            if kind == "fixed":
+                assert np.array_equal(got, ref), (pth, count)
+            else:
+                np.testing.assert_allclose(got, ref, rtol=1e-12, atol=0)
+        d = torch.from_numpy(perms.astype(np.uint16).view(np.int16)).cuda()
+        c = torch.empty(count, dtype=torch.float64, device="cuda")
+        for pth in paths:
+            probs[pth].evaluate_batch_device(spec, d.data_ptr(), 2, count, c.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            probs[pth].sync_errors()
+            if kind == "fixed":
+                assert np.array_equal(c.cpu().numpy(), ref), (pth, count, "u16")
     lat = fixtures.ring_spec(n, 1.0, rw.CostMode.LatencyOnly)
-    assert np.array_equal(auto.evaluate_batch(lat, perms), l2.evaluate_batch(lat, perms))
+    want = probs["l2"].evaluate_batch(lat, perms)
+    for pth in paths[1:]:
+        np.testing.assert_allclose(probs[pth].evaluate_batch(lat, perms), want, rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("cfg,path", [("C1", "auto"), ("C4", "auto"), ("C4", "cluster")])
+@pytest.mark.parametrize("cfg,path", [("C1", "auto"), ("C4", "auto"), ("C4", "cluster"), ("C4", "l2")])
 def test_invalid_orders_raise_domain_error(cfg, path):
     m = fixtures.config_matrix(cfg, "fixed")
     n = m.shape[0]
