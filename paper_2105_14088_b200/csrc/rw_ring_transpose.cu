@@ -119,70 +119,130 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
 }
 
 struct ScoreArgs {
-  int64_t count;
+  int64_t count;   // orders in this chunk
   int n;
-  int R;
+  int R;           // rows per block
   int nblocks;
-  double mul;      // final multiplier (ring_mul)
-  double* costs;   // chunk-relative output
+  int cpb;         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
+  double* part;    // [count][nblocks] partial sums
 };
 
+constexpr int kStageOrders = 128;  // orders per TMA bulk stage
+constexpr int kStages = 4;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared (1D, 16-byte multiple), completion on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+// Pass 2: a CTA keeps rows [b*R, b*R + rows) in shared memory and streams the
+// block's predecessor slices (contiguous in predbuf) through a 4-stage TMA
+// bulk-copy ring; each warp scores one order per step with shared-memory
+// lookups and writes the (order, block) partial.
 template <typename T>
 __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint16_t* __restrict__ pred,
-                                                        const T* __restrict__ gmat, double* __restrict__ part,
-                                                        unsigned int* __restrict__ cnt) {
+                                                        const T* __restrict__ gmat) {
   extern __shared__ __align__(16) unsigned char smem[];
-  T* blk = reinterpret_cast<T*>(smem);
   const int n = a.n, R = a.R, nb = a.nblocks;
-  const int G = gridDim.x;
-  // CTA -> (row block, order range); consecutive CTAs share a block
-  const int b = (int)(((int64_t)blockIdx.x * nb) / G);
-  int first = 0;
-  while (((int64_t)(first)*nb) / G < b) ++first;  // first CTA of block b
-  int last = first;
-  while (last + 1 < G && ((int64_t)(last + 1) * nb) / G == b) ++last;
-  const int cpb = last - first + 1, j = (int)blockIdx.x - first;
-  const int64_t o0 = a.count * j / cpb, o1 = a.count * (j + 1) / cpb;
-  const int row0 = b * R;
-  const int rows = min(R, n - row0);
-  {
-    const size_t bytes = (size_t)rows * n * sizeof(T);
-    const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
-    uint4* dst = reinterpret_cast<uint4*>(blk);
-    for (size_t k = threadIdx.x; k < (bytes >> 4); k += blockDim.x) dst[k] = __ldg(src + k);
-    __syncthreads();
-  }
+  T* blk = reinterpret_cast<T*>(smem);
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + al16((size_t)R * n * sizeof(T)));
+  __shared__ __align__(8) uint64_t bars[kStages];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  constexpr bool kInt = std::is_same<T, uint16_t>::value;
   const uint32_t nm1 = (uint32_t)(n - 1);
-  for (int64_t o = o0 + warp; o < o1; o += nwarps) {
-    const uint16_t* src = pred + ((size_t)b * a.count + o) * R;
-    unsigned long long iacc = 0;
-    double dacc = 0.0;
-    for (int s = 2 * lane; s < rows; s += 64) {  // R % 8 == 0: pairs never straddle
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
-      const uint32_t p0 = min(w & 0xFFFFu, nm1), p1 = min(w >> 16, nm1);
-      const T v0 = blk[s * n + p0];
-      const T v1 = blk[(s + 1) * n + p1];
-      if constexpr (kInt) iacc += (unsigned long long)v0 + v1;
-      else dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
+  constexpr bool kInt = std::is_same<T, uint16_t>::value;
+  const size_t stage_elems = (size_t)kStageOrders * R;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+  __syncthreads();
+  unsigned phase_bits = 0;  // parity per stage slot
+
+  // work items: (block, order range)
+  const int items = a.cpb > 0 ? nb * a.cpb : nb;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = a.cpb > 0 ? item / a.cpb : item;
+    const int j = a.cpb > 0 ? item % a.cpb : 0;
+    const int parts = a.cpb > 0 ? a.cpb : 1;
+    const int64_t o0 = a.count * j / parts, o1 = a.count * (j + 1) / parts;
+    const int row0 = b * R;
+    const int rows = min(R, n - row0);
+    __syncthreads();  // previous item fully consumed
+    {
+      const size_t bytes = (size_t)rows * n * sizeof(T);
+      const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
+      uint4* dst = reinterpret_cast<uint4*>(blk);
+      for (size_t k = threadIdx.x; k < (bytes >> 4); k += blockDim.x) dst[k] = __ldg(src + k);
     }
-    double partial;
-    if constexpr (kInt) partial = (double)warp_sum(iacc);  // < 2^53: exact
-    else partial = warp_sum(dacc);
-    if (lane == 0) {
-      part[o * nb + b] = partial;
-      __threadfence();
-      const unsigned prev = atomicAdd(cnt + o, 1u);
-      if (prev == (unsigned)(nb - 1)) {  // last block of this order: combine in block order
-        __threadfence();
-        const volatile double* pv = part + o * nb;
-        double sum = 0.0;
-        for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, pv[k]);
-        a.costs[o] = __dmul_rn(sum, a.mul);
-        cnt[o] = 0u;
+    const uint16_t* base = pred + ((size_t)b * a.count + o0) * R;
+    const int64_t total = o1 - o0;
+    const int64_t nstage = (total + kStageOrders - 1) / kStageOrders;
+    auto issue = [&](int64_t st) {
+      const int slot = (int)(st % kStages);
+      const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
+      const unsigned bytes = (unsigned)(cnt * R * 2);
+      mbar_expect_tx(&bars[slot], bytes);
+      bulk_g2s(ring + slot * stage_elems, base + (size_t)st * stage_elems, bytes, &bars[slot]);
+    };
+    if (threadIdx.x == 0)
+      for (int64_t st = 0; st < nstage && st < kStages; ++st) issue(st);
+    __syncthreads();  // matrix rows staged
+    for (int64_t st = 0; st < nstage; ++st) {
+      const int slot = (int)(st % kStages);
+      mbar_wait(&bars[slot], (phase_bits >> slot) & 1u);
+      const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
+      const uint16_t* sp = ring + slot * stage_elems;
+      for (int k = warp; k < cnt; k += nwarps) {
+        const uint16_t* src = sp + (size_t)k * R;
+        unsigned long long iacc = 0;
+        double dacc = 0.0;
+        for (int s = 2 * lane; s < rows; s += 64) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
+          const uint32_t p0 = min(w & 0xFFFFu, nm1), p1 = min(w >> 16, nm1);
+          const T v0 = blk[s * n + p0];
+          const T v1 = blk[(s + 1) * n + p1];
+          if constexpr (kInt) iacc += (unsigned long long)v0 + v1;
+          else dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
+        }
+        double partial;
+        if constexpr (kInt) partial = (double)warp_sum(iacc);  // < 2^53: exact
+        else partial = warp_sum(dacc);
+        if (lane == 0) a.part[(o0 + st * kStageOrders + k) * nb + b] = partial;
       }
+      phase_bits ^= 1u << slot;
+      __syncthreads();  // slot consumed
+      if (threadIdx.x == 0 && st + kStages < nstage) issue(st + kStages);
     }
+  }
+}
+
+// Pass 3: cost[o] = (sum of the order's block partials, in block order) * mul.
+__global__ void k_ring_combine(const double* __restrict__ part, int64_t count, int nb, double mul,
+                               double* __restrict__ costs) {
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < count; o += (int64_t)gridDim.x * blockDim.x) {
+    double sum = 0.0;
+    for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, part[o * nb + k]);
+    costs[o] = __dmul_rn(sum, mul);
   }
 }
 
@@ -195,28 +255,40 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   int sms = 148, optin = 227 * 1024;
   RW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
   RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
-  const size_t budget = (size_t)std::min(optin, 227 * 1024) - 1024;
+  const size_t budget = (size_t)std::min(optin, 227 * 1024) - 2048;
   const size_t esz = p.elem_bytes();
-  int rmax = (int)(budget / ((size_t)n * esz)) & ~7;
-  if (rmax < 8) return false;
-  const int nblocks = (n + rmax - 1) / rmax;
-  const int R = ((n + nblocks - 1) / nblocks + 7) & ~7;
-  if (nblocks > sms) return false;
+  auto fits = [&](int R) {
+    return al16((size_t)R * n * esz) + (size_t)kStages * kStageOrders * R * 2 <= budget;
+  };
+  // row blocks: prefer an exact split of n into multiples of 8 rows
+  int nblocks = 0, R = 0;
+  for (int nb = 1; nb <= n / 8 && !nblocks; ++nb) {
+    const int r = ((n + nb - 1) / nb + 7) & ~7;
+    if (!fits(r)) continue;
+    int best_nb = nb;
+    for (int e = nb; e <= 4 * nb && e <= n / 8; ++e)
+      if (n % e == 0 && (n / e) % 8 == 0 && fits(n / e)) {
+        best_nb = e;
+        break;
+      }
+    nblocks = best_nb;
+    R = ((n + nblocks - 1) / nblocks + 7) & ~7;
+  }
+  if (!nblocks) return false;
   // chunk so the predecessor buffer (~2n bytes per order) stays L2-resident
   const int64_t chunk = std::max<int64_t>(4096, ((int64_t)48 << 20) / ((int64_t)n * 2));
   ThreadCtx& c = thread_ctx(p.device);
   const int64_t kmax = std::min(batch, chunk);
   uint16_t* predbuf = static_cast<uint16_t*>(c.scratch(slot, (size_t)nblocks * kmax * R * 2));
-  char* aux = static_cast<char*>(c.scratch(slot + 1, (size_t)kmax * nblocks * 8 + (size_t)kmax * 4 + 64));
-  double* part = reinterpret_cast<double*>(aux);
-  unsigned int* cnt = reinterpret_cast<unsigned int*>(aux + al16((size_t)kmax * nblocks * 8));
-  RW_CUDA(cudaMemsetAsync(cnt, 0, (size_t)kmax * 4, st));
+  double* part = static_cast<double*>(c.scratch(slot + 1, (size_t)kmax * nblocks * 8 + 64));
 
   const size_t route_smem = 8 * al16((size_t)n * 2);
-  const size_t score_smem = al16((size_t)R * n * esz);
+  const size_t score_smem = al16((size_t)R * n * esz) + (size_t)kStages * kStageOrders * R * 2;
   auto set = [](auto kern, size_t bytes) {
     if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   };
+  const int cpb = nblocks <= sms ? sms / nblocks : 0;
+  const int sgrid = cpb > 0 ? nblocks * cpb : sms;
   for (int64_t off = 0; off < batch; off += kmax) {
     const int64_t cnt_o = std::min(kmax, batch - off);
     RouteArgs ra{cnt_o, off, n, R, nblocks, reinterpret_cast<unsigned long long*>(err_slot)};
@@ -231,31 +303,30 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
-    ScoreArgs sa{cnt_o, n, R, nblocks, plan.ring_mul, d_costs + off};
-    const int sgrid = (int)std::min<int64_t>(sms, std::max<int64_t>(nblocks, cnt_o / 256 * nblocks));
+    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, part};
     switch (p.storage) {
       case RW_STORAGE_U16: {
         auto k = k_ring_score<uint16_t>;
         set(k, score_smem);
-        k<<<std::max(sgrid, nblocks), 1024, score_smem, st>>>(sa, predbuf, static_cast<const uint16_t*>(p.d_mat),
-                                                               part, cnt);
+        k<<<sgrid, 1024, score_smem, st>>>(sa, predbuf, static_cast<const uint16_t*>(p.d_mat));
         break;
       }
       case RW_STORAGE_F32: {
         auto k = k_ring_score<float>;
         set(k, score_smem);
-        k<<<std::max(sgrid, nblocks), 1024, score_smem, st>>>(sa, predbuf, static_cast<const float*>(p.d_mat),
-                                                               part, cnt);
+        k<<<sgrid, 1024, score_smem, st>>>(sa, predbuf, static_cast<const float*>(p.d_mat));
         break;
       }
       default: {
         auto k = k_ring_score<double>;
         set(k, score_smem);
-        k<<<std::max(sgrid, nblocks), 1024, score_smem, st>>>(sa, predbuf, static_cast<const double*>(p.d_mat),
-                                                               part, cnt);
+        k<<<sgrid, 1024, score_smem, st>>>(sa, predbuf, static_cast<const double*>(p.d_mat));
         break;
       }
     }
+    RW_CUDA(cudaGetLastError());
+    k_ring_combine<<<(int)std::min<int64_t>((cnt_o + 255) / 256, (int64_t)sms * 8), 256, 0, st>>>(
+        part, cnt_o, nblocks, plan.ring_mul, d_costs + off);
     RW_CUDA(cudaGetLastError());
   }
   return true;
