@@ -212,22 +212,31 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
       mbar_wait(&bars[slot], (phase_bits >> slot) & 1u);
       const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
       const uint16_t* sp = ring + slot * stage_elems;
-      for (int k = warp; k < cnt; k += nwarps) {
-        const uint16_t* src = sp + (size_t)k * R;
-        unsigned long long iacc = 0;
-        double dacc = 0.0;
-        for (int s = 2 * lane; s < rows; s += 64) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
-          const uint32_t p0 = min(w & 0xFFFFu, nm1), p1 = min(w >> 16, nm1);
-          const T v0 = blk[s * n + p0];
-          const T v1 = blk[(s + 1) * n + p1];
-          if constexpr (kInt) iacc += (unsigned long long)v0 + v1;
-          else dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
+      if constexpr (kInt) {
+        // u16 codes: a block partial is < R * 65536 <= 2^32 for R <= 65536/... (R <= 1024 here)
+        for (int k = warp; k < cnt; k += nwarps) {
+          const uint16_t* src = sp + (size_t)k * R;
+          uint32_t acc = 0;
+          for (int s = 2 * lane; s < rows; s += 64) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
+            acc += (uint32_t)blk[s * n + min(w & 0xFFFFu, nm1)] + (uint32_t)blk[(s + 1) * n + min(w >> 16, nm1)];
+          }
+          acc = __reduce_add_sync(kFull, acc);
+          if (lane == 0) a.part[(o0 + st * kStageOrders + k) * nb + b] = (double)acc;
         }
-        double partial;
-        if constexpr (kInt) partial = (double)warp_sum(iacc);  // < 2^53: exact
-        else partial = warp_sum(dacc);
-        if (lane == 0) a.part[(o0 + st * kStageOrders + k) * nb + b] = partial;
+      } else {
+        for (int k = warp; k < cnt; k += nwarps) {
+          const uint16_t* src = sp + (size_t)k * R;
+          double dacc = 0.0;
+          for (int s = 2 * lane; s < rows; s += 64) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
+            const T v0 = blk[s * n + min(w & 0xFFFFu, nm1)];
+            const T v1 = blk[(s + 1) * n + min(w >> 16, nm1)];
+            dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
+          }
+          const double partial = warp_sum(dacc);
+          if (lane == 0) a.part[(o0 + st * kStageOrders + k) * nb + b] = partial;
+        }
       }
       phase_bits ^= 1u << slot;
       __syncthreads();  // slot consumed
