@@ -386,6 +386,28 @@ def run_extras(rw, torch):
                                        "cost": best[0], "steps_per_level": best[1], "evaluations": best[2],
                                        "chains": best[4],
                                        "reference_seconds_per_run_container": statistics.median(r["seconds"] for r in ref)}
+    gpath4 = os.path.join(ROOT, "tests", "golden", "anneal_c4.json")
+    if os.path.exists(gpath4):
+        g = json.load(open(gpath4))
+        ref = g["results"]
+        target = min(r["cost"] for r in ref)
+        m = rw.fixtures.config_matrix("C4", "fixed")
+        prob = rw.Problem(m)
+        spec = rw.fixtures.ring_spec(1024, rw.fixtures.SIZE_FIXED)
+        best = None
+        t = time.perf_counter()
+        for steps in (256, 1024, 4096):
+            t1 = time.perf_counter()
+            order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps),
+                                               schedule="calibrated")
+            best = (cost, steps, ev, time.perf_counter() - t1, rep["chains"])
+            if cost <= target:
+                break
+        out["time_to_best_ring_c4"] = {"seconds_cumulative": time.perf_counter() - t, "seconds_last_run": best[3],
+                                       "target_reference_min_seeds0_3": target, "reached": best[0] <= target,
+                                       "cost": best[0], "identity_cost": ref[0]["identity_cost"],
+                                       "steps_per_level": best[1], "evaluations": best[2], "chains": best[4],
+                                       "reference_seconds_per_run_container": statistics.median(r["seconds"] for r in ref)}
     return out
 
 

@@ -205,6 +205,30 @@ def test_anneal_quality_vs_reference_equal_budget():
     assert costs[0] <= ref_costs[0] * 1.0005, (costs[0], ref_costs[0])
 
 
+def test_anneal_quality_c4_equal_budget():
+    """C4 (N=1024 ring, fixed point): four GPU runs (seeds 0-3) at the reference
+    run's evaluation count (45,170,792: full default schedule) against the
+    reference's four runs (tests/golden/anneal_c4.json, ~50 min each)."""
+    path = os.path.join(GOLD, "anneal_c4.json")
+    if not os.path.exists(path):
+        pytest.skip("C4 anneal goldens not generated")
+    ref = json.load(open(path))["results"]
+    ref_costs = sorted(r["cost"] for r in ref)
+    budget = ref[0]["evaluations"]
+    prob = rw.Problem(fixtures.config_matrix("C4", "fixed"))
+    spec = fixtures.ring_spec(1024, fixtures.SIZE_FIXED)
+    costs = []
+    for seed in range(4):
+        order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=seed, budget=1e6), chains=1,
+                                           max_proposals=budget, schedule="calibrated")
+        assert ev <= budget
+        costs.append(cost)
+    costs.sort()
+    print("gpu", costs, "ref", ref_costs)
+    assert (costs[1] + costs[2]) / 2 <= (ref_costs[1] + ref_costs[2]) / 2
+    assert costs[0] <= ref_costs[0]
+
+
 # ---------------------------------------------------------- local search --
 def test_local_search_reaches_two_opt_optimum():
     port = Port()
