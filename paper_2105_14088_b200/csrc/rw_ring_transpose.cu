@@ -125,9 +125,6 @@ struct ScoreArgs {
   int nblocks;
   int cpb;         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
   double* part;    // [count][nblocks] partial sums
-  unsigned* done;  // per stage (indexed by its first order): blocks finished
-  double mul;      // cost = sum * mul
-  double* costs;   // chunk-relative output
 };
 
 constexpr int kStageOrders = 128;  // orders per TMA bulk stage
@@ -172,7 +169,6 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
   T* blk = reinterpret_cast<T*>(smem);
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem + al16((size_t)R * n * sizeof(T)));
   __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t nm1 = (uint32_t)(n - 1);
   constexpr bool kInt = std::is_same<T, uint16_t>::value;
@@ -243,27 +239,19 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
         }
       }
       phase_bits ^= 1u << slot;
-      __syncthreads();  // slot consumed, this stage's partials written
-      if (threadIdx.x == 0) {
-        if (st + kStages < nstage) issue(st + kStages);
-        // the same order range is scored by one CTA per row block; the last
-        // of them to finish combines the partials in block order
-        __threadfence();
-        s_last = atomicAdd(a.done + o0 + st * kStageOrders, 1u) == (unsigned)(nb - 1);
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
-          const int64_t o = o0 + st * kStageOrders + k;
-          const volatile double* pv = a.part + o * nb;
-          double sum = 0.0;
-          for (int q = 0; q < nb; ++q) sum = __dadd_rn(sum, pv[q]);
-          a.costs[o] = __dmul_rn(sum, a.mul);
-        }
-        if (threadIdx.x == 0) a.done[o0 + st * kStageOrders] = 0u;
-      }
+      __syncthreads();  // slot consumed
+      if (threadIdx.x == 0 && st + kStages < nstage) issue(st + kStages);
     }
+  }
+}
+
+// Pass 3: cost[o] = (sum of the order's block partials, in block order) * mul.
+__global__ void k_ring_combine(const double* __restrict__ part, int64_t count, int nb, double mul,
+                               double* __restrict__ costs) {
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < count; o += (int64_t)gridDim.x * blockDim.x) {
+    double sum = 0.0;
+    for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, part[o * nb + k]);
+    costs[o] = __dmul_rn(sum, mul);
   }
 }
 
@@ -301,10 +289,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   ThreadCtx& c = thread_ctx(p.device);
   const int64_t kmax = std::min(batch, chunk);
   uint16_t* predbuf = static_cast<uint16_t*>(c.scratch(slot, (size_t)nblocks * kmax * R * 2));
-  char* aux = static_cast<char*>(c.scratch(slot + 1, (size_t)kmax * nblocks * 8 + (size_t)kmax * 4 + 64));
-  double* part = reinterpret_cast<double*>(aux);
-  unsigned* done = reinterpret_cast<unsigned*>(aux + al16((size_t)kmax * nblocks * 8));
-  RW_CUDA(cudaMemsetAsync(done, 0, (size_t)kmax * 4, st));
+  double* part = static_cast<double*>(c.scratch(slot + 1, (size_t)kmax * nblocks * 8 + 64));
 
   const size_t route_smem = 8 * al16((size_t)n * 2);
   const size_t score_smem = al16((size_t)R * n * esz) + (size_t)kStages * kStageOrders * R * 2;
@@ -327,7 +312,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
-    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, part, done, plan.ring_mul, d_costs + off};
+    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, part};
     switch (p.storage) {
       case RW_STORAGE_U16: {
         auto k = k_ring_score<uint16_t>;
@@ -349,7 +334,9 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       }
     }
     RW_CUDA(cudaGetLastError());
-
+    k_ring_combine<<<(int)std::min<int64_t>((cnt_o + 255) / 256, (int64_t)sms * 8), 256, 0, st>>>(
+        part, cnt_o, nblocks, plan.ring_mul, d_costs + off);
+    RW_CUDA(cudaGetLastError());
   }
   return true;
 }
