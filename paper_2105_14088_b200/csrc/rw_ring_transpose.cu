@@ -124,7 +124,7 @@ struct ScoreArgs {
   int R;           // rows per block
   int nblocks;
   int cpb;         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
-  double* part;    // [count][nblocks] partial sums
+  double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
 };
 
 constexpr int kStageOrders = 128;  // orders per TMA bulk stage
@@ -217,17 +217,19 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
         for (int k = warp; k < cnt; k += nwarps) {
           const uint16_t* src = sp + (size_t)k * R;
           uint32_t acc = 0;
+#pragma unroll 1
           for (int s = 2 * lane; s < rows; s += 64) {
             const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
             acc += (uint32_t)blk[s * n + min(w & 0xFFFFu, nm1)] + (uint32_t)blk[(s + 1) * n + min(w >> 16, nm1)];
           }
           acc = __reduce_add_sync(kFull, acc);
-          if (lane == 0) a.part[(o0 + st * kStageOrders + k) * nb + b] = (double)acc;
+          if (lane == 0) a.part[(size_t)b * a.count + o0 + st * kStageOrders + k] = (double)acc;
         }
       } else {
         for (int k = warp; k < cnt; k += nwarps) {
           const uint16_t* src = sp + (size_t)k * R;
           double dacc = 0.0;
+#pragma unroll 1
           for (int s = 2 * lane; s < rows; s += 64) {
             const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
             const T v0 = blk[s * n + min(w & 0xFFFFu, nm1)];
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
             dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
           }
           const double partial = warp_sum(dacc);
-          if (lane == 0) a.part[(o0 + st * kStageOrders + k) * nb + b] = partial;
+          if (lane == 0) a.part[(size_t)b * a.count + o0 + st * kStageOrders + k] = partial;
         }
       }
       phase_bits ^= 1u << slot;
@@ -250,7 +252,7 @@ __global__ void k_ring_combine(const double* __restrict__ part, int64_t count, i
                                double* __restrict__ costs) {
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < count; o += (int64_t)gridDim.x * blockDim.x) {
     double sum = 0.0;
-    for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, part[o * nb + k]);
+    for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, part[(size_t)k * count + o]);
     costs[o] = __dmul_rn(sum, mul);
   }
 }
