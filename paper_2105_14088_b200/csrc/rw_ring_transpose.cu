@@ -125,6 +125,7 @@ struct ScoreArgs {
   int nblocks;
   int cpb;         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
   double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
+  unsigned long long* acc;  // u16 codes: per-order integer sums accumulated atomically (exact)
 };
 
 constexpr int kStageOrders = 128;  // orders per TMA bulk stage
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
             acc += (uint32_t)blk[s * n + min(w & 0xFFFFu, nm1)] + (uint32_t)blk[(s + 1) * n + min(w >> 16, nm1)];
           }
           acc = __reduce_add_sync(kFull, acc);
-          if (lane == 0) a.part[(size_t)b * a.count + o0 + st * kStageOrders + k] = (double)acc;
+          if (lane == 0) atomicAdd(a.acc + o0 + st * kStageOrders + k, (unsigned long long)acc);
         }
       } else {
         for (int k = warp; k < cnt; k += nwarps) {
@@ -255,6 +256,13 @@ __global__ void k_ring_combine(const double* __restrict__ part, int64_t count, i
     for (int k = 0; k < nb; ++k) sum = __dadd_rn(sum, part[(size_t)k * count + o]);
     costs[o] = __dmul_rn(sum, mul);
   }
+}
+
+// u16 path epilogue: costs hold integer sums (as u64 bits); scale in place.
+__global__ void k_ring_finalize(double* __restrict__ costs, int64_t count, double mul) {
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(costs);
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < count; o += (int64_t)gridDim.x * blockDim.x)
+    costs[o] = __dmul_rn((double)bits[o], mul);
 }
 
 }  // namespace
@@ -300,6 +308,8 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   };
   const int cpb = nblocks <= sms ? sms / nblocks : 0;
   const int sgrid = cpb > 0 ? nblocks * cpb : sms;
+  const bool int_sums = p.storage == RW_STORAGE_U16;
+  if (int_sums) RW_CUDA(cudaMemsetAsync(d_costs, 0, (size_t)batch * 8, st));
   for (int64_t off = 0; off < batch; off += kmax) {
     const int64_t cnt_o = std::min(kmax, batch - off);
     RouteArgs ra{cnt_o, off, n, R, nblocks, reinterpret_cast<unsigned long long*>(err_slot)};
@@ -314,7 +324,8 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
-    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, part};
+    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, part,
+                 reinterpret_cast<unsigned long long*>(d_costs + off)};
     switch (p.storage) {
       case RW_STORAGE_U16: {
         auto k = k_ring_score<uint16_t>;
@@ -336,8 +347,15 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       }
     }
     RW_CUDA(cudaGetLastError());
-    k_ring_combine<<<(int)std::min<int64_t>((cnt_o + 255) / 256, (int64_t)sms * 8), 256, 0, st>>>(
-        part, cnt_o, nblocks, plan.ring_mul, d_costs + off);
+    if (!int_sums) {
+      k_ring_combine<<<(int)std::min<int64_t>((cnt_o + 255) / 256, (int64_t)sms * 8), 256, 0, st>>>(
+          part, cnt_o, nblocks, plan.ring_mul, d_costs + off);
+      RW_CUDA(cudaGetLastError());
+    }
+  }
+  if (int_sums) {
+    k_ring_finalize<<<(int)std::min<int64_t>((batch + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(d_costs, batch,
+                                                                                                  plan.ring_mul);
     RW_CUDA(cudaGetLastError());
   }
   return true;
