@@ -179,7 +179,32 @@ std::string emit_smtlib(const CostMatrix& m, const CollectiveSpec& spec,
 RankOrder parse_model_file(const std::string& text, int n);
 bool balanced_sexpr(const std::string& text);
 
+// ------------------------------------------- topology / flow simulator -----
+// (topology.hpp / simulate.hpp: synthetic inputs and the validation ground
+// truth; not on the solver path, kept for the SPEC's validate workflow)
+struct TopologyLevel {
+  int fanout = 0;
+  double latency_us = 0.0;
+  double bandwidth_Bpus = 0.0;
+  double oversub = 1.0;
+};
+struct TopologySpec {
+  std::vector<TopologyLevel> levels;
+  double jitter = 0.0;
+  std::uint64_t seed = 0;
+  int host_count() const;
+};
+void validate(const TopologySpec& topo);
+int lca_level(const TopologySpec& topo, int i, int j);
+CostMatrix generate_matrix(const TopologySpec& topo);
+double simulate_collective(const TopologySpec& topo, const RankOrder& order, const CollectiveSpec& spec);
+double simulate_collective(const TopologySpec& topo, const CostMatrix& m, const RankOrder& order,
+                           const CollectiveSpec& spec);
+
 // ------------------------------------------------- GPU extensions (new) -----
+// Batched simulate_collective on the GPU.
+std::vector<double> simulate_batch(const TopologySpec& topo, const CostMatrix& m, const std::vector<RankOrder>& orders,
+                                   const CollectiveSpec& spec);
 // Process-wide defaults applied by anneal() / two_stage_solve().
 struct GpuOptions {
   int device = -1;      // -1: current CUDA device

@@ -1,0 +1,3 @@
+// rankweave/topology.hpp -- forwards to the consolidated drop-in API header.
+#pragma once
+#include "rankweave/rankweave.hpp"

@@ -211,6 +211,19 @@ rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* p
 rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed,
                           double* costs_out);
 
+/* ---- schedules and the flow simulator ---------------------------------- */
+/* expand_schedule (cost_model.hpp:33): call once with NULL arrays to get
+ * *nrounds_out and *count_out, then with round_offsets[nrounds+1] and
+ * src/dst/parent/bytes[count]. */
+rw_status rw_expand_schedule(const rw_spec* spec, int32_t* semantics_out, int32_t* nrounds_out, int64_t* count_out,
+                             int32_t* round_offsets, int32_t* src, int32_t* dst, int32_t* parent, double* bytes);
+/* simulate_collective(topo, m, order, spec) (simulate.hpp:24-25) for a batch
+ * of host orders; p must hold generate_matrix(topo).  bandwidth/oversub per
+ * level give the link capacities (bandwidth / oversub). */
+rw_status rw_simulate_batch(const rw_problem* p, int32_t nlevels, const int32_t* fanout, const double* bandwidth,
+                            const double* oversub, const rw_spec* spec, const int32_t* perms, int64_t batch,
+                            double* out);
+
 /* ---- synthetic inputs (topology.hpp:40, out of scope for kernels) ------ */
 /* generate_matrix(TopologySpec): writes n*n doubles; returns n in *n_out. */
 rw_status rw_generate_matrix(int32_t nlevels, const int32_t* fanout, const double* latency_us,

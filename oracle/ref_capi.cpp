@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "rankweave/cost_model.hpp"
+#include "rankweave/simulate.hpp"
 #include "rankweave/solver.hpp"
 #include "rankweave/stats.hpp"
 #include "rankweave/topology.hpp"
@@ -177,6 +178,31 @@ int ref_sample_costs(const double* m, const RefSpec* s, int32_t samples, uint64_
     const auto v = sample_costs(to_matrix(m, s->n), to_spec(s), samples, seed);
     std::memcpy(out, v.data(), sizeof(double) * v.size());
   });
+}
+
+// simulate_collective (simulate.cpp:81-138) for a batch of orders on the
+// topology's generated matrix.
+int ref_simulate_batch(int32_t nlevels, const int32_t* fanout, const double* latency_us, const double* bw,
+                       const double* oversub, double jitter, uint64_t seed, const RefSpec* s, const int32_t* perms,
+                       int64_t batch, double* out) {
+  return guarded([&] {
+    TopologySpec t;
+    for (int l = 0; l < nlevels; ++l) t.levels.push_back({fanout[l], latency_us[l], bw[l], oversub[l]});
+    t.jitter = jitter;
+    t.seed = seed;
+    const CostMatrix m = generate_matrix(t);
+    const CollectiveSpec spec = to_spec(s);
+    RankOrder o;
+    o.perm.resize(static_cast<size_t>(spec.n));
+    for (int64_t b = 0; b < batch; ++b) {
+      std::memcpy(o.perm.data(), perms + b * spec.n, sizeof(int32_t) * static_cast<size_t>(spec.n));
+      out[b] = simulate_collective(t, m, o, spec);
+    }
+  });
+}
+
+int ref_spearman(const double* x, const double* y, int64_t count, double* out) {
+  return guarded([&] { *out = spearman(std::vector<double>(x, x + count), std::vector<double>(y, y + count)); });
 }
 
 int ref_distribution_stats(const double* v, int32_t count, double* out4) {

@@ -91,6 +91,8 @@ SIGNATURES = {
     "rw_generate_matrix": (C.c_int, [C.c_int32, _i32p, _dp, _dp, _dp, C.c_double, C.c_uint64, _dp, C.c_int64,
                                      _i32p]),
     "rw_relabel_matrix": (C.c_int, [_dp, C.c_int32, C.c_uint64]),
+    "rw_expand_schedule": (C.c_int, [P(rw_spec), _i32p, _i32p, P(C.c_int64), _i32p, _i32p, _i32p, _i32p, _dp]),
+    "rw_simulate_batch": (C.c_int, [_vp, C.c_int32, _i32p, _dp, _dp, P(rw_spec), _i32p, C.c_int64, _dp]),
 }
 
 

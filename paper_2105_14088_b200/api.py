@@ -540,5 +540,66 @@ def generate_matrix(levels, jitter: float = 0.0, seed: int = 0) -> np.ndarray:
     return out
 
 
+def expand_schedule(spec: CollectiveSpec):
+    """expand_schedule (cost_model.hpp:33) -> (semantics, [ [(src, dst, bytes, parent), ...] per round ])."""
+    sem, nr, cnt = C.c_int32(), C.c_int32(), C.c_int64()
+    z = None
+    check(lib.rw_expand_schedule(C.byref(spec._c()), C.byref(sem), C.byref(nr), C.byref(cnt), z, z, z, z, z))
+    off = np.empty(nr.value + 1, dtype=np.int32)
+    src, dst, par = (np.empty(cnt.value, dtype=np.int32) for _ in range(3))
+    by = np.empty(cnt.value, dtype=np.float64)
+    check(lib.rw_expand_schedule(C.byref(spec._c()), C.byref(sem), C.byref(nr), C.byref(cnt), ptr(off, C.c_int32),
+                                 ptr(src, C.c_int32), ptr(dst, C.c_int32), ptr(par, C.c_int32), ptr(by, C.c_double)))
+    rounds = [[(int(src[t]), int(dst[t]), float(by[t]), int(par[t])) for t in range(off[r], off[r + 1])]
+              for r in range(nr.value)]
+    return ScheduleSemantics(sem.value), rounds
+
+
+def simulate_batch(m: CostMatrix, levels, spec: CollectiveSpec, orders: np.ndarray) -> np.ndarray:
+    """Batched simulate_collective (simulate.hpp:24) on the GPU; `m` must be
+    generate_matrix(levels, ...); levels = [(fanout, latency_us, bandwidth, oversub), ...]."""
+    o = np.ascontiguousarray(orders, dtype=np.int32)
+    if o.ndim == 1:
+        o = o[None, :]
+    fan = np.array([int(l[0]) for l in levels], dtype=np.int32)
+    bw = np.array([float(l[2]) for l in levels], dtype=np.float64)
+    ov = np.array([float(l[3]) if len(l) > 3 else 1.0 for l in levels], dtype=np.float64)
+    out = np.empty(o.shape[0], dtype=np.float64)
+    check(lib.rw_simulate_batch(m.problem().handle, len(levels), ptr(fan, C.c_int32), ptr(bw, C.c_double),
+                                ptr(ov, C.c_double), C.byref(spec._c()), ptr(o, C.c_int32), o.shape[0],
+                                ptr(out, C.c_double)))
+    return out
+
+
+def spearman(xs, ys) -> float:
+    """spearman (stats.hpp:14): Pearson correlation of average ranks."""
+    x = np.asarray(xs, dtype=np.float64)
+    y = np.asarray(ys, dtype=np.float64)
+    if x.size != y.size:
+        raise DomainError(f"spearman: series lengths differ ({x.size} vs {y.size})")
+    if x.size < 2:
+        raise DomainError("spearman: need at least 2 points")
+
+    def ranks(v):
+        idx = np.argsort(v, kind="stable")
+        r = np.empty(v.size)
+        i = 0
+        while i < v.size:
+            j = i
+            while j + 1 < v.size and v[idx[j + 1]] == v[idx[i]]:
+                j += 1
+            r[idx[i:j + 1]] = (i + j) / 2.0 + 1.0
+            i = j + 1
+        return r
+
+    rx, ry = ranks(x), ranks(y)
+    mx, my = rx.mean(), ry.mean()
+    dx, dy = rx - mx, ry - my
+    sxx, syy = float(dx @ dx), float(dy @ dy)
+    if sxx == 0.0 or syy == 0.0:
+        raise DomainError("spearman: constant series, coefficient undefined")
+    return float(dx @ dy) / math.sqrt(sxx * syy)
+
+
 def device_count() -> int:
     return int(lib.rw_device_count())

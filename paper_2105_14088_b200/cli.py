@@ -154,6 +154,41 @@ def cmd_generate(a) -> int:
     return 0
 
 
+def cmd_validate(a) -> int:
+    """SPEC cmd_validate: model cost vs simulated time over K random orders (GPU for both),
+    Spearman coefficient and DistributionStats of each series."""
+    try:
+        t = json.load(open(a.topology))
+    except OSError:
+        raise IOFailure(f"cannot read '{a.topology}'")
+    except json.JSONDecodeError:
+        raise IOFailure("malformed JSON in topology file")
+    if a.samples < 2:
+        raise api.DomainError("validate needs at least 2 samples")
+    levels = [(int(l["fanout"]), float(l["latency_us"]), float(l["bandwidth_Bpus"]), float(l.get("oversub", 1.0)))
+              for l in t["levels"]]
+    rtt = api.generate_matrix(levels, float(t.get("jitter", 0.0)), int(t.get("seed", 0)))
+    m = api.CostMatrix([f"node{i}" for i in range(rtt.shape[0])], rtt)
+    spec = api.CollectiveSpec(api.algorithm_from_string(a.algo), m.n(), a.size, a.b)
+    orders = api.sample_orders(m.n(), a.samples, a.seed)
+    model = m.problem().evaluate_batch(spec, orders, exact=True)
+    sim = api.simulate_batch(m, levels, spec, orders)
+
+    def stats(v):
+        s = api.distribution_stats(v)
+        return {"min": s.min, "max": s.max, "mean": s.mean, "stddev": s.stddev, "count": s.count}
+
+    try:
+        rho = api.spearman(model, sim)
+    except api.DomainError:
+        rho = "undefined"
+    report = {"algorithm": a.algo, "n": m.n(), "size_bytes": a.size, "samples": a.samples, "spearman": rho,
+              "model": stats(model), "simulated": stats(sim)}
+    _write(a.out, json.dumps(report, indent=2) + "\n")
+    print(f"spearman {rho}", file=sys.stderr)
+    return 0
+
+
 def cmd_evaluate(a) -> int:
     m = load_matrix(a.matrix)
     spec = api.CollectiveSpec(api.algorithm_from_string(a.algo), m.n(), a.size, a.b)
@@ -183,6 +218,14 @@ def main(argv=None) -> int:
     g = sub.add_parser("generate")
     g.add_argument("--topology", required=True)
     g.add_argument("--out", required=True)
+    v = sub.add_parser("validate")
+    v.add_argument("--topology", required=True)
+    v.add_argument("--algo", required=True, choices=["ring", "hd", "dbt", "bcube"])
+    v.add_argument("--size", type=float, required=True)
+    v.add_argument("--b", type=int, default=2)
+    v.add_argument("--samples", type=int, required=True)
+    v.add_argument("--seed", type=int, default=int(os.environ.get("RANKWEAVE_SEED", "0")))
+    v.add_argument("--out", required=True)
     e = sub.add_parser("evaluate")
     e.add_argument("--matrix", required=True)
     e.add_argument("--algo", required=True, choices=["ring", "hd", "dbt", "bcube"])
@@ -194,7 +237,8 @@ def main(argv=None) -> int:
     except SystemExit as ex:
         return 1 if ex.code else 0
     try:
-        return {"solve": cmd_solve, "reorder": cmd_reorder, "generate": cmd_generate, "evaluate": cmd_evaluate}[a.cmd](a)
+        return {"solve": cmd_solve, "reorder": cmd_reorder, "generate": cmd_generate, "evaluate": cmd_evaluate,
+                "validate": cmd_validate}[a.cmd](a)
     except IOFailure as ex:
         print(f"error: {ex}", file=sys.stderr)
         return 2

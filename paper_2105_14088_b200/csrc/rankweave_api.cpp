@@ -344,67 +344,25 @@ std::vector<double> evaluate_batch(const CostMatrix& m, const std::vector<RankOr
 
 // Schedule structure (matrix independent); semantics per cost_model.cpp:150-236.
 Schedule expand_schedule(const CollectiveSpec& spec) {
-  validate(spec);
-  const int n = spec.n;
+  const rw_spec cs = to_c(spec);
+  int32_t sem = 0, nrounds = 0;
+  int64_t count = 0;
+  check(rw_expand_schedule(&cs, &sem, &nrounds, &count, nullptr, nullptr, nullptr, nullptr, nullptr));
+  std::vector<int32_t> off(static_cast<std::size_t>(nrounds) + 1), src(static_cast<std::size_t>(count)),
+      dst(static_cast<std::size_t>(count)), parent(static_cast<std::size_t>(count));
+  std::vector<double> bytes(static_cast<std::size_t>(count));
+  check(rw_expand_schedule(&cs, &sem, &nrounds, &count, off.data(), src.data(), dst.data(), parent.data(),
+                           bytes.data()));
   Schedule s;
   s.algorithm = spec.algorithm;
-  s.node_count = n;
-  if (n == 1) {
-    s.semantics = ScheduleSemantics::SequentialHops;
-    return s;
-  }
-  switch (spec.algorithm) {
-    case Algorithm::Ring:
-      s.semantics = ScheduleSemantics::SequentialHops;
-      for (int i = 0; i < n; ++i) s.rounds.push_back({Transfer{i, alias_rank(i - 1, n), spec.size_bytes, -1}});
-      break;
-    case Algorithm::HalvingDoubling:
-    case Algorithm::BCube: {
-      s.semantics = ScheduleSemantics::BulkSynchronousRounds;
-      const bool hd = spec.algorithm == Algorithm::HalvingDoubling;
-      const int base = hd ? 2 : spec.bcube_b;
-      const int rounds = ilog(n, base);
-      long long stride = 1;
-      for (int r = 0; r < rounds; ++r, stride *= base) {
-        const double bytes = round_bytes(spec.size_bytes, base, r);
-        std::vector<Transfer> round;
-        if (hd && spec.hd_pairing == HdPairing::XorPairing) {
-          for (int j = 0; j < n; ++j) round.push_back(Transfer{j, j ^ static_cast<int>(stride), bytes, -1});
-        } else if (hd) {
-          for (int j = 0; j < n / 2; ++j)
-            round.push_back(Transfer{j, alias_rank(j + static_cast<int>(stride), n), bytes, -1});
-        } else {
-          for (int j = 0; j < n / base; ++j)
-            for (int k = 1; k < base; ++k)
-              round.push_back(Transfer{j, static_cast<int>((j + k * stride) % n), bytes, -1});
-        }
-        s.rounds.push_back(std::move(round));
-      }
-      break;
-    }
-    case Algorithm::DoubleBinaryTree: {
-      s.semantics = ScheduleSemantics::CriticalPath;
-      const double half = spec.size_bytes / 2.0;
-      // depth-first emission: an edge's children are the two edges of its
-      // sub-interval one depth below (the reference's recursion order)
-      std::function<void(int, int, int, int, int)> walk = [&](int i, int j, int shift, int depth, int parent) {
-        if (i >= j) return;
-        if (static_cast<int>(s.rounds.size()) <= depth) s.rounds.resize(static_cast<std::size_t>(depth) + 1);
-        const int mid = (i + j) / 2;
-        auto& level = s.rounds[static_cast<std::size_t>(depth)];
-        const int li = static_cast<int>(level.size());
-        level.push_back(Transfer{alias_rank(mid + shift, n), alias_rank((3 * i + j) / 2 - 1 + shift, n), half, parent});
-        walk(i, mid - 1, shift, depth + 1, li);
-        auto& level2 = s.rounds[static_cast<std::size_t>(depth)];
-        const int ri = static_cast<int>(level2.size());
-        level2.push_back(Transfer{alias_rank(mid + shift, n), alias_rank((i + 3 * j) / 2 + 1 + shift, n), half, parent});
-        walk(mid + 1, j, shift, depth + 1, ri);
-      };
-      walk(0, n - 1, 0, 0, -1);
-      walk(0, n - 1, -1, 0, -1);
-      break;
-    }
-  }
+  s.node_count = spec.n;
+  s.semantics = static_cast<ScheduleSemantics>(sem);
+  s.rounds.resize(static_cast<std::size_t>(nrounds));
+  for (int r = 0; r < nrounds; ++r)
+    for (int32_t t = off[static_cast<std::size_t>(r)]; t < off[static_cast<std::size_t>(r) + 1]; ++t)
+      s.rounds[static_cast<std::size_t>(r)].push_back(
+          Transfer{src[static_cast<std::size_t>(t)], dst[static_cast<std::size_t>(t)], bytes[static_cast<std::size_t>(t)],
+                   parent[static_cast<std::size_t>(t)]});
   return s;
 }
 
@@ -758,6 +716,96 @@ bool balanced_sexpr(const std::string& text) {
     else if (ch == ')' && --depth < 0) return false;
   }
   return depth == 0;
+}
+
+// ------------------------------------------------- topology / simulator --
+int TopologySpec::host_count() const {
+  long long h = 1;
+  for (const auto& l : levels) h *= l.fanout;
+  return static_cast<int>(h);
+}
+
+namespace {
+void topo_arrays(const TopologySpec& topo, std::vector<int32_t>& fan, std::vector<double>& lat, std::vector<double>& bw,
+                 std::vector<double>& ov) {
+  for (const auto& l : topo.levels) {
+    fan.push_back(l.fanout);
+    lat.push_back(l.latency_us);
+    bw.push_back(l.bandwidth_Bpus);
+    ov.push_back(l.oversub);
+  }
+}
+}  // namespace
+
+// validate(TopologySpec) (topology.cpp:20-29): the C ABI generator applies the
+// rule set; a size query validates without generating.
+void validate(const TopologySpec& topo) {
+  std::vector<int32_t> fan;
+  std::vector<double> lat, bw, ov;
+  topo_arrays(topo, fan, lat, bw, ov);
+  int32_t n = 0;
+  check(rw_generate_matrix(static_cast<int32_t>(fan.size()), fan.data(), lat.data(), bw.data(), ov.data(), topo.jitter,
+                           topo.seed, nullptr, 0, &n));
+}
+
+// Level of the lowest common ancestor (topology.cpp:31-38): index arithmetic.
+int lca_level(const TopologySpec& topo, int i, int j) {
+  long long group = 1;
+  for (std::size_t l = 0; l < topo.levels.size(); ++l) {
+    group *= topo.levels[l].fanout;
+    if (i / group == j / group) return static_cast<int>(l);
+  }
+  return static_cast<int>(topo.levels.size()) - 1;
+}
+
+CostMatrix generate_matrix(const TopologySpec& topo) {
+  std::vector<int32_t> fan;
+  std::vector<double> lat, bw, ov;
+  for (const auto& l : topo.levels) {
+    fan.push_back(l.fanout);
+    lat.push_back(l.latency_us);
+    bw.push_back(l.bandwidth_Bpus);
+    ov.push_back(l.oversub);
+  }
+  int32_t n = 0;
+  check(rw_generate_matrix(static_cast<int32_t>(fan.size()), fan.data(), lat.data(), bw.data(), ov.data(), topo.jitter,
+                           topo.seed, nullptr, 0, &n));
+  CostMatrix m;
+  m.rtt_us.resize(static_cast<std::size_t>(n) * static_cast<std::size_t>(n));
+  check(rw_generate_matrix(static_cast<int32_t>(fan.size()), fan.data(), lat.data(), bw.data(), ov.data(), topo.jitter,
+                           topo.seed, m.rtt_us.data(), static_cast<int64_t>(m.rtt_us.size()), &n));
+  for (int i = 0; i < n; ++i) m.hosts.push_back("node" + std::to_string(i));
+  return m;
+}
+
+std::vector<double> simulate_batch(const TopologySpec& topo, const CostMatrix& m, const std::vector<RankOrder>& orders,
+                                   const CollectiveSpec& spec) {
+  std::vector<int32_t> fan;
+  std::vector<double> bw, ov;
+  for (const auto& l : topo.levels) {
+    fan.push_back(l.fanout);
+    bw.push_back(l.bandwidth_Bpus);
+    ov.push_back(l.oversub);
+  }
+  std::vector<int32_t> flat;
+  for (const auto& o : orders) {
+    validate(o, spec.n);
+    flat.insert(flat.end(), o.perm.begin(), o.perm.end());
+  }
+  std::vector<double> out(orders.size());
+  const rw_spec cs = to_c(spec);
+  check(rw_simulate_batch(device_problem(m), static_cast<int32_t>(fan.size()), fan.data(), bw.data(), ov.data(), &cs,
+                          flat.data(), static_cast<int64_t>(orders.size()), out.data()));
+  return out;
+}
+
+double simulate_collective(const TopologySpec& topo, const CostMatrix& m, const RankOrder& order,
+                           const CollectiveSpec& spec) {
+  return simulate_batch(topo, m, {order}, spec).front();
+}
+
+double simulate_collective(const TopologySpec& topo, const RankOrder& order, const CollectiveSpec& spec) {
+  return simulate_collective(topo, generate_matrix(topo), order, spec);
 }
 
 // ---------------------------------------------------------- GPU options ----

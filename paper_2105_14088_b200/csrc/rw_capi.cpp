@@ -375,6 +375,56 @@ rw_status rw_generate_matrix(int32_t nlevels, const int32_t* fanout, const doubl
   return g != RW_OK ? g : st;
 }
 
+rw_status rw_expand_schedule(const rw_spec* spec, int32_t* semantics_out, int32_t* nrounds_out, int64_t* count_out,
+                             int32_t* round_offsets, int32_t* src, int32_t* dst, int32_t* parent, double* bytes) {
+  return guarded([&] {
+    need(spec, "spec");
+    const rwb::Expanded e = rwb::expand_schedule_core(*spec);
+    if (semantics_out) *semantics_out = e.semantics;
+    if (nrounds_out) *nrounds_out = e.nrounds();
+    if (count_out) *count_out = static_cast<int64_t>(e.src.size());
+    if (round_offsets) std::copy(e.off.begin(), e.off.end(), round_offsets);
+    if (src) std::copy(e.src.begin(), e.src.end(), src);
+    if (dst) std::copy(e.dst.begin(), e.dst.end(), dst);
+    if (parent) std::copy(e.parent.begin(), e.parent.end(), parent);
+    if (bytes) std::copy(e.bytes.begin(), e.bytes.end(), bytes);
+  });
+}
+
+rw_status rw_simulate_batch(const rw_problem* p, int32_t nlevels, const int32_t* fanout, const double* bandwidth,
+                            const double* oversub, const rw_spec* spec, const int32_t* perms, int64_t batch,
+                            double* out) {
+  return guarded([&] {
+    need(fanout, "fanout");
+    need(bandwidth, "bandwidth");
+    need(oversub, "oversub");
+    need(spec, "spec");
+    rwb::Problem& q = get(p);
+    rwb::validate_spec(*spec);
+    long long hosts = 1;
+    rwb::TopologyDesc topo;
+    for (int l = 0; l < nlevels; ++l) {
+      if (fanout[l] < 1) rwb::fail_domain("topology level fanout must be >= 1");
+      if (!(bandwidth[l] > 0.0)) rwb::fail_domain("topology level bandwidth must be > 0");
+      if (!(oversub[l] >= 1.0)) rwb::fail_domain("topology oversubscription must be >= 1");
+      hosts *= fanout[l];
+      topo.fanout.push_back(fanout[l]);
+      topo.capacity.push_back(bandwidth[l] / oversub[l]);  // simulate.cpp:45-48
+    }
+    if (hosts != spec->n)
+      rwb::fail_domain("topology has " + std::to_string(hosts) + " hosts but spec.n=" + std::to_string(spec->n));
+    if (q.n != spec->n) rwb::fail_domain("matrix dimension does not match spec.n");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(perms, "perms");
+      need(out, "out");
+    }
+    for (int64_t b = 0; b < batch; ++b) validate_host_order(perms + b * spec->n, spec->n, spec->n);
+    const rwb::Expanded e = rwb::expand_schedule_core(*spec);
+    rwb::simulate_batch_device(q, topo, e, perms, batch, out);
+  });
+}
+
 rw_status rw_relabel_matrix(double* m, int32_t n, uint64_t seed) {
   return guarded([&] {
     need(m, "m");

@@ -95,6 +95,24 @@ struct EvalPlan {
   const DbtPlan* dbt = nullptr;
 };
 
+// expand_schedule (cost_model.cpp:150-236): rounds of transfers in rank space.
+struct Expanded {
+  int semantics = RW_SEQUENTIAL_HOPS;
+  std::vector<int32_t> off{0};  // round offsets (nrounds + 1)
+  std::vector<int32_t> src, dst, parent;
+  std::vector<double> bytes;
+  int nrounds() const { return static_cast<int>(off.size()) - 1; }
+};
+Expanded expand_schedule_core(const rw_spec& s);
+
+// Batched simulate_collective (simulate.cpp:52-138) on the device.
+struct TopologyDesc {
+  std::vector<int32_t> fanout;
+  std::vector<double> capacity;  // bandwidth / oversub per level
+};
+void simulate_batch_device(Problem& p, const TopologyDesc& topo, const Expanded& sch, const int32_t* perms,
+                           int64_t batch, double* out);
+
 void validate_spec(const rw_spec& s);                  // types.cpp:143-163 wording
 EvalPlan make_plan(Problem& p, const rw_spec& s);       // + n / matrix checks
 int64_t lookups_per_eval(const EvalPlan& plan);

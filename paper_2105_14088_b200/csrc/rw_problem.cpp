@@ -206,6 +206,99 @@ static double round_bytes(double size_bytes, int base, int round) {
   return size_bytes / divisor;
 }
 
+// Rounds of transfers in rank space; the double binary tree reuses the
+// critical-path plan builder's emission order (left edge, its subtree, right
+// edge, its subtree; primary tree then mirrored tree).
+Expanded expand_schedule_core(const rw_spec& s) {
+  validate_spec(s);
+  Expanded e;
+  const int n = s.n;
+  auto alias = [n](int r) { return ((r % n) + n) % n; };
+  auto close_round = [&] { e.off.push_back(static_cast<int32_t>(e.src.size())); };
+  auto add = [&](int a, int b, double by, int parent) {
+    e.src.push_back(a);
+    e.dst.push_back(b);
+    e.bytes.push_back(by);
+    e.parent.push_back(parent);
+  };
+  if (n == 1) return e;  // no rounds
+  switch (s.algorithm) {
+    case kRing:
+      e.semantics = RW_SEQUENTIAL_HOPS;
+      for (int i = 0; i < n; ++i) {
+        add(i, alias(i - 1), s.size_bytes, -1);
+        close_round();
+      }
+      break;
+    case kHalvingDoubling:
+    case kBCube: {
+      e.semantics = RW_BULK_SYNCHRONOUS_ROUNDS;
+      const bool hd = s.algorithm == kHalvingDoubling;
+      const int base = hd ? 2 : s.bcube_b;
+      const int rounds = ilog_exact(n, base);
+      long long stride = 1;
+      for (int r = 0; r < rounds; ++r, stride *= base) {
+        const double by = round_bytes(s.size_bytes, base, r);
+        if (hd && s.hd_pairing == RW_PAIRING_XOR) {
+          for (int j = 0; j < n; ++j) add(j, j ^ static_cast<int>(stride), by, -1);
+        } else if (hd) {
+          for (int j = 0; j < n / 2; ++j) add(j, alias(j + static_cast<int>(stride)), by, -1);
+        } else {
+          for (int j = 0; j < n / base; ++j)
+            for (int k = 1; k < base; ++k) add(j, static_cast<int>((j + k * stride) % n), by, -1);
+        }
+        close_round();
+      }
+      break;
+    }
+    case kDoubleBinaryTree: {
+      e.semantics = RW_CRITICAL_PATH;
+      struct Edge {
+        int src, dst, parent;
+      };
+      std::vector<std::vector<Edge>> rounds;
+      struct Frame {
+        int i, j, shift, depth, parent, stage, mid;
+      };
+      for (int shift : {0, -1}) {
+        std::vector<Frame> st;
+        st.push_back({0, n - 1, shift, 0, -1, 0, 0});
+        while (!st.empty()) {
+          Frame& f = st.back();
+          if (f.stage == 0) {
+            if (f.i >= f.j) {
+              st.pop_back();
+              continue;
+            }
+            if (static_cast<int>(rounds.size()) <= f.depth) rounds.resize(f.depth + 1);
+            f.mid = (f.i + f.j) / 2;
+            const int idx = static_cast<int>(rounds[f.depth].size());
+            rounds[f.depth].push_back({alias(f.mid + f.shift), alias((3 * f.i + f.j) / 2 - 1 + f.shift), f.parent});
+            f.stage = 1;
+            const Frame child{f.i, f.mid - 1, f.shift, f.depth + 1, idx, 0, 0};
+            st.push_back(child);
+          } else if (f.stage == 1) {
+            const int idx = static_cast<int>(rounds[f.depth].size());
+            rounds[f.depth].push_back({alias(f.mid + f.shift), alias((f.i + 3 * f.j) / 2 + 1 + f.shift), f.parent});
+            f.stage = 2;
+            const Frame child{f.mid + 1, f.j, f.shift, f.depth + 1, idx, 0, 0};
+            st.push_back(child);
+          } else {
+            st.pop_back();
+          }
+        }
+      }
+      const double half = s.size_bytes / 2.0;
+      for (const auto& r : rounds) {
+        for (const auto& ed : r) add(ed.src, ed.dst, half, ed.parent);
+        close_round();
+      }
+      break;
+    }
+  }
+  return e;
+}
+
 // Odd integer mantissa of a positive finite double (x = m * 2^e, m odd).
 static double odd_mantissa(double x) {
   int e = 0;

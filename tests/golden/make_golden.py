@@ -189,6 +189,46 @@ def anneal_c4_goldens(ref: Reference, seeds=(0, 1, 2, 3)):
     json.dump({"results": results, "budget_s": 1e6}, open(os.path.join(HERE, "anneal_c4.json"), "w"), indent=1)
 
 
+SIM_TOPOLOGIES = {
+    "t64": ([(8, 5, 1000, 1), (8, 25, 1000, 4)], 0.1, 2105),
+    "t256": ([(8, 5, 1000, 1), (16, 25, 1000, 4), (2, 100, 1000, 4)], 0.1, 2105),
+}
+
+
+def simulate_goldens(ref: Reference):
+    """simulate_collective from the reference on random orders (simulate.cpp:81-138)."""
+    import ctypes as C
+    P = C.POINTER
+    L = ref.lib
+    L.ref_simulate_batch.argtypes = [C.c_int32, P(C.c_int32), P(C.c_double), P(C.c_double), P(C.c_double), C.c_double,
+                                     C.c_uint64, P(type(make_spec())), P(C.c_int32), C.c_int64, P(C.c_double)]
+    payload = {}
+    for name, (levels, jitter, seed) in SIM_TOPOLOGIES.items():
+        fan = np.array([l[0] for l in levels], dtype=np.int32)
+        lat = np.array([l[1] for l in levels], dtype=np.float64)
+        bw = np.array([l[2] for l in levels], dtype=np.float64)
+        ov = np.array([l[3] for l in levels], dtype=np.float64)
+        n = int(np.prod(fan))
+        rng = np.random.default_rng(n)
+        perms = np.stack([np.arange(n)] + [rng.permutation(n) for _ in range(7)]).astype(np.int32)
+        payload[f"{name}_perms"] = perms
+        cases = [("ring", 0, 2, 0), ("hd_paper", 1, 2, 0), ("hd_xor", 1, 2, 1), ("dbt", 2, 2, 0), ("bcube2", 3, 2, 0)]
+        if name == "t64":
+            cases += [("bcube4", 3, 4, 0), ("bcube8", 3, 8, 0)]
+        for cname, alg, b, pair in cases:
+            s = make_spec(alg, n, 1e6, b, 1, pair)
+            out = np.empty(perms.shape[0], dtype=np.float64)
+            rc = L.ref_simulate_batch(len(levels), fan.ctypes.data_as(P(C.c_int32)), lat.ctypes.data_as(P(C.c_double)),
+                                      bw.ctypes.data_as(P(C.c_double)), ov.ctypes.data_as(P(C.c_double)), jitter, seed,
+                                      C.byref(s), perms.ctypes.data_as(P(C.c_int32)), perms.shape[0],
+                                      out.ctypes.data_as(P(C.c_double)))
+            assert rc == 0, L.ref_last_error()
+            payload[f"{name}_{cname}"] = out
+            payload[f"{name}_{cname}_spec"] = np.array([alg, n, b, 1, pair], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "simulate.npz"), **payload)
+    print("simulate goldens:", sorted(k for k in payload if not k.endswith(("_spec", "_perms"))), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true")
@@ -206,6 +246,8 @@ def main():
         anneal_goldens(ref)
     if "anneal_c4" in steps:
         anneal_c4_goldens(ref)
+    if "simulate" in steps or not a.only:
+        simulate_goldens(ref)
 
 
 if __name__ == "__main__":
