@@ -735,8 +735,14 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
         launch_ring_cluster<P>(p, plan, d_perms, batch, d_costs, validate, err_slot, st, budget))
       return;
   }
-  if (model == kRing && !smem_mat && (p.path == RW_PATH_AUTO || p.path == RW_PATH_TRANSPOSE) &&
+  // Ring transpose pays while a row block holds enough rows per order slice:
+  // on B200 it wins at N=1024 (4.2e8 vs 2.8e8 evals/s) and loses from N=2048
+  // (1.23e8 vs 1.35e8; N=4096 3.4e7 vs 6.7e7), so AUTO stops at 1536.
+  if (model == kRing && !smem_mat && (p.path == RW_PATH_TRANSPOSE || (p.path == RW_PATH_AUTO && n <= 1536)) &&
       launch_ring_transpose(p, plan, d_perms, (int)sizeof(P), batch, d_costs, validate, err_slot, st, slot))
+    return;
+  if (model == kHalvingDoubling && !smem_mat && (p.path == RW_PATH_AUTO || p.path == RW_PATH_TRANSPOSE) &&
+      launch_rounds_transpose(p, plan, d_perms, (int)sizeof(P), batch, d_costs, validate, err_slot, st, slot))
     return;
   if constexpr (std::is_same<P, uint16_t>::value) {
     if (model == kRing && n % 256 == 0 && (reinterpret_cast<uintptr_t>(d_perms) & 15) == 0) {

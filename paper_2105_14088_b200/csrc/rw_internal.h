@@ -147,6 +147,11 @@ void launch_evaluate(const Problem& p, const EvalPlan& plan, const void* d_perms
 bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
                            double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot);
 
+// Halving-doubling (paper / xor pairing) through per-round partner-by-host
+// slices (rw_rounds_transpose.cu); false when the shape is not supported.
+bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes,
+                             int64_t batch, double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot);
+
 // Generic schedule re-costing (schedule_cost, cost_model.cpp:238-285), one order.
 double schedule_cost_device(const Problem& p, int semantics, int nrounds, const int32_t* round_offsets,
                             const int32_t* src, const int32_t* dst, const double* bytes, const int32_t* parent,

@@ -29,6 +29,7 @@
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
+#include "rw_tma.cuh"
 
 namespace rwb {
 
@@ -131,33 +132,6 @@ struct ScoreArgs {
 constexpr int kStageOrders = 128;  // orders per TMA bulk stage
 constexpr int kStages = 4;
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-// TMA bulk copy global -> shared (1D, 16-byte multiple), completion on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-
 // Pass 2: a CTA keeps rows [b*R, b*R + rows) in shared memory and streams the
 // block's predecessor slices (contiguous in predbuf) through a 4-stage TMA
 // bulk-copy ring; each warp scores one order per step with shared-memory
@@ -169,13 +143,16 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
   const int n = a.n, R = a.R, nb = a.nblocks;
   T* blk = reinterpret_cast<T*>(smem);
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem + al16((size_t)R * n * sizeof(T)));
-  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ __align__(8) uint64_t bars[kStages], mat_bar;
+  unsigned mat_phase = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t nm1 = (uint32_t)(n - 1);
   constexpr bool kInt = std::is_same<T, uint16_t>::value;
   const size_t stage_elems = (size_t)kStageOrders * R;
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    mbar_init(&mat_bar, 1);
+  }
   __syncthreads();
   unsigned phase_bits = 0;  // parity per stage slot
 
@@ -189,12 +166,7 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
     const int row0 = b * R;
     const int rows = min(R, n - row0);
     __syncthreads();  // previous item fully consumed
-    {
-      const size_t bytes = (size_t)rows * n * sizeof(T);
-      const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)row0 * n);
-      uint4* dst = reinterpret_cast<uint4*>(blk);
-      for (size_t k = threadIdx.x; k < (bytes >> 4); k += blockDim.x) dst[k] = __ldg(src + k);
-    }
+    stage_rows(blk, gmat + (size_t)row0 * n, (size_t)rows * n * sizeof(T), &mat_bar, &mat_phase);
     const uint16_t* base = pred + ((size_t)b * a.count + o0) * R;
     const int64_t total = o1 - o0;
     const int64_t nstage = (total + kStageOrders - 1) / kStageOrders;

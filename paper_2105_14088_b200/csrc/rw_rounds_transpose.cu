@@ -1,0 +1,424 @@
+// rw_rounds_transpose.cu -- halving-doubling scoring (paper and xor pairing)
+// for matrices beyond one CTA's shared memory (C5: N=4096, 32 MiB u16),
+// without random L2 gathers.  Same plan as the ring transpose path
+// (rw_ring_transpose.cu):
+//
+//   route     one CTA per order: stage the order and its inverse pos = p^-1
+//             in shared memory, then gather partner-by-host for every round,
+//             part_r[h] = p[partner_r(pos[h])] (paper pairing: sources
+//             pos[h] < N/2 only, other hosts get the 0xFFFF sentinel; xor:
+//             every host is a source), written in 16-byte chunks grouped by
+//             row block: buf[block][round][order][R].  It also resets the
+//             order's per-round max keys.
+//   score     a CTA keeps R matrix rows in shared memory; a producer warp
+//             streams the block's partner slices with TMA bulk copies (one per
+//             round and stage) through a full/empty mbarrier ring; each
+//             consumer thread takes (round, order) tasks, walks the R rows and
+//             folds the block maximum into key[round][order] with atomicMax.
+//   finalize  per order, the reference's FP64 sequence fl(max * bytes_r)
+//             summed over rounds in order (halving_doubling_cost,
+//             proj/src/cost_model.cpp:71-92).
+//
+// Max is exact under any grouping, so the result is bit-identical to the
+// L2-gather kernel on every storage kind.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "rw_device.cuh"
+#include "rw_internal.h"
+#include "rw_tma.cuh"
+
+namespace rwb {
+
+using namespace dev;
+
+namespace {
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Order-preserving keys for the raw matrix codes (max over keys == the
+// reference's running std::max from 0, cost_model.cpp:83: NaN never wins).
+template <typename T>
+struct KeyOf;
+template <>
+struct KeyOf<uint16_t> {
+  using type = unsigned int;
+  __device__ static unsigned int enc(uint16_t v) { return v; }
+  __device__ static uint16_t dec(unsigned int k) { return (uint16_t)k; }
+};
+template <>
+struct KeyOf<float> {
+  using type = unsigned int;
+  __device__ static unsigned int enc(float v) {
+    if (v != v) return 0u;
+    const unsigned int b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  }
+  __device__ static float dec(unsigned int k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k); }
+};
+template <>
+struct KeyOf<double> {
+  using type = unsigned long long;
+  __device__ static unsigned long long enc(double v) {
+    if (v != v) return 0ull;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  }
+  __device__ static double dec(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+  }
+};
+
+// ------------------------------------------------------------------ route --
+struct RRouteArgs {
+  int64_t count;
+  int64_t base;
+  int n;
+  int rounds;
+  int xor_pairing;
+  int R;
+  unsigned long long* err;
+  void* keys;       // [round][order], reset to key(0) here
+  int key_bytes;    // 4 or 8
+  unsigned long long zero_key;
+  int aligned;      // order rows are 16-byte aligned
+};
+
+// Stages one order into shared memory as uint16 (vectorised when the row is
+// 16-byte aligned); out-of-range entries are masked into range and reported.
+template <typename P>
+__device__ __forceinline__ bool stage_order_vec(const P* __restrict__ pp, int n, uint16_t* p, bool aligned) {
+  bool bad = false;
+  const uint32_t mask = (uint32_t)n - 1;  // n is a power of two
+  if (aligned) {
+    uint4* p4 = reinterpret_cast<uint4*>(p);
+    for (int c = threadIdx.x; c < (n >> 3); c += blockDim.x) {
+      uint32_t v[8];
+      if constexpr (sizeof(P) == 2) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(pp) + c);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[2 * k] = ws[k] & 0xFFFFu;
+          v[2 * k + 1] = ws[k] >> 16;
+        }
+      } else {
+        const int4 w0 = __ldg(reinterpret_cast<const int4*>(pp) + 2 * c);
+        const int4 w1 = __ldg(reinterpret_cast<const int4*>(pp) + 2 * c + 1);
+        const int ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (uint32_t)ws[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        bad |= v[k] > mask;
+        v[k] &= mask;
+      }
+      p4[c] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t v = (uint32_t)ld_order<P>(pp, i);
+      bad |= v > mask;
+      p[i] = (uint16_t)(v & mask);
+    }
+  }
+  return bad;
+}
+
+// One CTA per order.  pos = p^-1 (one scatter per order); then every thread
+// emits 8 consecutive hosts' partners for one round as a 16-byte store:
+// part_r[h] = p[pos[h] ^ s] (xor) or p[pos[h] + s] for pos[h] < N/2 (paper).
+// Bijection check: p[pos[h]] == h for every host h.
+template <typename P, bool kValidate>
+__global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __restrict__ perms,
+                                                      uint16_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem);
+  uint16_t* pos = reinterpret_cast<uint16_t*>(smem + al16((size_t)n * 2));
+  const uint4* pos4 = reinterpret_cast<const uint4*>(pos);
+  for (int k = threadIdx.x; k < n; k += blockDim.x) pos[k] = 0;
+  const int half = n >> 1;
+  const int chunks8 = n >> 3;
+  const int cshift = 31 - __clz(chunks8);
+  const int rshift = 31 - __clz(a.R);
+  const int items = a.rounds << cshift;
+  const bool aligned = a.aligned != 0;
+  for (int64_t o = blockIdx.x; o < a.count; o += gridDim.x) {
+    __syncthreads();  // the previous order's readers of p / pos are done
+    bool bad = stage_order_vec<P>(perms + o * n, n, p, aligned);
+    if ((int)threadIdx.x < a.rounds) {
+      if (a.key_bytes == 8)
+        static_cast<unsigned long long*>(a.keys)[(size_t)threadIdx.x * a.count + o] = a.zero_key;
+      else
+        static_cast<unsigned int*>(a.keys)[(size_t)threadIdx.x * a.count + o] = (unsigned int)a.zero_key;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) pos[p[i]] = (uint16_t)i;
+    __syncthreads();
+    if (kValidate) {
+      for (int h = threadIdx.x; h < n; h += blockDim.x) bad |= p[pos[h]] != h;
+      if (__syncthreads_or(bad) && threadIdx.x == 0) report_bad_order(a.err, n, a.base + o);
+    }
+    for (int w = threadIdx.x; w < items; w += blockDim.x) {
+      const int r = w >> cshift;
+      const int c = w & (chunks8 - 1);
+      const int s = 1 << r;
+      const uint4 q4 = pos4[c];
+      const uint32_t js[4] = {q4.x, q4.y, q4.z, q4.w};
+      uint32_t outw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t j0 = js[k] & 0xFFFFu, j1 = js[k] >> 16;
+        uint32_t v0, v1;
+        if (a.xor_pairing) {
+          v0 = p[j0 ^ s];
+          v1 = p[j1 ^ s];
+        } else {
+          v0 = (int)j0 < half ? (uint32_t)p[j0 + s] : 0xFFFFu;
+          v1 = (int)j1 < half ? (uint32_t)p[j1 + s] : 0xFFFFu;
+        }
+        outw[k] = v0 | (v1 << 16);
+      }
+      const int h0 = c << 3;
+      const int b = h0 >> rshift;
+      const int s0 = h0 & (a.R - 1);
+      *reinterpret_cast<uint4*>(out + (((size_t)b * a.rounds + r) * a.count + o) * a.R + s0) =
+          make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ score --
+constexpr int kRStageOrders = 64;
+constexpr int kRMaxStages = 4;
+constexpr int kRThreads = 1024;  // 31 consumer warps + 1 producer warp
+
+struct RScoreArgs {
+  int64_t count;
+  int n;
+  int rounds;
+  int nblocks;
+  int stages;   // ring depth
+  void* keys;   // [round][order]
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, const uint16_t* __restrict__ buf,
+                                                               const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using K = typename KeyOf<T>::type;
+  const int n = a.n, rounds = a.rounds;
+  T* blk = reinterpret_cast<T*>(smem);
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + al16((size_t)R * n * sizeof(T)));
+  __shared__ __align__(8) uint64_t full[kRMaxStages], empty[kRMaxStages], mat_bar;
+  unsigned mat_phase = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kConsumers = kRThreads - 32;
+  const bool producer = warp == (kRThreads >> 5) - 1;
+  const size_t stage_elems = (size_t)kRStageOrders * rounds * R;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
+    }
+  if (threadIdx.x == 0) mbar_init(&mat_bar, 1);
+  __syncthreads();
+  K* keys = static_cast<K*>(a.keys);
+  // Stream-K split: the (block, stage) units are cut into gridDim.x equal
+  // contiguous ranges, so every CTA does the same work and reloads the matrix
+  // only where its range crosses a row block.
+  const int64_t nstage = (a.count + kRStageOrders - 1) / kRStageOrders;
+  const int64_t units = nstage * a.nblocks;
+  const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+  uint32_t g = 0;  // running stage counter of this CTA (same sequence in every role)
+  for (int64_t u = units * blockIdx.x / gridDim.x; u < u_end;) {
+    const int b = (int)(u / nstage);
+    const int64_t st0 = u - (int64_t)b * nstage;
+    const int64_t my_stages = min(nstage - st0, u_end - u);
+    u += my_stages;
+    __syncthreads();  // previous block's consumers are done with blk
+    stage_rows(blk, gmat + (size_t)b * R * n, (size_t)R * n * sizeof(T), &mat_bar, &mat_phase);
+    if (producer) {
+      if (lane == 0) {
+        for (int64_t i = 0; i < my_stages; ++i) {
+          const uint32_t gi = g + (uint32_t)i;
+          const int slot = (int)(gi % a.stages);
+          const uint32_t use = gi / a.stages;
+          if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1u);
+          const int64_t o0 = (st0 + i) * kRStageOrders;
+          const int cnt = (int)min((int64_t)kRStageOrders, a.count - o0);
+          const unsigned bytes = (unsigned)cnt * R * 2;
+          mbar_expect_tx(&full[slot], bytes * rounds);
+          uint16_t* dst = ring + slot * stage_elems;
+          for (int r = 0; r < rounds; ++r)
+            bulk_g2s(dst + (size_t)r * kRStageOrders * R, buf + (((size_t)b * rounds + r) * a.count + o0) * R, bytes,
+                      &full[slot]);
+        }
+      }
+    } else {
+      for (int64_t i = 0; i < my_stages; ++i) {
+        const uint32_t gi = g + (uint32_t)i;
+        const int slot = (int)(gi % a.stages);
+        mbar_wait(&full[slot], (gi / a.stages) & 1u);
+        const int64_t o0 = (st0 + i) * kRStageOrders;
+        const int cnt = (int)min((int64_t)kRStageOrders, a.count - o0);
+        const uint16_t* sp = ring + slot * stage_elems;
+        const int tasks = cnt * rounds;
+        for (int t = threadIdx.x; t < tasks; t += kConsumers) {
+          const int r = t / cnt;
+          const int k = t - r * cnt;
+          const uint4* q4 = reinterpret_cast<const uint4*>(sp + ((size_t)r * kRStageOrders + k) * R);
+          K key = KeyOf<T>::enc(T(0));
+#pragma unroll
+          for (int c = 0; c < R / 8; ++c) {
+            const uint4 q = q4[c];
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+              const uint32_t col = (h & 1) ? (w[h >> 1] >> 16) : (w[h >> 1] & 0xFFFFu);
+              if (col < (uint32_t)n) {
+                const K v = KeyOf<T>::enc(blk[(c * 8 + h) * n + col]);
+                key = v > key ? v : key;
+              }
+            }
+          }
+          if (key != KeyOf<T>::enc(T(0))) atomicMax(keys + (size_t)r * a.count + o0 + k, key);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+    }
+    g += (uint32_t)my_stages;
+  }
+}
+
+// --------------------------------------------------------------- finalize --
+struct RFinalArgs {
+  int64_t count;
+  int rounds;
+  int mode;
+  double scale;
+  double bytes[kMaxRounds];
+};
+
+template <typename T>
+__global__ void k_rounds_finalize(RFinalArgs a, const void* __restrict__ keys_v, double* __restrict__ costs) {
+  using K = typename KeyOf<T>::type;
+  const K* keys = static_cast<const K*>(keys_v);
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= a.count) return;
+  double total = 0.0;
+  for (int r = 0; r < a.rounds; ++r) {
+    double v = to_double(KeyOf<T>::dec(keys[(size_t)r * a.count + o]), a.scale);
+    if (a.mode == RW_LATENCY_TIMES_SIZE) v = __dmul_rn(v, a.bytes[r]);
+    total = __dadd_rn(total, v);
+  }
+  costs[o] = total;
+}
+
+template <typename T, int R>
+void launch_score(const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat, cudaStream_t st) {
+  auto k = k_rounds_score<T, R>;
+  RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, kRThreads, smem, st>>>(sa, buf, static_cast<const T*>(mat));
+}
+
+template <typename T>
+void launch_score_r(int R, const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat,
+                    cudaStream_t st) {
+  if (R == 32) launch_score<T, 32>(sa, grid, smem, buf, mat, st);
+  else if (R == 16) launch_score<T, 16>(sa, grid, smem, buf, mat, st);
+  else launch_score<T, 8>(sa, grid, smem, buf, mat, st);
+}
+
+}  // namespace
+
+bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                             double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot) {
+  const int n = plan.n;
+  if (plan.model != kHalvingDoubling || n < 512 || n > 16384 || (n & (n - 1)) != 0 || batch <= 0) return false;
+  const int rounds = plan.rounds;
+  if (rounds < 1 || rounds > 14) return false;
+  int sms = 148, optin = 227 * 1024;
+  RW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+  RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
+  const size_t budget = (size_t)std::min(optin, 227 * 1024) - 1024;
+  const size_t esz = p.elem_bytes();
+  // Largest row block that leaves room for a >= 2-deep ring of stages.
+  int R = 0, stages = 0;
+  for (int cand : {32, 16, 8}) {
+    const size_t mat = al16((size_t)cand * n * esz);
+    const size_t stage = (size_t)kRStageOrders * rounds * cand * 2;
+    if (mat + 2 * stage <= budget) {
+      R = cand;
+      stages = (int)std::min<size_t>(kRMaxStages, (budget - mat) / stage);
+      break;
+    }
+  }
+  if (!R) return false;
+  const int nblocks = n / R;
+  const size_t score_smem = al16((size_t)R * n * esz) + (size_t)stages * kRStageOrders * rounds * R * 2;
+  const size_t route_smem = 2 * al16((size_t)n * 2);
+
+  const int64_t per_order_bytes = (int64_t)2 * rounds * n;
+  // Partner-buffer size: every score CTA restages ~2.5 row blocks per chunk,
+  // so chunks of >= 4096 orders keep that below a quarter of the partner
+  // traffic (measured on B200: 48 MB -> 7.8e6, 384 MB -> 1.14e7 evals/s at
+  // N=4096).  The buffer then streams through HBM; RW_TRANSPOSE_BUF_MB overrides.
+  static const int64_t buf_override = [] {
+    const char* e = std::getenv("RW_TRANSPOSE_BUF_MB");
+    return e ? std::max(8L, std::atol(e)) << 20 : 0L;
+  }();
+  const int64_t buf_bytes =
+      buf_override ? buf_override : std::min<int64_t>(384ll << 20, std::max<int64_t>(48ll << 20, per_order_bytes * 16384));
+  const int64_t chunk = std::max<int64_t>(kRStageOrders, buf_bytes / per_order_bytes);
+  const int64_t kmax = std::min(batch, chunk);
+  ThreadCtx& c = thread_ctx(p.device);
+  uint16_t* buf = static_cast<uint16_t*>(c.scratch(slot, (size_t)kmax * per_order_bytes));
+  const int key_bytes = esz == 8 ? 8 : 4;
+  void* keys = c.scratch(slot + 1, (size_t)rounds * kmax * key_bytes);
+  unsigned long long zero_key = 0;
+  if (p.storage == RW_STORAGE_F32) zero_key = 0x80000000ull;
+  if (p.storage == RW_STORAGE_F64) zero_key = 0x8000000000000000ull;
+
+  auto route = validate ? (perm_bytes == 2 ? (void*)k_rounds_route<uint16_t, true> : (void*)k_rounds_route<int32_t, true>)
+                        : (perm_bytes == 2 ? (void*)k_rounds_route<uint16_t, false> : (void*)k_rounds_route<int32_t, false>);
+  RW_CUDA(cudaFuncSetAttribute(route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)route_smem));
+  RFinalArgs fa{};
+  fa.rounds = rounds;
+  fa.mode = plan.mode;
+  fa.scale = p.scale;
+  for (int r = 0; r < rounds; ++r) fa.bytes[r] = plan.round_bytes[r];
+  for (int64_t off = 0; off < batch; off += kmax) {
+    const int64_t cnt_o = std::min(kmax, batch - off);
+    RRouteArgs ra{cnt_o, off, n, rounds, plan.pairing == RW_PAIRING_XOR ? 1 : 0, R,
+                  reinterpret_cast<unsigned long long*>(err_slot), keys, key_bytes, zero_key, 0};
+    const int rgrid = (int)std::min<int64_t>(cnt_o, (int64_t)sms * 8);
+    const char* perms = static_cast<const char*>(d_perms) + (size_t)off * n * perm_bytes;
+    ra.aligned = (reinterpret_cast<uintptr_t>(perms) & 15) == 0 ? 1 : 0;
+    void* args[] = {&ra, (void*)&perms, (void*)&buf};
+    RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), args, route_smem, st));
+    RScoreArgs sa{cnt_o, n, rounds, nblocks, stages, keys};
+    const int sgrid = (int)std::min<int64_t>(sms, nblocks * ((cnt_o + kRStageOrders - 1) / kRStageOrders));
+    switch (p.storage) {
+      case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
+      case RW_STORAGE_F32: launch_score_r<float>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
+      default: launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
+    }
+    RW_CUDA(cudaGetLastError());
+    fa.count = cnt_o;
+    const int fgrid = (int)((cnt_o + 127) / 128);
+    switch (p.storage) {
+      case RW_STORAGE_U16: k_rounds_finalize<uint16_t><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
+      case RW_STORAGE_F32: k_rounds_finalize<float><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
+      default: k_rounds_finalize<double><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
+    }
+    RW_CUDA(cudaGetLastError());
+  }
+  return true;
+}
+
+}  // namespace rwb

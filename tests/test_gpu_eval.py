@@ -174,7 +174,41 @@ def test_ring_paths_agree(cfg, kind):
         np.testing.assert_allclose(probs[pth].evaluate_batch(lat, perms), want, rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("cfg,path", [("C1", "auto"), ("C4", "auto"), ("C4", "cluster"), ("C4", "l2")])
+@pytest.mark.parametrize("cfg,kind", [("C4", "fixed"), ("C4", "f32"), ("C4", "f64"), ("C5", "fixed"), ("C5", "f32")])
+def test_hd_paths_agree(port, cfg, kind):
+    """Halving-doubling beyond shared memory: the transpose path (per-round
+    partner slices, rw_rounds_transpose.cu) equals the L2-gather path bit for
+    bit (max-of-rounds is exact on every storage), for both pairings and both
+    cost modes, on full and partial chunks, and matches the oracle."""
+    import torch
+    m = fixtures.config_matrix(cfg, kind)
+    n = m.shape[0]
+    l2, tr = rw.Problem(m), rw.Problem(m)
+    l2.set_path("l2")
+    tr.set_path("transpose")
+    rng = np.random.default_rng(23)
+    size = fixtures.size_for(kind)
+    for pairing in (rw.HdPairing.PaperFormula, rw.HdPairing.XorPairing):
+        for mode in (rw.CostMode.LatencyTimesSize, rw.CostMode.LatencyOnly):
+            spec = rw.CollectiveSpec(rw.Algorithm.HalvingDoubling, n, size, 2, mode, pairing)
+            for count in (1, 7, 700) if cfg == "C5" else (1, 129, 3000):
+                perms = np.array([rng.permutation(n) for _ in range(count)], dtype=np.int32)
+                want = l2.evaluate_batch(spec, perms)
+                got = tr.evaluate_batch(spec, perms)
+                assert np.array_equal(got, want), (pairing, mode, count)
+            ospec = make_spec(1, n, size, 2, int(mode), int(pairing))
+            assert np.array_equal(got[:3], port.evaluate_batch(m, perms[:3], ospec))
+            d = torch.from_numpy(perms.astype(np.uint16).view(np.int16)).cuda()
+            c = torch.empty(count, dtype=torch.float64, device="cuda")
+            tr.evaluate_batch_device(spec, d.data_ptr(), 2, count, c.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            tr.sync_errors()
+            assert np.array_equal(c.cpu().numpy(), want), (pairing, mode, "u16")
+
+
+@pytest.mark.parametrize("cfg,path", [("C1", "auto"), ("C4", "auto"), ("C4", "cluster"), ("C4", "l2"),
+                                      ("C5", "transpose")])
 def test_invalid_orders_raise_domain_error(cfg, path):
     m = fixtures.config_matrix(cfg, "fixed")
     n = m.shape[0]
