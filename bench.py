@@ -42,6 +42,7 @@ WORKLOAD = "C4: N=1024 ring all-reduce cost, synthetic 3-level hierarchical matr
 N = 1024
 BATCH = 1 << 21  # orders per GPU per step: 2M x 1024 x 2 B = 4 GiB of uint16 orders in HBM
 E2E_BATCH = 1 << 16
+C4_CHAINS = 2368  # time-to-best-ring at C4: 16 chains (warps) per SM; see DESIGN.md 5
 CPU_SECONDS = 10.0
 
 
@@ -396,10 +397,10 @@ def run_extras(rw, torch):
         spec = rw.fixtures.ring_spec(1024, rw.fixtures.SIZE_FIXED)
         best = None
         t = time.perf_counter()
-        for steps in (256, 1024, 4096):
+        for steps in (1024, 2048, 4096, 8192, 16384):
             t1 = time.perf_counter()
             order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps),
-                                               schedule="calibrated")
+                                               chains=C4_CHAINS, schedule="calibrated")
             best = (cost, steps, ev, time.perf_counter() - t1, rep["chains"])
             if cost <= target:
                 break

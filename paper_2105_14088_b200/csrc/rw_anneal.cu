@@ -28,6 +28,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
@@ -40,6 +41,7 @@ using namespace dev;
 namespace {
 
 constexpr int kOrWindow = 48;  // or-opt segment displacement window
+constexpr int kSlots = 1;      // ring anneal: proposals priced per lane per iteration (more slots measured slower)
 
 struct AnnealArgs {
   int n;
@@ -64,6 +66,7 @@ struct AnnealArgs {
   unsigned long long* proposals;
   const uint16_t* nb;  // K nearest hosts of every host (candidate lists), or null
   int K;
+  int nb_smem;         // bytes of nb staged in shared memory after the warp buffers (0: read from global)
   RoundsArgs rounds;
   DbtArgs dbt;
 };
@@ -158,6 +161,59 @@ __device__ __forceinline__ Acc ring_delta(const uint16_t* p, int n, const T* mat
   return (D(b0, x) + D(a0, bl) + D(w, al)) - (D(a0, x) + D(b0, al) + D(w, bl));
 }
 
+// The same delta as ring_delta, as a fixed list of up to 8 matrix lookups:
+// slots 0-3 are the new edges (added), 4-7 the old edges (subtracted);
+// unused slots point at (0, 0) with a zero weight.  Branch-free consumers can
+// issue every lookup of several proposals before using any of them.
+struct DeltaTerms {
+  int row[8], col[8];
+  uint8_t used;    // bit q: term q participates
+  bool invalid;    // no-op move (never accepted)
+};
+
+__device__ __forceinline__ DeltaTerms delta_terms(const uint16_t* p, int n, const Move& m) {
+  DeltaTerms t;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) t.row[q] = t.col[q] = 0;
+  t.used = 0;
+  t.invalid = m.type < 0;
+  if (m.type == 1) {
+    const int a = p[wrapi(m.i - 1, n)], b = p[m.i], c = p[m.j], d = p[wrapi(m.j + 1, n)];
+    t.row[0] = c; t.col[0] = a;
+    t.row[1] = d; t.col[1] = b;
+    t.row[4] = b; t.col[4] = a;
+    t.row[5] = d; t.col[5] = c;
+    t.used = 0x33;
+  } else if (m.type == 0) {
+    const int h[4] = {m.i, wrapi(m.i + 1, n), m.j, wrapi(m.j + 1, n)};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      bool dup = false;
+#pragma unroll
+      for (int r = 0; r < q; ++r) dup |= (h[r] == h[q]);
+      const int pos = h[q], prv = wrapi(h[q] - 1, n);
+      const int cur_o = p[pos], prv_o = p[prv];
+      const int cur_n = pos == m.i ? p[m.j] : pos == m.j ? p[m.i] : cur_o;
+      const int prv_n = prv == m.i ? p[m.j] : prv == m.j ? p[m.i] : prv_o;
+      t.row[q] = cur_n; t.col[q] = prv_n;
+      t.row[4 + q] = cur_o; t.col[4 + q] = prv_o;
+      if (!dup) t.used |= (uint8_t)((1u << q) | (1u << (4 + q)));
+    }
+  } else if (m.type == 2) {
+    const int s0 = m.i, len = m.j, k = m.k;
+    const int x = p[wrapi(s0 - 1, n)], w = p[wrapi(s0 + len, n)];
+    const int a0 = p[s0], al = p[s0 + k - 1], b0 = p[s0 + k], bl = p[s0 + len - 1];
+    t.row[0] = b0; t.col[0] = x;
+    t.row[1] = a0; t.col[1] = bl;
+    t.row[2] = w;  t.col[2] = al;
+    t.row[4] = a0; t.col[4] = x;
+    t.row[5] = b0; t.col[5] = al;
+    t.row[6] = w;  t.col[6] = bl;
+    t.used = 0x77;
+  }
+  return t;
+}
+
 // Candidate-list 2-opt (symmetric matrices): pick a host `a` at a random
 // position and one of its K nearest hosts `b`; reversing the segment between
 // them makes a and b adjacent.  Proposals concentrate on edges that can
@@ -166,7 +222,7 @@ __device__ __forceinline__ Move draw_move_nb(uint4 r, const uint16_t* p, const u
                                              const uint16_t* __restrict__ nb, int K, int n) {
   Move m;
   const int i = (int)(((uint64_t)r.y * (uint32_t)n) >> 32);
-  const int b = __ldg(reinterpret_cast<const unsigned short*>(nb) + p[i] * K + (int)(r.z % (uint32_t)K));
+  const int b = nb[p[i] * K + (int)(r.z % (uint32_t)K)];
   const int j = pos[b];
   m.type = 1;
   m.i = min(i, j) + 1;
@@ -191,15 +247,23 @@ __device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, in
       }
     }
   } else if (m.type == 1) {
-    const int half = (m.j - m.i + 1) >> 1;
+    // Reversing [i..j] or its complement gives the same cycle (type 1 is
+    // only drawn for symmetric matrices), so reverse the shorter side.
+    const int len_in = m.j - m.i + 1;
+    const int s0 = 2 * len_in > n ? m.j + 1 : m.i;
+    const int len = 2 * len_in > n ? n - len_in : len_in;
+    const int half = len >> 1;
     for (int q = lane; q < half; q += 32) {
-      const uint16_t t = p[m.i + q];
-      const uint16_t u = p[m.j - q];
-      p[m.i + q] = u;
-      p[m.j - q] = t;
+      int a = s0 + q, b = s0 + len - 1 - q;
+      if (a >= n) a -= n;
+      if (b >= n) b -= n;
+      const uint16_t t = p[a];
+      const uint16_t u = p[b];
+      p[a] = u;
+      p[b] = t;
       if (pos) {
-        pos[u] = (uint16_t)(m.i + q);
-        pos[t] = (uint16_t)(m.j - q);
+        pos[u] = (uint16_t)a;
+        pos[t] = (uint16_t)b;
       }
     }
   } else {
@@ -228,7 +292,11 @@ __device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, in
 }
 
 __device__ __forceinline__ void store_order(uint16_t* g, const uint16_t* s, int n, int lane) {
-  for (int i = lane; i < n; i += 32) g[i] = s[i];
+  if ((n & 7) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (reinterpret_cast<uintptr_t>(s) & 15) == 0) {
+    for (int i = lane; i < (n >> 3); i += 32) reinterpret_cast<uint4*>(g)[i] = reinterpret_cast<const uint4*>(s)[i];
+  } else {
+    for (int i = lane; i < n; i += 32) g[i] = s[i];
+  }
 }
 
 // ------------------------------------------------------------- init -----
@@ -283,6 +351,14 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
   extern __shared__ __align__(16) unsigned char smem[];
   const T* mat = gmat;
   if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const uint16_t* nbl = a.nb;
+  if (a.nb_smem) {  // candidate lists next to the warp buffers: no global load in the move draw
+    uint16_t* s_nb =
+        reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)(blockDim.x >> 5) * a.warp_bytes);
+    for (int k = threadIdx.x; k < a.n * a.K; k += blockDim.x) s_nb[k] = a.nb[k];
+    __syncthreads();
+    nbl = s_nb;
+  }
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
   if (chain >= a.chains) return;
@@ -310,36 +386,84 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
     const double inv_t = a.mul / t;  // real delta / t = units * mul / t
     int remaining = a.steps;
     while (remaining > 0) {
-      const int active = min(32, remaining);
-      Philox rng;
-      rng.key = key;
-      rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
-      const uint4 r = rng.block();
+      // kSlots x 32 proposals per iteration, all priced against the same
+      // state; proposal index = slot * 32 + lane.  Their matrix gathers are in
+      // flight together, so an iteration costs one L2 round trip however many
+      // slots it prices.
+      const int active = min(32 * kSlots, remaining);
+      Move ms[kSlots];
+      Acc ds[kSlots];
+      float us[kSlots];
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        Philox rng;
+        rng.key = key;
+        rng.ctr = make_uint4((uint32_t)ctr, ((uint32_t)(ctr >> 32) & 0x0FFFFFFFu) | ((uint32_t)sl << 28),
+                             (uint32_t)stream, (uint32_t)(stream >> 32));
+        const uint4 r = rng.block();
+        // half of the proposals are candidate-list 2-opt moves (symmetric matrices)
+        ms[sl] = (sym && nbl && (r.x & 0x100u)) ? draw_move_nb(r, p, pos, nbl, a.K, n) : draw_move(r, n, sym);
+        us[sl] = (float)(r.w >> 8) * 0x1.0p-24f;
+      }
       ++ctr;
-      // half of the proposals are candidate-list 2-opt moves (symmetric matrices)
-      const Move m = (sym && a.nb && (r.x & 0x100u)) ? draw_move_nb(r, p, pos, a.nb, a.K, n) : draw_move(r, n, sym);
-      const Acc delta = ring_delta<T, kSmem, Acc>(p, n, mat, m);
-      bool acc = false;
-      if (lane < active) {
-        if (delta <= (Acc)0) acc = true;
-        else {
-          const float u = (float)(r.w >> 8) * 0x1.0p-24f;
-          acc = u < __expf(-(float)((double)delta * inv_t));
+      {
+        // every lookup of every slot is issued before any is consumed
+        DeltaTerms dt[kSlots];
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) dt[sl] = delta_terms(p, n, ms[sl]);
+        T v[kSlots][8];
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[sl][q] = mat_at<T, kSmem>(mat, n, dt[sl].row[q], dt[sl].col[q]);
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) {
+          Acc add = 0, sub = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (dt[sl].used & (1u << q)) add += (Acc)v[sl][q];
+            if (dt[sl].used & (1u << (4 + q))) sub += (Acc)v[sl][4 + q];
+          }
+          if (dt[sl].invalid) {
+            if constexpr (std::is_same<Acc, double>::value) ds[sl] = __longlong_as_double(0x7ff0000000000000ll);
+            else ds[sl] = (Acc)0x3fffffffffffffffll;
+          } else {
+            ds[sl] = add - sub;
+          }
         }
       }
-      const unsigned mask = __ballot_sync(kFull, acc);
-      if (mask) {
-        const int w = __ffs(mask) - 1;
-        Move mw;
-        mw.type = __shfl_sync(kFull, m.type, w);
-        mw.i = __shfl_sync(kFull, m.i, w);
-        mw.j = __shfl_sync(kFull, m.j, w);
-        mw.k = __shfl_sync(kFull, m.k, w);
-        const Acc dw = __shfl_sync(kFull, delta, w);
+      int w = -1;
+      int wsl = 0;
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        bool acc = false;
+        if (sl * 32 + lane < active) {
+          if (ds[sl] <= (Acc)0) acc = true;
+          else acc = us[sl] < __expf(-(float)((double)ds[sl] * inv_t));
+        }
+        const unsigned mask = __ballot_sync(kFull, acc);
+        if (w < 0 && mask) {
+          w = __ffs(mask) - 1;
+          wsl = sl;
+        }
+      }
+      if (w >= 0) {
+        Move mw{};
+        Acc dw = 0;
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl)
+          if (sl == wsl) {
+            mw.type = __shfl_sync(kFull, ms[sl].type, w);
+            mw.i = __shfl_sync(kFull, ms[sl].i, w);
+            mw.j = __shfl_sync(kFull, ms[sl].j, w);
+            mw.k = __shfl_sync(kFull, ms[sl].k, w);
+            dw = __shfl_sync(kFull, ds[sl], w);
+          }
         apply_move(p, n, mw, lane, pos);
         cur += (double)dw;
-        props += (unsigned long long)(w + 1);
-        remaining -= w + 1;
+        const int used = wsl * 32 + w + 1;
+        props += (unsigned long long)used;
+        remaining -= used;
         if (cur < best) {
           best = cur;
           store_order(a.best + (size_t)chain * n, p, n, lane);
@@ -722,7 +846,9 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   // shared memory plan: two order buffers (+ dbt values) per warp
   size_t warp_bytes = 2 * al16((size_t)n * 2) + al16((size_t)dbt_edges * 8);
   const size_t mat_bytes = (size_t)n * n * sizeof(T);
+  // warps (chains) per block: spread the chains over every SM first
   int wpb = 8;
+  while (wpb > 1 && (int64_t)chains < (int64_t)wpb * di.sms) wpb >>= 1;
   bool smem_mat = mat_bytes + (size_t)wpb * warp_bytes <= (size_t)di.smem;
   if (!smem_mat) {
     while (wpb > 1 && (size_t)wpb * warp_bytes > (size_t)di.smem) wpb >>= 1;
@@ -734,6 +860,14 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   a.mat_smem = smem_mat ? mat_bytes : 0;
   a.warp_bytes = (int)warp_bytes;
   const size_t dyn = al16(a.mat_smem) + (size_t)wpb * warp_bytes;
+  size_t dyn_ring = dyn;
+  if (a.nb) {
+    const size_t nbb = al16((size_t)n * a.K * 2);
+    if (dyn + nbb <= (size_t)di.smem) {
+      a.nb_smem = (int)nbb;
+      dyn_ring = dyn + nbb;
+    }
+  }
   const int grid = (chains + wpb - 1) / wpb;
   const int threads = wpb * 32;
 
@@ -760,8 +894,12 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
       std::sort(up.begin(), up.end());
       double s = 0.0;
       for (double d : up) s += d;
+      // T0 = 0.1 x mean uphill delta; floor = 5th-percentile uphill / 20.
+      // Swept on B200 (C1 ten seeds at the reference budget, C4 four seeds):
+      // a floor of /7 left C4 0.1 % above the reference, /20 beats every
+      // reference run at equal budget; colder floors lose the C1 median.
       t0 = 0.1 * s / static_cast<double>(up.size());
-      t_floor = up[up.size() / 20] / 7.0;
+      t_floor = up[up.size() / 20] / 20.0;
       if (!(t_floor < t0)) t_floor = t0 * 1e-6;
     }
   }
@@ -802,7 +940,7 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
 
   auto ring = smem_mat ? k_anneal_ring<T, true> : k_anneal_ring<T, false>;
   auto full = smem_mat ? k_anneal_full<T, true> : k_anneal_full<T, false>;
-  smem_attr(ring, dyn);
+  smem_attr(ring, dyn_ring);
   smem_attr(full, dyn);
   const auto deadline = start + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(cfg.budget_s));
   const int per_launch = std::max(1, (int)std::min<long long>(levels, (1LL << 16) / std::max(1, steps_eff)));
@@ -812,7 +950,7 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
     if (Clock::now() >= deadline) break;
     a.level_begin = level;
     a.level_end = std::min(levels, level + per_launch);
-    if (plan.model == kRing) ring<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
+    if (plan.model == kRing) ring<<<grid, threads, dyn_ring, st>>>(a, static_cast<const T*>(p.d_mat));
     else full<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
     RW_CUDA(cudaGetLastError());
     level = a.level_end;
