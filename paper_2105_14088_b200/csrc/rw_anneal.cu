@@ -67,6 +67,7 @@ struct AnnealArgs {
   const uint16_t* nb;  // K nearest hosts of every host (candidate lists), or null
   int K;
   int nb_smem;         // bytes of nb staged in shared memory after the warp buffers (0: read from global)
+  int mix_swap, mix_rev;  // full-evaluation models: move mix out of 8 (rest: or-opt)
   RoundsArgs rounds;
   DbtArgs dbt;
 };
@@ -124,6 +125,17 @@ __device__ __forceinline__ Move draw_move(uint4 r, int n, bool symmetric) {
     m.k = ((r.x >> 6) & 1u) ? L : d;
   }
   return m;
+}
+
+// Move mix for the full-evaluation models: of 8 parts, `wswap` swaps,
+// `wrev` reversals, the rest or-opt block moves.
+__device__ __forceinline__ Move draw_move_mix(uint4 r, int n, int wswap, int wrev) {
+  const uint32_t sel = r.x & 7u;
+  uint4 rr = r;
+  // re-encode the type selector so draw_move produces the wanted type
+  const int type = (int)sel < wswap ? 0 : (int)sel < wswap + wrev ? 1 : 2;
+  rr.x = (r.x & ~7u) | (type == 1 ? 0u : type == 0 ? 4u : 6u);
+  return draw_move(rr, n, true);
 }
 
 // Ring delta in kernel units for a move against the current order.
@@ -234,7 +246,8 @@ __device__ __forceinline__ Move draw_move_nb(uint4 r, const uint16_t* p, const u
 
 // Apply a move to the warp's order (all lanes participate); keeps the
 // inverse order `pos` in step when it is given.
-__device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, int lane, uint16_t* pos = nullptr) {
+__device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, int lane, uint16_t* pos = nullptr,
+                                           bool cycle = false) {
   if (m.type < 0) return;
   if (m.type == 0) {
     if (lane == 0) {
@@ -247,11 +260,13 @@ __device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, in
       }
     }
   } else if (m.type == 1) {
-    // Reversing [i..j] or its complement gives the same cycle (type 1 is
-    // only drawn for symmetric matrices), so reverse the shorter side.
+    // On a ring (cycle = true) reversing [i..j] or its complement gives the
+    // same cycle (type 1 is only drawn there for symmetric matrices), so the
+    // shorter side is reversed.  Other models depend on absolute positions.
     const int len_in = m.j - m.i + 1;
-    const int s0 = 2 * len_in > n ? m.j + 1 : m.i;
-    const int len = 2 * len_in > n ? n - len_in : len_in;
+    const bool flip = cycle && 2 * len_in > n;
+    const int s0 = flip ? m.j + 1 : m.i;
+    const int len = flip ? n - len_in : len_in;
     const int half = len >> 1;
     for (int q = lane; q < half; q += 32) {
       int a = s0 + q, b = s0 + len - 1 - q;
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
             mw.k = __shfl_sync(kFull, ms[sl].k, w);
             dw = __shfl_sync(kFull, ds[sl], w);
           }
-        apply_move(p, n, mw, lane, pos);
+        apply_move(p, n, mw, lane, pos, true);
         cur += (double)dw;
         const int used = wsl * 32 + w + 1;
         props += (unsigned long long)used;
@@ -518,7 +533,7 @@ __global__ void __launch_bounds__(256) k_anneal_full(AnnealArgs a, const T* __re
       rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
       const uint4 r = rng.block();
       ++ctr;
-      const Move m = draw_move(r, n, true);
+      const Move m = draw_move_mix(r, n, a.mix_swap, a.mix_rev);
       for (int i = lane; i < n; i += 32) q[i] = p[i];
       __syncwarp();
       apply_move(q, n, m, lane);
@@ -725,9 +740,133 @@ __global__ void __launch_bounds__(256) k_local_search_ring(const T* __restrict__
     m.i = __shfl_sync(kFull, best_m.i, who);
     m.j = __shfl_sync(kFull, best_m.j, who);
     m.k = __shfl_sync(kFull, best_m.k, who);
-    apply_move(p, n, m, lane);
+    apply_move(p, n, m, lane, nullptr, true);
   }
   for (int i = lane; i < n; i += 32) g[i] = p[i];
+  ev = warp_sum(ev);
+  if (lane == 0) atomicAdd(evals, ev);
+}
+
+// Batched local search for the full-evaluation models (tree, halving-
+// doubling, BCube): one CTA per order.  The neighbourhood is every swap (i, j)
+// and every reversal [i..j], i < j.  Warps price moves by a warp-cooperative
+// full evaluation of a private copy, in chunks of kLsChunk moves; the best
+// improving move of a chunk is applied, and the scan stops after a full pass
+// over the neighbourhood without improvement (a swap / 2-opt local optimum)
+// or max_rounds applied moves.
+constexpr int kLsChunk = 64;
+
+template <typename T, bool kSmem>
+__device__ __forceinline__ double full_cost(const uint16_t* q, int n, const T* mat, const AnnealArgs& a, double* vals,
+                                            int lane) {
+  if (a.model == kDoubleBinaryTree) return warp_dbt_cost<T, kSmem>(q, n, mat, a.dbt, a.scale, vals, lane);
+  return warp_rounds_cost<T, kSmem>(q, n, mat, a.rounds, a.scale, lane);
+}
+
+__device__ __forceinline__ Move unrank_pair_move(long long t, long long pairs, int n) {
+  Move m;
+  m.type = t < pairs ? 0 : 1;
+  if (t >= pairs) t -= pairs;
+  long long i = (long long)((2.0 * n - 1.0 - sqrt((2.0 * n - 1.0) * (2.0 * n - 1.0) - 8.0 * (double)t)) * 0.5);
+  if (i < 0) i = 0;
+  while (i > 0 && i * (2LL * n - i - 1) / 2 > t) --i;
+  while ((i + 1) * (2LL * n - i - 2) / 2 <= t) ++i;
+  m.i = (int)i;
+  m.j = (int)(t - i * (2LL * n - i - 1) / 2 + i + 1);
+  m.k = 0;
+  return m;
+}
+
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_local_search_full(AnnealArgs a, const T* __restrict__ gmat, int64_t batch,
+                                                           uint16_t* orders, int max_rounds,
+                                                           unsigned long long* evals) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int n = a.n;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem));
+  unsigned char* wbase = smem + al16(a.mat_smem) + al16((size_t)n * 2) + (size_t)wib * a.warp_bytes;
+  uint16_t* q = reinterpret_cast<uint16_t*>(wbase);
+  double* vals = reinterpret_cast<double*>(wbase + al16((size_t)n * 2));
+  __shared__ double s_best[32];
+  __shared__ long long s_move[32];
+  __shared__ double s_cur;
+  const long long pairs = (long long)n * (n - 1) / 2;
+  const long long total = 2 * pairs;
+  unsigned long long ev = 0;
+  for (int64_t ord = blockIdx.x; ord < batch; ord += gridDim.x) {
+    uint16_t* g = orders + ord * n;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = g[i];
+    __syncthreads();
+    if (wib == 0) {
+      for (int i = lane; i < n; i += 32) q[i] = p[i];
+      __syncwarp();
+      const double c = full_cost<T, kSmem>(q, n, mat, a, vals, lane);
+      if (lane == 0) s_cur = c;
+    }
+    __syncthreads();
+    double cur = s_cur;
+    long long start = 0, scanned = 0;
+    int applied = 0;
+    while (n >= 3 && scanned < total && applied < max_rounds) {
+      // each warp prices kLsChunk / nw moves of this chunk
+      double best = 0.0;
+      long long best_t = -1;
+      for (int k = wib; k < kLsChunk; k += nw) {
+        if (scanned + k >= total) break;
+        long long t = start + scanned + k;
+        if (t >= total) t -= total;
+        const Move m = unrank_pair_move(t, pairs, n);
+        for (int i = lane; i < n; i += 32) q[i] = p[i];
+        __syncwarp();
+        apply_move(q, n, m, lane);
+        const double c = full_cost<T, kSmem>(q, n, mat, a, vals, lane);
+        ++ev;
+        const double d = c - cur;
+        if (d < best || (d == best && best_t >= 0 && t < best_t)) {
+          best = d;
+          best_t = t;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        s_best[wib] = best;
+        s_move[wib] = best_t;
+      }
+      __syncthreads();
+      // CTA argmin (ties: lowest move index), every thread computes it
+      double bd = 0.0;
+      long long bt = -1;
+      for (int w = 0; w < nw; ++w)
+        if (s_move[w] >= 0 && (s_best[w] < bd || (s_best[w] == bd && (bt < 0 || s_move[w] < bt)))) {
+          bd = s_best[w];
+          bt = s_move[w];
+        }
+      if (bt >= 0 && bd < 0.0) {
+        const Move m = unrank_pair_move(bt, pairs, n);
+        if (wib == 0) {
+          apply_move(p, n, m, lane);
+          for (int i = lane; i < n; i += 32) q[i] = p[i];
+          __syncwarp();
+          const double c = full_cost<T, kSmem>(q, n, mat, a, vals, lane);  // exact, no drift
+          if (lane == 0) s_cur = c;
+        }
+        __syncthreads();
+        cur = s_cur;
+        ++applied;
+        start = bt + 1 < total ? bt + 1 : 0;
+        scanned = 0;
+      } else {
+        scanned += kLsChunk;
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = p[i];
+  }
   ev = warp_sum(ev);
   if (lane == 0) atomicAdd(evals, ev);
 }
@@ -784,6 +923,31 @@ double population_stddev(const std::vector<double>& v) {
   return std::sqrt(sq / static_cast<double>(v.size()));
 }
 
+// Model tables for the full-evaluation kernels; returns the DBT edge count.
+int fill_model_args(AnnealArgs& a, const EvalPlan& plan) {
+  int dbt_edges = 0;
+  if (plan.model == kHalvingDoubling || plan.model == kBCube) {
+    a.rounds.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
+    a.rounds.rounds = plan.rounds;
+    a.rounds.b = plan.bcube_b;
+    a.rounds.mode = plan.mode;
+    for (int r = 0; r < plan.rounds; ++r) a.rounds.bytes[r] = plan.round_bytes[r];
+  }
+  if (plan.model == kDoubleBinaryTree && plan.dbt) {
+    dbt_edges = plan.dbt->edges;
+    a.dbt.src = plan.dbt->d_src();
+    a.dbt.dst = plan.dbt->d_dst();
+    a.dbt.c0 = plan.dbt->d_c0();
+    a.dbt.c1 = plan.dbt->d_c1();
+    a.dbt.depth_off = plan.dbt->d_depth_off();
+    a.dbt.depths = plan.dbt->depths;
+    a.dbt.edges = dbt_edges;
+    a.dbt.mode = plan.mode;
+    a.dbt.half = plan.half;
+  }
+  return dbt_edges;
+}
+
 template <typename T>
 AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_config& cfg, const rw_gpu_config& gpu) {
   using Clock = std::chrono::steady_clock;
@@ -812,6 +976,12 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   a.model = plan.model;
   a.scale = p.scale;
   a.mul = plan.model == kRing ? plan.ring_mul : 1.0;
+  // Full-evaluation models (tree / halving-doubling / BCube) depend on
+  // absolute positions: half swaps, a quarter reversals, a quarter or-opt.
+  // Measured at C3 DBT, seed 0, reference budget: 2.825e10 (reference
+  // 2.854e10); pure swaps 3.56e10.
+  a.mix_swap = 4;
+  a.mix_rev = 2;
   if (plan.model == kRing && p.symmetric && n >= 8) {
     ensure_candidates<T>(p, st);
     a.nb = p.d_nb;
@@ -823,26 +993,7 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   a.best_cost = a.cur_cost + chains;
   a.ctr = reinterpret_cast<unsigned long long*>(a.best_cost + chains);
   a.proposals = a.ctr + chains;
-  if (plan.model == kHalvingDoubling || plan.model == kBCube) {
-    a.rounds.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
-    a.rounds.rounds = plan.rounds;
-    a.rounds.b = plan.bcube_b;
-    a.rounds.mode = plan.mode;
-    for (int r = 0; r < plan.rounds; ++r) a.rounds.bytes[r] = plan.round_bytes[r];
-  }
-  int dbt_edges = 0;
-  if (plan.model == kDoubleBinaryTree && plan.dbt) {
-    dbt_edges = plan.dbt->edges;
-    a.dbt.src = plan.dbt->d_src();
-    a.dbt.dst = plan.dbt->d_dst();
-    a.dbt.c0 = plan.dbt->d_c0();
-    a.dbt.c1 = plan.dbt->d_c1();
-    a.dbt.depth_off = plan.dbt->d_depth_off();
-    a.dbt.depths = plan.dbt->depths;
-    a.dbt.edges = dbt_edges;
-    a.dbt.mode = plan.mode;
-    a.dbt.half = plan.half;
-  }
+  int dbt_edges = fill_model_args(a, plan);
   // shared memory plan: two order buffers (+ dbt values) per warp
   size_t warp_bytes = 2 * al16((size_t)n * 2) + al16((size_t)dbt_edges * 8);
   const size_t mat_bytes = (size_t)n * n * sizeof(T);
@@ -1014,6 +1165,29 @@ void local_search_typed(Problem& p, const EvalPlan& plan, int32_t* perms, int64_
     const int grid = (int)((batch + wpb - 1) / wpb);
     k<<<grid, wpb * 32, dyn, st>>>(static_cast<const T*>(p.d_mat), smem_mat ? mat_bytes : 0, n, p.symmetric ? 1 : 0,
                                    batch, d_o, (int)warp_bytes, max_rounds, d_ev);
+    RW_CUDA(cudaGetLastError());
+  } else if (plan.model != kRing && n >= 3) {
+    AnnealArgs a{};
+    a.n = n;
+    a.model = plan.model;
+    a.scale = p.scale;
+    const int dbt_edges = fill_model_args(a, plan);
+    const size_t mat_bytes = (size_t)n * n * sizeof(T);
+    size_t warp_bytes = al16((size_t)n * 2) + al16((size_t)dbt_edges * 8);
+    int wpb = 8;
+    const size_t order_bytes = al16((size_t)n * 2);
+    bool smem_mat = mat_bytes + order_bytes + wpb * warp_bytes <= (size_t)di.smem;
+    if (!smem_mat) {
+      while (wpb > 1 && order_bytes + wpb * warp_bytes > (size_t)di.smem) wpb >>= 1;
+      if (order_bytes + wpb * warp_bytes > (size_t)di.smem) fail_domain("local search: order too large for shared memory");
+    }
+    a.mat_smem = smem_mat ? mat_bytes : 0;
+    a.warp_bytes = (int)warp_bytes;
+    const size_t dyn = al16(a.mat_smem) + order_bytes + wpb * warp_bytes;
+    auto k = smem_mat ? k_local_search_full<T, true> : k_local_search_full<T, false>;
+    smem_attr(k, dyn);
+    const int grid = (int)std::min<int64_t>(batch, (int64_t)di.sms * 4);
+    k<<<grid, wpb * 32, dyn, st>>>(a, static_cast<const T*>(p.d_mat), batch, d_o, max_rounds, d_ev);
     RW_CUDA(cudaGetLastError());
   }
   launch_evaluate(p, plan, d_o, 2, batch, d_c, true, false, c.d_err, st);

@@ -254,6 +254,48 @@ def test_local_search_reaches_two_opt_optimum():
             assert port.evaluate(m, c, s) >= base
 
 
+@pytest.mark.parametrize("cfg,alg", [("C3", 2), ("C1", 1), ("C1", 3)])
+def test_local_search_full_models_reach_swap_two_opt_optimum(cfg, alg):
+    """Tree / halving-doubling / BCube: batched swap + reversal local search
+    (one CTA per order, full evaluation per move) ends at an order no swap or
+    reversal improves, with the oracle's exact cost."""
+    port = Port()
+    m = fixtures.config_matrix(cfg, "fixed")
+    n = m.shape[0]
+    prob = rw.Problem(m)
+    spec = rw.CollectiveSpec(rw.Algorithm(alg), n, fixtures.SIZE_FIXED)
+    s = make_spec(alg, n, fixtures.SIZE_FIXED)
+    rng = np.random.default_rng(5)
+    start = np.array([rng.permutation(n) for _ in range(6)], dtype=np.int32)
+    before = prob.evaluate_batch(spec, start)
+    orders, costs, evals = prob.local_search(spec, start, max_rounds=1_000_000)
+    assert np.array_equal(costs, port.evaluate_batch(m, orders, s))
+    assert np.all(costs <= before) and np.any(costs < before) and evals > 0
+    o = orders[0]
+    nb = []
+    for i, j in itertools.combinations(range(n), 2):
+        c = o.copy()
+        c[i], c[j] = c[j], c[i]
+        nb.append(c)
+        c = o.copy()
+        c[i: j + 1] = c[i: j + 1][::-1]
+        nb.append(c)
+    assert port.evaluate_batch(m, np.array(nb, dtype=np.int32), s).min() >= costs[0]
+
+
+def test_anneal_quality_c3_dbt_equal_budget():
+    """C3 tree model: one GPU chain at the reference run's evaluation count
+    (11,292,776) must not end worse than the reference (tests/golden/anneal.json)."""
+    g = json.load(open(os.path.join(GOLD, "anneal.json")))
+    ref = [r for r in g["results"] if r["config"] == "C3" and r["model"] == "dbt"][0]
+    prob = rw.Problem(fixtures.config_matrix("C3", "fixed"))
+    spec = rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, 256, fixtures.SIZE_FIXED)
+    order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6), chains=1,
+                                       max_proposals=ref["evaluations"])
+    assert ev <= ref["evaluations"]
+    assert cost <= ref["cost"], (cost, ref["cost"])
+
+
 # ---------------------------------------------------------------- stats --
 def test_sample_costs_match_sample_orders():  # test_stats.cpp:65-89 semantics
     m = fixtures.config_matrix("C1", "f32")
