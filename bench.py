@@ -353,9 +353,66 @@ def run_ours(args):
     return 0
 
 
+def time_config(rw, torch, cfg, spec, count, reps=5):
+    """evals/s of one config + model through rw_evaluate_batch_device (uint16
+    orders resident in HBM, CUDA events on the launching stream)."""
+    m = rw.fixtures.config_matrix(cfg, "fixed")
+    n = m.shape[0]
+    prob = rw.Problem(m)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    o = torch.rand((count, n), device="cuda", generator=g).argsort(dim=1).to(torch.int16)
+    c = torch.empty(count, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+    for _ in range(2):
+        prob.evaluate_batch_device(spec, o.data_ptr(), 2, count, c.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        prob.evaluate_batch_device(spec, o.data_ptr(), 2, count, c.data_ptr(), st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    prob.sync_errors()
+    return count * reps / (e0.elapsed_time(e1) / 1000.0)
+
+
+def run_config_extras(rw, torch):
+    """Per-config evaluation throughput and C3 local search."""
+    A, S = rw.Algorithm, rw.fixtures.SIZE_FIXED
+    ref_1t = {"C3_ring": 6.15e4, "C3_dbt": 1.35e5, "C5_hd_xor": 1.16e3, "C5_hd_paper": 1.92e3}  # SURVEY 8(d) [measured]
+    rows = {
+        "C3_ring": ("C3", rw.CollectiveSpec(A.Ring, 256, S), 1 << 21),
+        "C3_dbt": ("C3", rw.CollectiveSpec(A.DoubleBinaryTree, 256, S), 1 << 19),
+        "C5_hd_xor": ("C5", rw.CollectiveSpec(A.HalvingDoubling, 4096, S, 2, rw.CostMode.LatencyTimesSize,
+                                              rw.HdPairing.XorPairing), 1 << 15),
+        "C5_hd_paper": ("C5", rw.CollectiveSpec(A.HalvingDoubling, 4096, S), 1 << 15),
+    }
+    out = {"unit": "evals/s", "orders": "uint16, device resident", "reference_single_thread_container": ref_1t}
+    for k, (cfg, spec, count) in rows.items():
+        out[k] = time_config(rw, torch, cfg, spec, count)
+    # batched local search to a swap/2-opt local optimum, C3, 148 random orders
+    import numpy as np
+    rng = np.random.default_rng(3)
+    m3 = rw.fixtures.config_matrix("C3", "fixed")
+    p3 = rw.Problem(m3)
+    starts = np.array([rng.permutation(256) for _ in range(148)], dtype=np.int32)
+    ls = {}
+    for name, spec in (("ring", rw.CollectiveSpec(A.Ring, 256, S)), ("dbt", rw.CollectiveSpec(A.DoubleBinaryTree, 256, S))):
+        t = time.perf_counter()
+        orders, costs, evals = p3.local_search(spec, starts, max_rounds=1_000_000)
+        dt = time.perf_counter() - t
+        ls[name] = {"orders": len(starts), "seconds": dt, "move_evaluations": int(evals),
+                    "move_evaluations_per_s": evals / dt, "mean_cost": float(costs.mean()),
+                    "start_mean_cost": float(p3.evaluate_batch(spec, starts).mean())}
+    out["local_search_c3"] = ls
+    return out
+
+
 def run_extras(rw, torch):
     """Secondary north-star numbers (single GPU, small): exhaustive N=13 and C1 time-to-best-ring."""
     out = {}
+    out["configs"] = run_config_extras(rw, torch)
     m13 = rw.fixtures.config_matrix("C2")
     M13 = rw.CostMatrix.from_array(m13)
     spec13 = rw.CollectiveSpec(rw.Algorithm.Ring, 13, 1.0)
