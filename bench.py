@@ -288,6 +288,10 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_batch * e2e_steps / float(te.item())
 
+    multi = {}
+    if not args.no_extras:
+        multi = run_multi_extras(rw, torch, dist, rank, world, local, prob, spec, barrier)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -345,12 +349,70 @@ def run_ours(args):
         "clocks": clock,
         "gpu_launches": args.steps * launches_per_step,
         "extras": extras,
+        "multi_gpu_configs": multi,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def run_multi_extras(rw, torch, dist, rank, world, local, prob4, spec4, barrier):
+    """BASELINE configs C4 and C5 at this run's GPU count (every rank works;
+    times are the max over ranks):
+      * C5 halving-doubling (xor) scoring, weak scaling: 16K orders per GPU;
+      * C4 annealing with 65,536 chains split over the GPUs (strong scaling in
+        chains), winner picked by NCCL all-reduce MIN (cost, chain) + broadcast."""
+    from paper_2105_14088_b200 import dist as rwd
+    out = {}
+
+    def max_over_ranks(t):
+        x = torch.tensor([t], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        return float(x.item())
+
+    A = rw.Algorithm
+    m5 = rw.fixtures.config_matrix("C5", "fixed")
+    p5 = rw.Problem(m5, device=local)
+    spec5 = rw.CollectiveSpec(A.HalvingDoubling, 4096, rw.fixtures.SIZE_FIXED, 2, rw.CostMode.LatencyTimesSize,
+                              rw.HdPairing.XorPairing)
+    count, reps = 1 << 14, 4
+    o5 = make_orders_device(torch, count, 4096, seed=77 + rank)
+    c5 = torch.empty(count, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+    p5.evaluate_batch_device(spec5, o5.data_ptr(), 2, count, c5.data_ptr(), st.cuda_stream)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        p5.evaluate_batch_device(spec5, o5.data_ptr(), 2, count, c5.data_ptr(), st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    p5.sync_errors()
+    t5 = max_over_ranks(e0.elapsed_time(e1) / 1000.0)
+    out["c5_hd_xor"] = {"value": world * count * reps / t5, "unit": "evals/s", "n_gpus": world,
+                        "orders_per_gpu": count * reps, "scaling": "weak",
+                        "kernel": "k_rounds_route + k_rounds_score + k_rounds_finalize (transpose path)"}
+    del o5, c5, p5
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "anneal_c4.json")))
+    target = min(r["cost"] for r in g["results"])
+    chains_total, steps = 65536, 2048
+    barrier()
+    t0 = time.perf_counter()
+    sol, rep = rwd.anneal_sharded(prob4, spec4, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps),
+                                  chains_total, schedule="calibrated")
+    barrier()
+    ta = max_over_ranks(time.perf_counter() - t0)
+    out["c4_anneal_65536_chains"] = {"seconds": ta, "cost": sol.cost, "target_reference_min_seeds0_3": target,
+                                     "reached": sol.cost <= target, "chains_total": chains_total,
+                                     "chains_per_gpu": chains_total // world, "steps_per_level": steps,
+                                     "evaluations": sol.evaluations, "winner_chain": rep["winner_chain"],
+                                     "n_gpus": world, "scaling": "strong (fixed total chains)",
+                                     "argmin": "NCCL all-reduce MIN on (cost, chain id), broadcast of the order"}
+    return out
 
 
 def time_config(rw, torch, cfg, spec, count, reps=5):

@@ -120,7 +120,7 @@ def brute_force_sharded(prob: Problem, spec: CollectiveSpec, threshold: int = 10
 
 
 def anneal_sharded(prob: Problem, spec: CollectiveSpec, cfg: SolverConfig, chains_total: int,
-                   max_proposals: int = 0):
+                   max_proposals: int = 0, schedule: str = "reference"):
     """Simulated annealing with `chains_total` chains split over the ranks.
     Returns (Solution, report) where evaluations are summed over ranks."""
     import torch
@@ -129,7 +129,7 @@ def anneal_sharded(prob: Problem, spec: CollectiveSpec, cfg: SolverConfig, chain
     begin, count = shard(chains_total, r, w)
     per_rank_budget = max_proposals * count // max(1, chains_total) if max_proposals else 0
     order, cost, ev, rep = prob.anneal(spec, cfg, chains=count, chain_begin=begin, chain_total=chains_total,
-                                       max_proposals=per_rank_budget)
+                                       max_proposals=per_rank_budget, schedule=schedule)
     best, chain, perm = reduce_argmin(cost, int(rep["winner_chain"]), order, spec.n)
     total_ev = ev
     if w > 1:
