@@ -207,6 +207,36 @@ def test_hd_paths_agree(port, cfg, kind):
             assert np.array_equal(c.cpu().numpy(), want), (pairing, mode, "u16")
 
 
+@pytest.mark.parametrize("n,kind", [(1024, "u16"), (1024, "f64"), (2048, "u16")])
+def test_transpose_paths_on_asymmetric_matrices(port, n, kind):
+    """The transpose paths index blk[host][partner]; asymmetric matrices pin the
+    lookup direction (ring: rtt[p_i][p_{i-1}], cost_model.cpp:59-69; HD:
+    rtt[p_j][p_partner], cost_model.cpp:71-92) against the oracle."""
+    rng = np.random.default_rng(n)
+    if kind == "u16":
+        m = rng.integers(0, 4000, size=(n, n)).astype(np.float64) / 16.0
+    else:
+        m = rng.random((n, n)) * 100.0
+    np.fill_diagonal(m, 0.0)
+    probs = {}
+    for pth in ("l2", "transpose"):
+        probs[pth] = rw.Problem(m)
+        probs[pth].set_path(pth)
+    perms = np.array([rng.permutation(n) for _ in range(300)], dtype=np.int32)
+    specs = [(0, 2, 1, 0), (1, 2, 1, 0), (1, 2, 1, 1), (1, 2, 0, 1)]  # (alg, b, mode, pairing)
+    for alg, b, mode, pair in specs:
+        spec = rw.CollectiveSpec(rw.Algorithm(alg), n, 2.0 ** 20, b, rw.CostMode(mode), rw.HdPairing(pair))
+        want = port.evaluate_batch(m, perms[:40], make_spec(alg, n, 2.0 ** 20, b, mode, pair))
+        got_t = probs["transpose"].evaluate_batch(spec, perms)
+        got_l = probs["l2"].evaluate_batch(spec, perms)
+        if alg == 0 and kind != "u16":
+            np.testing.assert_allclose(got_t[:40], want, rtol=1e-12, atol=0)
+            np.testing.assert_allclose(got_t, got_l, rtol=1e-12, atol=0)
+        else:
+            assert np.array_equal(got_t[:40], want), (alg, mode, pair)
+            assert np.array_equal(got_t, got_l), (alg, mode, pair)
+
+
 @pytest.mark.parametrize("cfg,path", [("C1", "auto"), ("C4", "auto"), ("C4", "cluster"), ("C4", "l2"),
                                       ("C5", "transpose")])
 def test_invalid_orders_raise_domain_error(cfg, path):
