@@ -207,6 +207,34 @@ def test_hd_paths_agree(port, cfg, kind):
             assert np.array_equal(c.cpu().numpy(), want), (pairing, mode, "u16")
 
 
+def test_host_orders_narrowed_pipeline():
+    """Large host batches (>= 4M positions) travel as uint16 narrowed on host
+    threads: results equal the device path, and out-of-range int32 values
+    (negative, >= n, >= 65536 that would wrap into range) are still rejected
+    with the right batch entry."""
+    import torch
+    m = fixtures.config_matrix("C4", "fixed")
+    n = m.shape[0]
+    prob = rw.Problem(m)
+    spec = fixtures.ring_spec(n, fixtures.SIZE_FIXED)
+    rng = np.random.default_rng(9)
+    perms = np.argsort(rng.random((6000, n)), axis=1).astype(np.int32)
+    got = prob.evaluate_batch(spec, perms)
+    d = torch.from_numpy(perms.astype(np.uint16).view(np.int16)).cuda()
+    c = torch.empty(perms.shape[0], dtype=torch.float64, device="cuda")
+    prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, c.cpu().numpy())
+    for row, col, val in ((4321, 17, 65536 + int(perms[4321, 18])), (5999, 0, -1), (3, 5, n),
+                          (2500, 9, int(perms[2500, 10]))):
+        bad = perms.copy()
+        bad[row, col] = val
+        with pytest.raises(rw.DomainError, match=f"batch entry {row}"):
+            prob.evaluate_batch(spec, bad)
+    assert np.array_equal(prob.evaluate_batch(spec, perms), got)  # error slot cleared
+
+
 @pytest.mark.parametrize("n,kind", [(1024, "u16"), (1024, "f64"), (2048, "u16")])
 def test_transpose_paths_on_asymmetric_matrices(port, n, kind):
     """The transpose paths index blk[host][partner]; asymmetric matrices pin the
