@@ -124,13 +124,14 @@ struct ScoreArgs {
   int n;
   int R;           // rows per block
   int nblocks;
-  int cpb;         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
+  int cpb;
+  int stages;        // TMA ring depth
+  int stage_orders;  // orders per TMA stage         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
   double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
   unsigned long long* acc;  // u16 codes: per-order integer sums accumulated atomically (exact)
 };
 
-constexpr int kStageOrders = 128;  // orders per TMA bulk stage
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;
 
 // Pass 2: a CTA keeps rows [b*R, b*R + rows) in shared memory and streams the
 // block's predecessor slices (contiguous in predbuf) through a 4-stage TMA
@@ -143,18 +144,22 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
   const int n = a.n, R = a.R, nb = a.nblocks;
   T* blk = reinterpret_cast<T*>(smem);
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem + al16((size_t)R * n * sizeof(T)));
-  __shared__ __align__(8) uint64_t bars[kStages], mat_bar;
+  __shared__ __align__(8) uint64_t bars[kMaxStages], empty[kMaxStages], mat_bar;
+  const int kStages = a.stages, kStageOrders = a.stage_orders;
   unsigned mat_phase = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t nm1 = (uint32_t)(n - 1);
   constexpr bool kInt = std::is_same<T, uint16_t>::value;
   const size_t stage_elems = (size_t)kStageOrders * R;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&empty[s], nwarps - 1);
+    }
     mbar_init(&mat_bar, 1);
   }
   __syncthreads();
-  unsigned phase_bits = 0;  // parity per stage slot
+  uint32_t g = 0;  // running stage counter of this CTA (same in every role)
 
   // work items: (block, order range)
   const int items = a.cpb > 0 ? nb * a.cpb : nb;
@@ -170,53 +175,63 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
     const uint16_t* base = pred + ((size_t)b * a.count + o0) * R;
     const int64_t total = o1 - o0;
     const int64_t nstage = (total + kStageOrders - 1) / kStageOrders;
-    auto issue = [&](int64_t st) {
-      const int slot = (int)(st % kStages);
-      const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
-      const unsigned bytes = (unsigned)(cnt * R * 2);
-      mbar_expect_tx(&bars[slot], bytes);
-      bulk_g2s(ring + slot * stage_elems, base + (size_t)st * stage_elems, bytes, &bars[slot]);
-    };
-    if (threadIdx.x == 0)
-      for (int64_t st = 0; st < nstage && st < kStages; ++st) issue(st);
-    __syncthreads();  // matrix rows staged
-    for (int64_t st = 0; st < nstage; ++st) {
-      const int slot = (int)(st % kStages);
-      mbar_wait(&bars[slot], (phase_bits >> slot) & 1u);
-      const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
-      const uint16_t* sp = ring + slot * stage_elems;
-      if constexpr (kInt) {
-        // u16 codes: a block partial is < R * 65536 <= 2^32 for R <= 65536/... (R <= 1024 here)
-        for (int k = warp; k < cnt; k += nwarps) {
-          const uint16_t* src = sp + (size_t)k * R;
-          uint32_t acc = 0;
-#pragma unroll 1
-          for (int s = 2 * lane; s < rows; s += 64) {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
-            acc += (uint32_t)blk[s * n + min(w & 0xFFFFu, nm1)] + (uint32_t)blk[(s + 1) * n + min(w >> 16, nm1)];
-          }
-          acc = __reduce_add_sync(kFull, acc);
-          if (lane == 0) atomicAdd(a.acc + o0 + st * kStageOrders + k, (unsigned long long)acc);
-        }
-      } else {
-        for (int k = warp; k < cnt; k += nwarps) {
-          const uint16_t* src = sp + (size_t)k * R;
-          double dacc = 0.0;
-#pragma unroll 1
-          for (int s = 2 * lane; s < rows; s += 64) {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
-            const T v0 = blk[s * n + min(w & 0xFFFFu, nm1)];
-            const T v1 = blk[(s + 1) * n + min(w >> 16, nm1)];
-            dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
-          }
-          const double partial = warp_sum(dacc);
-          if (lane == 0) a.part[(size_t)b * a.count + o0 + st * kStageOrders + k] = partial;
+    // Producer / consumer ring: the last warp issues the bulk copies, gated
+    // by per-slot "empty" barriers that the 31 consumer warps arrive on; no
+    // CTA-wide barrier per stage.
+    if (warp == nwarps - 1) {
+      if (lane == 0) {
+        for (int64_t st = 0; st < nstage; ++st) {
+          const uint32_t gi = g + (uint32_t)st;
+          const int slot = (int)(gi % (uint32_t)kStages);
+          const uint32_t use = gi / (uint32_t)kStages;
+          if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1u);
+          const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
+          const unsigned bytes = (unsigned)(cnt * R * 2);
+          mbar_expect_tx(&bars[slot], bytes);
+          bulk_g2s(ring + slot * stage_elems, base + (size_t)st * stage_elems, bytes, &bars[slot]);
         }
       }
-      phase_bits ^= 1u << slot;
-      __syncthreads();  // slot consumed
-      if (threadIdx.x == 0 && st + kStages < nstage) issue(st + kStages);
+    } else {
+      const int cw = nwarps - 1;
+      for (int64_t st = 0; st < nstage; ++st) {
+        const uint32_t gi = g + (uint32_t)st;
+        const int slot = (int)(gi % (uint32_t)kStages);
+        mbar_wait(&bars[slot], (gi / (uint32_t)kStages) & 1u);
+        const int64_t cnt = min((int64_t)kStageOrders, total - st * kStageOrders);
+        const uint16_t* sp = ring + slot * stage_elems;
+        if constexpr (kInt) {
+          // u16 codes: a block partial is < R * 65536 <= 2^32 (R <= 1024 here)
+          for (int k = warp; k < cnt; k += cw) {
+            const uint16_t* src = sp + (size_t)k * R;
+            uint32_t acc = 0;
+#pragma unroll 1
+            for (int s = 2 * lane; s < rows; s += 64) {
+              const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
+              acc += (uint32_t)blk[s * n + min(w & 0xFFFFu, nm1)] + (uint32_t)blk[(s + 1) * n + min(w >> 16, nm1)];
+            }
+            acc = __reduce_add_sync(kFull, acc);
+            if (lane == 0) atomicAdd(a.acc + o0 + st * kStageOrders + k, (unsigned long long)acc);
+          }
+        } else {
+          for (int k = warp; k < cnt; k += cw) {
+            const uint16_t* src = sp + (size_t)k * R;
+            double dacc = 0.0;
+#pragma unroll 1
+            for (int s = 2 * lane; s < rows; s += 64) {
+              const uint32_t w = *reinterpret_cast<const uint32_t*>(src + s);
+              const T v0 = blk[s * n + min(w & 0xFFFFu, nm1)];
+              const T v1 = blk[(s + 1) * n + min(w >> 16, nm1)];
+              dacc = __dadd_rn(__dadd_rn(dacc, (double)v0), (double)v1);
+            }
+            const double partial = warp_sum(dacc);
+            if (lane == 0) a.part[(size_t)b * a.count + o0 + st * kStageOrders + k] = partial;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
     }
+    g += (uint32_t)nstage;
   }
 }
 
@@ -248,9 +263,8 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
   const size_t budget = (size_t)std::min(optin, 227 * 1024) - 2048;
   const size_t esz = p.elem_bytes();
-  auto fits = [&](int R) {
-    return al16((size_t)R * n * esz) + (size_t)kStages * kStageOrders * R * 2 <= budget;
-  };
+  // A row block must leave room for at least two 128-order stages.
+  auto fits = [&](int R) { return al16((size_t)R * n * esz) + (size_t)2 * 128 * R * 2 <= budget; };
   // row blocks: prefer an exact split of n into multiples of 8 rows
   int nblocks = 0, R = 0;
   for (int nb = 1; nb <= n / 8 && !nblocks; ++nb) {
@@ -266,6 +280,16 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
     R = ((n + nblocks - 1) / nblocks + 7) & ~7;
   }
   if (!nblocks) return false;
+  // Stages: the shared memory the row block leaves, as two stages of up to
+  // 512 orders (more stages only beyond that).  Larger bulk copies and fewer
+  // stage hand-offs measured faster on B200 at N=1024, R=64: 4 x 128 orders
+  // 4.0e8, 3 x 256 4.4e8, 2 x 384 4.55e8 evals/s.
+  const size_t ring_bytes = budget - al16((size_t)R * n * esz);
+  int kStageOrders = (int)std::min<size_t>(512, ring_bytes / (2 * (size_t)R * 2)) & ~31;
+  int kStages = 2;
+  if (kStageOrders >= 512)
+    kStages = (int)std::min<size_t>(kMaxStages, ring_bytes / ((size_t)kStageOrders * R * 2));
+  if (kStageOrders < 32) return false;
   // Predecessor buffer of ~96 MB (2n bytes per order).  Each chunk costs ~10 us
   // of fixed work (two launches, every score CTA restaging its row block), so
   // larger chunks win until the buffer leaves L2; measured on B200 at N=1024:
@@ -299,7 +323,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
-    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, part,
+    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, kStages, kStageOrders, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
     switch (p.storage) {
       case RW_STORAGE_U16: {

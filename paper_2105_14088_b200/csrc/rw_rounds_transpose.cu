@@ -192,7 +192,6 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
 }
 
 // ------------------------------------------------------------------ score --
-constexpr int kRStageOrders = 64;
 constexpr int kRMaxStages = 4;
 constexpr int kRThreads = 1024;  // 31 consumer warps + 1 producer warp
 
@@ -202,6 +201,7 @@ struct RScoreArgs {
   int rounds;
   int nblocks;
   int stages;   // ring depth
+  int stage_orders;  // orders per stage (a multiple of 32)
   void* keys;   // [round][order]
 };
 
@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kConsumers = kRThreads - 32;
   const bool producer = warp == (kRThreads >> 5) - 1;
+  const int kRStageOrders = a.stage_orders;
   const size_t stage_elems = (size_t)kRStageOrders * rounds * R;
   if (threadIdx.x == 0)
     for (int s = 0; s < a.stages; ++s) {
@@ -347,14 +348,16 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
   const size_t budget = (size_t)std::min(optin, 227 * 1024) - 1024;
   const size_t esz = p.elem_bytes();
-  // Largest row block that leaves room for a >= 2-deep ring of stages.
-  int R = 0, stages = 0;
+  // Largest row block that leaves room for two stages of >= 64 orders; the
+  // rest of shared memory becomes two stages of up to 256 orders (larger bulk
+  // copies and fewer hand-offs, as measured for the ring score).
+  int R = 0, stages = 2, kRStageOrders = 0;
   for (int cand : {32, 16, 8}) {
     const size_t mat = al16((size_t)cand * n * esz);
-    const size_t stage = (size_t)kRStageOrders * rounds * cand * 2;
-    if (mat + 2 * stage <= budget) {
+    const size_t per_order = (size_t)rounds * cand * 2;
+    if (mat + 2 * 64 * per_order <= budget) {
       R = cand;
-      stages = (int)std::min<size_t>(kRMaxStages, (budget - mat) / stage);
+      kRStageOrders = (int)std::min<size_t>(256, (budget - mat) / (2 * per_order)) & ~31;
       break;
     }
   }
@@ -401,7 +404,7 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
     ra.aligned = (reinterpret_cast<uintptr_t>(perms) & 15) == 0 ? 1 : 0;
     void* args[] = {&ra, (void*)&perms, (void*)&buf};
     RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), args, route_smem, st));
-    RScoreArgs sa{cnt_o, n, rounds, nblocks, stages, keys};
+    RScoreArgs sa{cnt_o, n, rounds, nblocks, stages, kRStageOrders, keys};
     const int sgrid = (int)std::min<int64_t>(sms, nblocks * ((cnt_o + kRStageOrders - 1) / kRStageOrders));
     switch (p.storage) {
       case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
