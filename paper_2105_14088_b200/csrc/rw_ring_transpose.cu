@@ -68,19 +68,30 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
       if ((n & 255) == 0) {
         const uint4* pv = reinterpret_cast<const uint4*>(pp);
         uint32_t carry = ld_order<P>(pp, n - 1);
-        for (int c = 0; c < (n >> 8); ++c) {
-          const uint4 v = __ldg(pv + c * 32 + lane);
-          const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
-                                 v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
-          uint32_t prev = __shfl_up_sync(kFull, e[7], 1);
-          const uint32_t last = __shfl_sync(kFull, e[7], 31);
-          if (lane == 0) prev = carry;
-          carry = last;
+        const int nc = n >> 8;
+        for (int c0 = 0; c0 < nc; c0 += 4) {
+          // up to four 16-byte loads in flight per lane (one HBM round trip
+          // per order at N=1024), then the scatter
+          uint4 vv[4];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t cur = e[k];
-            if (cur < (uint32_t)n) buf[cur] = (uint16_t)(k == 0 ? prev : e[k - 1]);
-            else bad = true;
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q < nc) vv[q] = __ldg(pv + (c0 + q) * 32 + lane);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (c0 + q >= nc) break;
+            const uint4 v = vv[q];
+            const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                                   v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+            uint32_t prev = __shfl_up_sync(kFull, e[7], 1);
+            const uint32_t last = __shfl_sync(kFull, e[7], 31);
+            if (lane == 0) prev = carry;
+            carry = last;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t cur = e[k];
+              if (cur < (uint32_t)n) buf[cur] = (uint16_t)(k == 0 ? prev : e[k - 1]);
+              else bad = true;
+            }
           }
         }
       } else {
