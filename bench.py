@@ -167,6 +167,22 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------- our arm ---
+def graph_kernel_nodes(graph) -> int:
+    """Kernel launches one replay of the captured step performs (the graph's
+    kernel nodes: route + score per chunk, the finalize pass)."""
+    from cuda.bindings import runtime as cudart
+    raw = graph.raw_cuda_graph()
+    g = raw if isinstance(raw, cudart.cudaGraph_t) else cudart.cudaGraph_t(init_value=int(raw))
+    err, _, num = cudart.cudaGraphGetNodes(g, 0)
+    err, nodes, num = cudart.cudaGraphGetNodes(g, num)
+    kernels = 0
+    for nd in nodes[:num]:
+        err, ty = cudart.cudaGraphNodeGetType(nd)
+        if ty == cudart.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+            kernels += 1
+    return kernels
+
+
 def make_orders_device(torch, count: int, n: int, seed: int):
     g = torch.Generator(device="cuda")
     g.manual_seed(seed)
@@ -218,15 +234,14 @@ def run_ours(args):
 
     # One step (the route/score kernel pairs of every chunk) captured as a CUDA
     # graph; the timed loop replays it.
-    graph = torch.cuda.CUDAGraph()
+    graph = torch.cuda.CUDAGraph(keep_graph=True)
     with torch.cuda.graph(graph):
         cap = torch.cuda.current_stream()
         prob.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), cap.cuda_stream)
     graph.replay()
     torch.cuda.synchronize()
     prob.sync_errors()
-    chunk = max(4096, (48 << 20) // (N * 2))
-    launches_per_step = 2 * ((batch + chunk - 1) // chunk)
+    launches_per_step = graph_kernel_nodes(graph)
 
     # ---- timed region: device-resident orders (value) ----
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -308,7 +323,8 @@ def run_ours(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("ring_eval_bytes_per_launch")
+        bpo = json.load(open(tpath)).get("bytes_per_order")
+        traffic = bpo * batch if bpo else None  # per bench step (one graph replay)
     clock = clocks.summary()
 
     cpu_value, cpu_info = (None, {"kind": "skipped", "cores": 0, "sample": "--no-cpu"})
