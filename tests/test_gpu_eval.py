@@ -375,3 +375,33 @@ def test_schedule_cost_equals_evaluate_via_cpp_suite_semantics(port):
                                                  _lib.ptr(nbytes, C.c_double), _lib.ptr(par, C.c_int32), 1,
                                                  _lib.ptr(perm, C.c_int32), C.byref(out)))
             assert out.value == port.evaluate(m, perm, s), (n, alg, pair)
+
+
+@pytest.mark.parametrize("n", [1000, 3000])
+def test_ring_sizes_off_the_transpose_grid(port, n):
+    """N % 8 != 0 takes the L2-gather ring kernel; costs equal the oracle."""
+    rng = np.random.default_rng(n)
+    m = rng.integers(0, 3000, size=(n, n)).astype(np.float64) / 16.0
+    np.fill_diagonal(m, 0.0)
+    prob = rw.Problem(m)
+    perms = np.array([rng.permutation(n) for _ in range(50)], dtype=np.int32)
+    spec = rw.CollectiveSpec(rw.Algorithm.Ring, n, 2.0 ** 20)
+    assert np.array_equal(prob.evaluate_batch(spec, perms), port.evaluate_batch(m, perms, make_spec(0, n, 2.0 ** 20)))
+
+
+def test_largest_transpose_shapes_n8192(port):
+    """Upper bounds of the transpose grids: ring at N=8192 (R=24 row blocks)
+    and halving-doubling at N=8192 (R=8); both equal the L2 path and the oracle."""
+    n = 8192
+    rng = np.random.default_rng(8192)
+    m = (rng.integers(0, 4000, size=(n, n), dtype=np.uint16).astype(np.float64)) / 16.0
+    np.fill_diagonal(m, 0.0)
+    tr, l2 = rw.Problem(m), rw.Problem(m)
+    tr.set_path("transpose")
+    l2.set_path("l2")
+    perms = np.array([rng.permutation(n) for _ in range(40)], dtype=np.int32)
+    for alg, pair in ((0, 0), (1, 1), (1, 0)):
+        spec = rw.CollectiveSpec(rw.Algorithm(alg), n, 2.0 ** 20, 2, rw.CostMode.LatencyTimesSize, rw.HdPairing(pair))
+        got = tr.evaluate_batch(spec, perms)
+        assert np.array_equal(got, l2.evaluate_batch(spec, perms)), (alg, pair)
+        assert np.array_equal(got[:4], port.evaluate_batch(m, perms[:4], make_spec(alg, n, 2.0 ** 20, 2, 1, pair)))
