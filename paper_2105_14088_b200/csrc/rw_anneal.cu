@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(256) k_anneal_init(AnnealArgs a, const T* __re
   extern __shared__ __align__(16) unsigned char smem[];
   const T* mat = gmat;
   if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  stage_dbt_plan(a.dbt, smem);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
   if (chain >= a.chains) return;
@@ -506,6 +507,7 @@ __global__ void __launch_bounds__(256) k_anneal_full(AnnealArgs a, const T* __re
   extern __shared__ __align__(16) unsigned char smem[];
   const T* mat = gmat;
   if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  stage_dbt_plan(a.dbt, smem);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
   if (chain >= a.chains) return;
@@ -784,6 +786,7 @@ __global__ void __launch_bounds__(256) k_local_search_full(AnnealArgs a, const T
   extern __shared__ __align__(16) unsigned char smem[];
   const T* mat = gmat;
   if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  stage_dbt_plan(a.dbt, smem);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int n = a.n;
   uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem));
@@ -1010,7 +1013,15 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   }
   a.mat_smem = smem_mat ? mat_bytes : 0;
   a.warp_bytes = (int)warp_bytes;
-  const size_t dyn = al16(a.mat_smem) + (size_t)wpb * warp_bytes;
+  size_t dyn = al16(a.mat_smem) + (size_t)wpb * warp_bytes;
+  if (plan.model == kDoubleBinaryTree && dbt_edges > 0) {
+    const size_t pb = dbt_plan_bytes(dbt_edges, a.dbt.depths);
+    if (al16(dyn) + pb <= (size_t)di.smem) {
+      a.dbt.stage_plan = 1;
+      a.dbt.plan_off = (int)al16(dyn);
+      dyn = al16(dyn) + pb;
+    }
+  }
   size_t dyn_ring = dyn;
   if (a.nb) {
     const size_t nbb = al16((size_t)n * a.K * 2);
@@ -1183,7 +1194,15 @@ void local_search_typed(Problem& p, const EvalPlan& plan, int32_t* perms, int64_
     }
     a.mat_smem = smem_mat ? mat_bytes : 0;
     a.warp_bytes = (int)warp_bytes;
-    const size_t dyn = al16(a.mat_smem) + order_bytes + wpb * warp_bytes;
+    size_t dyn = al16(a.mat_smem) + order_bytes + wpb * warp_bytes;
+    if (plan.model == kDoubleBinaryTree && dbt_edges > 0) {
+      const size_t pb = dbt_plan_bytes(dbt_edges, a.dbt.depths);
+      if (al16(dyn) + pb <= (size_t)di.smem) {
+        a.dbt.stage_plan = 1;
+        a.dbt.plan_off = (int)al16(dyn);
+        dyn = al16(dyn) + pb;
+      }
+    }
     auto k = smem_mat ? k_local_search_full<T, true> : k_local_search_full<T, false>;
     smem_attr(k, dyn);
     const int grid = (int)std::min<int64_t>(batch, (int64_t)di.sms * 4);

@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(1024) k_dbt(KArgs a, DbtArgs d, const P* __res
   extern __shared__ __align__(16) unsigned char smem[];
   const T* mat = gmat;
   if constexpr (kSmem) mat = stage_matrix<T>(gmat, a.mat_smem, smem);
+  stage_dbt_plan(d, smem);
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   unsigned char* wbase = smem + align16(a.mat_smem) + (size_t)wib * (a.flag_stride + a.perm_stride + a.val_stride);
@@ -774,10 +775,17 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
       ThreadCtx& c = thread_ctx(p.device);
       d.gvals = static_cast<double*>(c.scratch(slot, (size_t)grid * warps_per_block * edges * 8));
     }
+    size_t dyn_d = dyn;
+    const size_t plan_bytes = dbt_plan_bytes(edges, plan.dbt->depths);
+    if (n > 1 && align16(dyn) + plan_bytes <= budget) {
+      d.stage_plan = 1;
+      d.plan_off = (int)align16(dyn);
+      dyn_d = align16(dyn) + plan_bytes;
+    }
     auto kern = smem_mat ? (validate ? k_dbt<T, P, true, true> : k_dbt<T, P, true, false>)
                          : (validate ? k_dbt<T, P, false, true> : k_dbt<T, P, false, false>);
-    set_smem(kern, dyn);
-    kern<<<grid, threads, dyn, st>>>(a, d, d_perms, gmat, d_costs);
+    set_smem(kern, dyn_d);
+    kern<<<grid, threads, dyn_d, st>>>(a, d, d_perms, gmat, d_costs);
   } else {
     RoundsArgs r{};
     r.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);

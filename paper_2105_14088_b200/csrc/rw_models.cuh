@@ -35,7 +35,33 @@ struct DbtArgs {
   int mode;
   double half;
   double* gvals;  // global per-warp scratch when shared memory is too small
+  int stage_plan;  // kernels copy the plan arrays into shared memory at plan_off
+  int plan_off;    // byte offset in the kernel's dynamic shared memory
 };
+
+// Plan arrays (src | dst | c0 | c1 | depth_off, int32) in shared memory:
+// 16 B per edge.  All threads of the CTA call it before any early exit.
+__host__ __device__ inline size_t dbt_plan_bytes(int edges, int depths) {
+  return ((size_t)4 * edges + depths + 1) * 4 + 16;
+}
+__device__ __forceinline__ void stage_dbt_plan(DbtArgs& d, unsigned char* smem) {
+  if (!d.stage_plan) return;
+  int32_t* s = reinterpret_cast<int32_t*>(smem + d.plan_off);
+  const int E = d.edges;
+  for (int k = threadIdx.x; k < E; k += blockDim.x) {
+    s[k] = d.src[k];
+    s[E + k] = d.dst[k];
+    s[2 * E + k] = d.c0[k];
+    s[3 * E + k] = d.c1[k];
+  }
+  for (int k = threadIdx.x; k <= d.depths; k += blockDim.x) s[4 * E + k] = d.depth_off[k];
+  __syncthreads();
+  d.src = s;
+  d.dst = s + E;
+  d.c0 = s + 2 * E;
+  d.c1 = s + 3 * E;
+  d.depth_off = s + 4 * E;
+}
 
 // Sum over rounds of the round maximum (cost_model.cpp:71-92, 118-138).
 template <typename T, bool kSmem>
@@ -79,18 +105,19 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
                                 double* vals, int lane) {
   if (n <= 1) return 0.0;
   for (int depth = d.depths - 1; depth >= 0; --depth) {
-    const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
+    const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 4
     for (int e = lo + lane; e < hi; e += 32) {
-      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[__ldg(d.src + e)], s_perm[__ldg(d.dst + e)]), scale);
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[d.src[e]], s_perm[d.dst[e]]), scale);
       if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-      const int ch = __ldg(d.c0 + e);
+      const int ch = d.c0[e];
       // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
-      const double sub = ch >= 0 ? ref_max(vals[ch], vals[__ldg(d.c1 + e)]) : 0.0;
+      const double sub = ch >= 0 ? ref_max(vals[ch], vals[d.c1[e]]) : 0.0;
       vals[e] = __dadd_rn(c, sub);
     }
     __syncwarp();
   }
-  const int top = __ldg(d.depth_off + 1);
+  const int top = d.depth_off[1];
   double best = vals[0];
   for (int e = 1; e < top; ++e) best = ref_max(best, vals[e]);
   __syncwarp();

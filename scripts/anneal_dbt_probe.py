@@ -1,3 +1,8 @@
+#!/usr/bin/env python3
+"""C3 tree-model anneal at the reference run's evaluation budget (one chain by default):
+
+    python scripts/anneal_dbt_probe.py [chains]
+"""
 import json, sys, time
 sys.path.insert(0, ".")
 import paper_2105_14088_b200 as rw
