@@ -397,6 +397,17 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
   const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
   const uint64_t stream = ((uint64_t)gid << 5) | (uint64_t)lane;
   const bool sym = a.symmetric != 0;
+  // Philox4x32-10 block for (iteration counter, slot) of this lane's stream
+  auto philox_at = [&](unsigned long long c, int sl) {
+    Philox rng;
+    rng.key = key;
+    rng.ctr = make_uint4((uint32_t)c, ((uint32_t)(c >> 32) & 0x0FFFFFFFu) | ((uint32_t)sl << 28), (uint32_t)stream,
+                         (uint32_t)(stream >> 32));
+    return rng.block();
+  };
+  uint4 rnext[kSlots];
+#pragma unroll
+  for (int sl = 0; sl < kSlots; ++sl) rnext[sl] = philox_at(ctr, sl);
   for (int level = a.level_begin; level < a.level_end; ++level) {
     const double t = a.temps[level];
     const double inv_t = a.mul / t;  // real delta / t = units * mul / t
@@ -412,11 +423,7 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
       float us[kSlots];
 #pragma unroll
       for (int sl = 0; sl < kSlots; ++sl) {
-        Philox rng;
-        rng.key = key;
-        rng.ctr = make_uint4((uint32_t)ctr, ((uint32_t)(ctr >> 32) & 0x0FFFFFFFu) | ((uint32_t)sl << 28),
-                             (uint32_t)stream, (uint32_t)(stream >> 32));
-        const uint4 r = rng.block();
+        const uint4 r = rnext[sl];
         // half of the proposals are candidate-list 2-opt moves (symmetric matrices)
         ms[sl] = (sym && nbl && (r.x & 0x100u)) ? draw_move_nb(r, p, pos, nbl, a.K, n) : draw_move(r, n, sym);
         us[sl] = (float)(r.w >> 8) * 0x1.0p-24f;
@@ -432,6 +439,9 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
         for (int sl = 0; sl < kSlots; ++sl)
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[sl][q] = mat_at<T, kSmem>(mat, n, dt[sl].row[q], dt[sl].col[q]);
+        // the next iteration's random blocks while the gathers are in flight
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) rnext[sl] = philox_at(ctr, sl);
 #pragma unroll
         for (int sl = 0; sl < kSlots; ++sl) {
           Acc add = 0, sub = 0;
