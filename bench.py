@@ -42,7 +42,7 @@ WORKLOAD = "C4: N=1024 ring all-reduce cost, synthetic 3-level hierarchical matr
 N = 1024
 BATCH = 1 << 21  # orders per GPU per step: 2M x 1024 x 2 B = 4 GiB of uint16 orders in HBM
 E2E_BATCH = 1 << 16
-C4_CHAINS = 2368  # time-to-best-ring at C4: 16 chains (warps) per SM; see DESIGN.md 5
+C4_CHAINS = 592  # time-to-best-ring at C4: 4 chains (warps) per SM, the fastest per chain; DESIGN.md 5
 CPU_SECONDS = 10.0
 
 
