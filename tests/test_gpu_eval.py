@@ -405,3 +405,38 @@ def test_largest_transpose_shapes_n8192(port):
         got = tr.evaluate_batch(spec, perms)
         assert np.array_equal(got, l2.evaluate_batch(spec, perms)), (alg, pair)
         assert np.array_equal(got[:4], port.evaluate_batch(m, perms[:4], make_spec(alg, n, 2.0 ** 20, 2, 1, pair)))
+
+
+def test_concurrent_host_threads():
+    """SURVEY 8(b) threading contract: concurrent calls from several host
+    threads (one stream and scratch set per thread) on a shared Problem and on
+    per-thread Problems give the same costs as sequential calls."""
+    import threading
+    m = fixtures.config_matrix("C4", "fixed")
+    n = m.shape[0]
+    shared = rw.Problem(m)
+    rng = np.random.default_rng(31)
+    batches = [np.array([rng.permutation(n) for _ in range(500)], dtype=np.int32) for _ in range(6)]
+    specs = [rw.CollectiveSpec(rw.Algorithm(alg), n, fixtures.SIZE_FIXED) for alg in (0, 1, 2, 0, 1, 2)]
+    want = [shared.evaluate_batch(s, b) for s, b in zip(specs, batches)]
+    got = [None] * 6
+    errors = []
+
+    def work(k):
+        try:
+            prob = shared if k % 2 == 0 else rw.Problem(m)
+            if k == 3:
+                prob.set_path("l2")
+            for _ in range(3):
+                got[k] = prob.evaluate_batch(specs[k], batches[k])
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k in range(6):
+        assert np.array_equal(got[k], want[k]), k
