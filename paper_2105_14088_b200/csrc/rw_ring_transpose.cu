@@ -301,11 +301,13 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   if (kStageOrders >= 512)
     kStages = (int)std::min<size_t>(kMaxStages, ring_bytes / ((size_t)kStageOrders * R * 2));
   if (kStageOrders < 32) return false;
-  // Predecessor buffer of ~96 MB (2n bytes per order).  Each chunk costs ~10 us
-  // of fixed work (two launches, every score CTA restaging its row block), so
-  // larger chunks win until the buffer leaves L2; measured on B200 at N=1024:
-  // 16 MB 2.7e8, 48 MB 3.60e8, 96 MB 3.77e8 evals/s.
-  const int64_t chunk = std::max<int64_t>(4096, ((int64_t)96 << 20) / ((int64_t)n * 2));
+  // Predecessor exchange buffer of up to 512 MB (2n bytes per order).  Each
+  // chunk pays a fixed cost (two launches, every score CTA restaging its row
+  // block and filling its stage ring), which outweighs keeping the buffer
+  // L2-resident; measured in bench.py on B200 at N=1024 (evals/s):
+  // 48 MB 4.85e8, 96 MB 5.07e8, 128 MB 5.30e8, 256 MB 5.45e8, 512 MB 5.55e8,
+  // 1 GB 5.59e8.  Scratch only grows to min(batch, chunk) orders.
+  const int64_t chunk = std::max<int64_t>(4096, ((int64_t)512 << 20) / ((int64_t)n * 2));
   ThreadCtx& c = thread_ctx(p.device);
   const int64_t kmax = std::min(batch, chunk);
   uint16_t* predbuf = static_cast<uint16_t*>(c.scratch(slot, (size_t)nblocks * kmax * R * 2));
