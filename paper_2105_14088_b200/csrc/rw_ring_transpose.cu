@@ -172,20 +172,24 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
   __syncthreads();
   uint32_t g = 0;  // running stage counter of this CTA (same in every role)
 
-  // work items: (block, order range)
-  const int items = a.cpb > 0 ? nb * a.cpb : nb;
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int b = a.cpb > 0 ? item / a.cpb : item;
-    const int j = a.cpb > 0 ? item % a.cpb : 0;
-    const int parts = a.cpb > 0 ? a.cpb : 1;
-    const int64_t o0 = a.count * j / parts, o1 = a.count * (j + 1) / parts;
+  // Stream-K split: the (row block, stage) units are cut into gridDim.x equal
+  // contiguous ranges, so every SM gets the same work and a CTA restages the
+  // matrix only where its range crosses a row block.
+  const int64_t nst_all = (a.count + kStageOrders - 1) / kStageOrders;
+  const int64_t units = nst_all * nb;
+  const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t u = units * blockIdx.x / gridDim.x; u < u_end;) {
+    const int b = (int)(u / nst_all);
+    const int64_t st0 = u - (int64_t)b * nst_all;
+    const int64_t nstage = min(nst_all - st0, u_end - u);
+    u += nstage;
+    const int64_t o0 = st0 * kStageOrders;
+    const int64_t total = min(a.count, (st0 + nstage) * kStageOrders) - o0;
     const int row0 = b * R;
     const int rows = min(R, n - row0);
     __syncthreads();  // previous item fully consumed
     stage_rows(blk, gmat + (size_t)row0 * n, (size_t)rows * n * sizeof(T), &mat_bar, &mat_phase);
     const uint16_t* base = pred + ((size_t)b * a.count + o0) * R;
-    const int64_t total = o1 - o0;
-    const int64_t nstage = (total + kStageOrders - 1) / kStageOrders;
     // Producer / consumer ring: the last warp issues the bulk copies, gated
     // by per-slot "empty" barriers that the 31 consumer warps arrive on; no
     // CTA-wide barrier per stage.
@@ -318,8 +322,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   auto set = [](auto kern, size_t bytes) {
     if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   };
-  const int cpb = nblocks <= sms ? sms / nblocks : 0;
-  const int sgrid = cpb > 0 ? nblocks * cpb : sms;
+  const int cpb = 0;  // unused: the score pass splits (block, stage) units stream-K
   const bool int_sums = p.storage == RW_STORAGE_U16;
   if (int_sums) RW_CUDA(cudaMemsetAsync(d_costs, 0, (size_t)batch * 8, st));
   for (int64_t off = 0; off < batch; off += kmax) {
@@ -338,6 +341,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
     RW_CUDA(cudaGetLastError());
     ScoreArgs sa{cnt_o, n, R, nblocks, cpb, kStages, kStageOrders, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
+    const int sgrid = (int)std::min<int64_t>(sms, (int64_t)nblocks * ((cnt_o + kStageOrders - 1) / kStageOrders));
     switch (p.storage) {
       case RW_STORAGE_U16: {
         auto k = k_ring_score<uint16_t>;
