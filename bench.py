@@ -544,6 +544,25 @@ def run_extras(rw, torch):
                                        "cost": best[0], "identity_cost": ref[0]["identity_cost"],
                                        "steps_per_level": best[1], "evaluations": best[2], "chains": best[4],
                                        "reference_seconds_per_run_container": statistics.median(r["seconds"] for r in ref)}
+    dbt = [r for r in json.load(open(gpath))["results"] if r["config"] == "C3" and r["model"] == "dbt"] \
+        if os.path.exists(gpath) else []
+    if dbt:
+        target = dbt[0]["cost"]
+        p3 = rw.Problem(rw.fixtures.config_matrix("C3", "fixed"))
+        spec3 = rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, 256, rw.fixtures.SIZE_FIXED)
+        best = None
+        t = time.perf_counter()
+        for steps in (64, 128, 256, 512):
+            t1 = time.perf_counter()
+            order, cost, ev, rep = p3.anneal(spec3, rw.SolverConfig(seed=0, budget=1e6, steps_per_temperature=steps),
+                                             chains=C4_CHAINS)
+            best = (cost, steps, ev, time.perf_counter() - t1, rep["chains"])
+            if cost <= target:
+                break
+        out["time_to_best_dbt_c3"] = {"seconds_cumulative": time.perf_counter() - t, "seconds_last_run": best[3],
+                                      "target_reference_seed0": target, "reached": best[0] <= target,
+                                      "cost": best[0], "steps_per_level": best[1], "evaluations": best[2],
+                                      "chains": best[4], "reference_seconds_per_run_container": dbt[0]["seconds"]}
     return out
 
 
