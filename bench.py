@@ -326,6 +326,17 @@ def run_ours(args):
         bpo = json.load(open(tpath)).get("bytes_per_order")
         traffic = bpo * batch if bpo else None  # per bench step (one graph replay)
     clock = clocks.summary()
+    # The lookups run against shared memory: one random 2-byte scatter (route) and
+    # one random 2-byte gather (score) per hop, against the measured random-gather
+    # peak (profiles/gather_peaks.json, scripts/microbench/gather_peaks.cu).
+    smem_access = None
+    gpath_peaks = os.path.join(ROOT, "profiles", "gather_peaks.json")
+    if os.path.exists(gpath_peaks):
+        gp = json.load(open(gpath_peaks))
+        acc_per_s = 2 * N * batch / (launch_ms / 1000.0)
+        smem_access = {"accesses_per_s": acc_per_s, "peak_per_s": gp["smem_random_u16_lookups_per_s"],
+                       "frac": acc_per_s / gp["smem_random_u16_lookups_per_s"],
+                       "note": "route scatter + score gather, 2 random u16 shared-memory accesses per hop"}
 
     cpu_value, cpu_info = (None, {"kind": "skipped", "cores": 0, "sample": "--no-cpu"})
     if not args.no_cpu:
@@ -353,6 +364,7 @@ def run_ours(args):
                    "validation": "bijection check on every order", "parallelism": f"dp{world} (independent batches)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
+                     "smem_random_access": smem_access,
                      "kernel": "k_ring_route + k_ring_score (transpose ring path, one pair per chunk)",
                      "algorithmic_bytes_per_eval": bytes_per_eval,
                      "lookups_per_s": N * batch / (launch_ms / 1000.0),
