@@ -162,6 +162,54 @@ __global__ void __launch_bounds__(1024) k_ring_vec(KArgs a, const uint16_t* __re
   uint8_t marker = 0;
   constexpr bool kInt = std::is_same<T, uint16_t>::value;
   const int chunks = n >> 8;
+  if (chunks == 1) {
+    // N = 256: one 16-byte chunk per lane and order.  The next order's chunk
+    // is loaded while this one is scored (the order stream is the latency the
+    // warp would otherwise wait on), and the wrap-around predecessor comes
+    // from lane 31 of the same chunk.
+    int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint4 vnext = make_uint4(0, 0, 0, 0);
+    if (b < a.batch) vnext = __ldg(reinterpret_cast<const uint4*>(perms + b * n) + lane);
+    for (; b < a.batch; b += nwarps) {
+      marker = marker == 255 ? 1 : marker + 1;
+      const uint4 v = vnext;
+      if (b + nwarps < a.batch) vnext = __ldg(reinterpret_cast<const uint4*>(perms + (b + nwarps) * n) + lane);
+      const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                             v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+      uint32_t prev = __shfl_up_sync(kFull, e[7], 1);
+      const uint32_t last = __shfl_sync(kFull, e[7], 31);
+      if (lane == 0) prev = last;
+      unsigned long long iacc = 0;
+      double dacc = 0.0;
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t cur = e[k];
+        const uint32_t pr = k == 0 ? prev : e[k - 1];
+        if (cur < (uint32_t)n && pr < (uint32_t)n) {
+          if (kValidate) flags[cur] = marker;
+          const T val = mat_at<T, kSmem>(mat, n, (int)cur, (int)pr);
+          if constexpr (kInt) iacc += val;
+          else dacc = __dadd_rn(dacc, (double)val);
+        } else {
+          bad = true;
+        }
+      }
+      double cost;
+      if constexpr (kInt) cost = __dmul_rn((double)warp_sum(iacc), mul);
+      else cost = __dmul_rn(warp_sum(dacc), mul);
+      if constexpr (kValidate) {
+        __syncwarp();
+        bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        costs[b] = cost;
+        if (kValidate && bad) report_bad_order(a.err, n, b);
+      }
+    }
+    return;
+  }
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < a.batch; b += nwarps) {
     marker = marker == 255 ? 1 : marker + 1;
     const uint16_t* pp = perms + b * n;
