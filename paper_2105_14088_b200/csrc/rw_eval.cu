@@ -275,6 +275,48 @@ __device__ __forceinline__ bool stage_order(const P* __restrict__ pp, int n, uin
   return bad;
 }
 
+// Order staging with a one-order prefetch for the common shared-memory case
+// (uint16 orders, N = 256: one 16-byte chunk per lane): the next order's chunk
+// is in flight while the current one is evaluated.  Other shapes fall back to
+// stage_order.
+template <typename P, bool kValidate>
+struct OrderStager {
+  bool vec = false;
+  uint4 next = make_uint4(0, 0, 0, 0);
+  __device__ __forceinline__ void init(const P* perms, int n, int64_t b, int64_t batch, int lane) {
+    if constexpr (std::is_same<P, uint16_t>::value) {
+      vec = n == 256 && (reinterpret_cast<uintptr_t>(perms) & 15) == 0;
+      if (vec && b < batch) next = __ldg(reinterpret_cast<const uint4*>(perms + b * n) + lane);
+    }
+  }
+  __device__ __forceinline__ bool stage(const P* perms, int n, int64_t b, int64_t stride, int64_t batch,
+                                        uint16_t* s_perm, uint8_t* flags, uint8_t marker, int lane) {
+    if constexpr (std::is_same<P, uint16_t>::value) {
+      if (vec) {
+        uint4 v = next;
+        if (b + stride < batch) next = __ldg(reinterpret_cast<const uint4*>(perms + (b + stride) * n) + lane);
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t lo = w[k] & 0xFFFFu, hi = w[k] >> 16;
+          if (lo >= (uint32_t)n) { bad = true; lo = 0; }
+          if (hi >= (uint32_t)n) { bad = true; hi = 0; }
+          if (kValidate) {
+            flags[lo] = marker;
+            flags[hi] = marker;
+          }
+          w[k] = lo | (hi << 16);
+        }
+        reinterpret_cast<uint4*>(s_perm)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
+        __syncwarp();
+        return bad;
+      }
+    }
+    return stage_order<P, kValidate>(perms + b * n, n, s_perm, flags, marker, lane);
+  }
+};
+
 // ------------------------------------------------- K1: max-of-rounds ----
 template <typename T, typename P, bool kSmem, bool kValidate>
 __global__ void __launch_bounds__(1024) k_rounds(KArgs a, RoundsArgs r, const P* __restrict__ perms,
@@ -293,9 +335,11 @@ __global__ void __launch_bounds__(1024) k_rounds(KArgs a, RoundsArgs r, const P*
   __syncwarp();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint8_t marker = 0;
+  OrderStager<P, kValidate> stager;
+  stager.init(perms, n, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, a.batch, lane);
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < a.batch; b += nwarps) {
     marker = marker == 255 ? 1 : marker + 1;
-    bool bad = stage_order<P, kValidate>(perms + b * n, n, s_perm, flags, marker, lane);
+    bool bad = stager.stage(perms, n, b, nwarps, a.batch, s_perm, flags, marker, lane);
     const double total = warp_rounds_cost<T, kSmem>(s_perm, n, mat, r, a.scale, lane);
     if constexpr (kValidate) {
       bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
@@ -331,9 +375,11 @@ __global__ void __launch_bounds__(1024) k_dbt(KArgs a, DbtArgs d, const P* __res
   __syncwarp();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint8_t marker = 0;
+  OrderStager<P, kValidate> stager;
+  stager.init(perms, n, gwarp, a.batch, lane);
   for (int64_t b = gwarp; b < a.batch; b += nwarps) {
     marker = marker == 255 ? 1 : marker + 1;
-    bool bad = stage_order<P, kValidate>(perms + b * n, n, s_perm, flags, marker, lane);
+    bool bad = stager.stage(perms, n, b, nwarps, a.batch, s_perm, flags, marker, lane);
     const double best = warp_dbt_cost<T, kSmem>(s_perm, n, mat, d, a.scale, vals, lane);
     if constexpr (kValidate) {
       bad = __any_sync(kFull, bad) || !flags_complete(flags, n, marker, lane);
