@@ -957,6 +957,8 @@ int fill_model_args(AnnealArgs& a, const EvalPlan& plan) {
     a.dbt.edges = dbt_edges;
     a.dbt.mode = plan.mode;
     a.dbt.half = plan.half;
+    a.dbt.int_mode = plan.dbt_int ? 1 : 0;
+    a.dbt.w = plan.dbt_w;
   }
   return dbt_edges;
 }
@@ -1008,7 +1010,8 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   a.proposals = a.ctr + chains;
   int dbt_edges = fill_model_args(a, plan);
   // shared memory plan: two order buffers (+ dbt values) per warp
-  size_t warp_bytes = 2 * al16((size_t)n * 2) + al16((size_t)dbt_edges * 8);
+  const size_t vb = (std::is_same<T, uint16_t>::value && plan.dbt_int) ? 4 : 8;  // edge value bytes
+  size_t warp_bytes = 2 * al16((size_t)n * 2) + al16((size_t)dbt_edges * vb);
   const size_t mat_bytes = (size_t)n * n * sizeof(T);
   // warps (chains) per block: spread the chains over every SM first
   int wpb = 8;
@@ -1194,7 +1197,8 @@ void local_search_typed(Problem& p, const EvalPlan& plan, int32_t* perms, int64_
     a.scale = p.scale;
     const int dbt_edges = fill_model_args(a, plan);
     const size_t mat_bytes = (size_t)n * n * sizeof(T);
-    size_t warp_bytes = al16((size_t)n * 2) + al16((size_t)dbt_edges * 8);
+    const size_t vb = (std::is_same<T, uint16_t>::value && plan.dbt_int) ? 4 : 8;  // edge value bytes
+    size_t warp_bytes = al16((size_t)n * 2) + al16((size_t)dbt_edges * vb);
     int wpb = 8;
     const size_t order_bytes = al16((size_t)n * 2);
     bool smem_mat = mat_bytes + order_bytes + wpb * warp_bytes <= (size_t)di.smem;

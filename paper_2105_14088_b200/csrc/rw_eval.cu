@@ -801,7 +801,9 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   int edges = 0;
   if (model == kDoubleBinaryTree) {
     edges = plan.dbt->edges;
-    a.val_stride = (int)align16((size_t)edges * 8);
+    // edge values: uint32 in the exact integer form (u16 storage), FP64 otherwise
+    const size_t vb = (std::is_same<T, uint16_t>::value && plan.dbt_int) ? 4 : 8;
+    a.val_stride = (int)align16((size_t)edges * vb);
   }
   int threads = 256;
   bool smem_mat = mat_bytes + 16 * (per_warp + a.val_stride) <= budget;
@@ -865,6 +867,8 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
     d.edges = edges;
     d.mode = plan.mode;
     d.half = plan.half;
+    d.int_mode = plan.dbt_int ? 1 : 0;
+    d.w = plan.dbt_w;
     if (a.val_stride == 0 && n > 1) {
       ThreadCtx& c = thread_ctx(p.device);
       d.gvals = static_cast<double*>(c.scratch(slot, (size_t)grid * warps_per_block * edges * 8));

@@ -93,6 +93,8 @@ struct EvalPlan {
   bool ring_int = false;               // ring sums raw u16 codes as integers
   bool bit_exact = false;              // fast path reproduces reference bits
   const DbtPlan* dbt = nullptr;
+  bool dbt_int = false;                // dbt on u16: exact integer critical path (see make_plan)
+  double dbt_w = 0.0;                  //   value = (sum of codes on the path) * dbt_w
 };
 
 // expand_schedule (cost_model.cpp:150-236): rounds of transfers in rank space.

@@ -37,6 +37,8 @@ struct DbtArgs {
   double* gvals;  // global per-warp scratch when shared memory is too small
   int stage_plan;  // kernels copy the plan arrays into shared memory at plan_off
   int plan_off;    // byte offset in the kernel's dynamic shared memory
+  int int_mode;    // u16 storage, EvalPlan::dbt_int: uint32 path sums, vals as uint32
+  double w;        // int_mode: value = sum * w
 };
 
 // Plan arrays (src | dst | c0 | c1 | depth_off, int32) in shared memory:
@@ -104,6 +106,32 @@ template <typename T, bool kSmem>
 __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d, double scale,
                                 double* vals, int lane) {
   if (n <= 1) return 0.0;
+  if constexpr (std::is_same<T, uint16_t>::value) {
+    if (d.int_mode) {
+      // exact integer form (EvalPlan::dbt_int): path sums of raw codes
+      uint32_t* iv = reinterpret_cast<uint32_t*>(vals);
+      for (int depth = d.depths - 1; depth >= 0; --depth) {
+        const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 4
+        for (int e = lo + lane; e < hi; e += 32) {
+          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[d.src[e]], s_perm[d.dst[e]]);
+          const int ch = d.c0[e];
+          uint32_t sub = 0;
+          if (ch >= 0) {
+            const uint32_t x = iv[ch], y = iv[d.c1[e]];
+            sub = x > y ? x : y;
+          }
+          iv[e] = c + sub;
+        }
+        __syncwarp();
+      }
+      const int top = d.depth_off[1];
+      uint32_t best = iv[0];
+      for (int e = 1; e < top; ++e) best = iv[e] > best ? iv[e] : best;
+      __syncwarp();
+      return __dmul_rn((double)best, d.w);
+    }
+  }
   for (int depth = d.depths - 1; depth >= 0; --depth) {
     const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 4

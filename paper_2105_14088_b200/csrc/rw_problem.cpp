@@ -361,6 +361,19 @@ EvalPlan make_plan(Problem& p, const rw_spec& s) {
         p.dbt = std::move(d);
       }
       plan.dbt = p.dbt.get();
+      if (p.storage == RW_STORAGE_U16) {
+        // Each edge term is fl(q * 2^-f * half) (or q * 2^-f); with
+        // (depths + 2) * max_q * odd(half) < 2^53 every term, sum and max
+        // of the recursion (cost_model.cpp:94-116) is exact, so the result is
+        // (max path sum of codes) * w, w = 2^-f * half, bit for bit.
+        const bool times = s.cost_mode == RW_LATENCY_TIMES_SIZE;
+        const double w = times ? p.scale * plan.half : p.scale;
+        const double odd = times ? (plan.half > 0.0 ? odd_mantissa(plan.half) : 0.0) : 1.0;
+        const double terms = static_cast<double>(plan.dbt->depths + 2) * static_cast<double>(p.max_q);
+        plan.dbt_int = std::isfinite(w) && w > 0.0 && odd > 0.0 && terms * odd < 9007199254740992.0 &&
+                       terms < 4294967295.0;
+        plan.dbt_w = w;
+      }
       break;
     }
   }
