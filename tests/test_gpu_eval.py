@@ -440,3 +440,21 @@ def test_concurrent_host_threads():
     assert not errors, errors
     for k in range(6):
         assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("n", [16, 256, 1024])
+def test_dbt_integer_path_with_non_dyadic_sizes(port, n):
+    """The tree model's exact integer form (EvalPlan::dbt_int, u16 storage)
+    multiplies code sums by w = 2^-f * S/2 once; with S/2 = 5e7 (odd part
+    390625) or 3 * 2^20 + 1 and both cost modes the result must still equal
+    the reference's FP64 recursion bit for bit."""
+    rng = np.random.default_rng(n + 7)
+    m = rng.integers(0, 60000, size=(n, n)).astype(np.float64) / 16.0
+    prob = rw.Problem(m)
+    assert prob.info["storage"] == 1
+    perms = np.array([np.arange(n)] + [rng.permutation(n) for _ in range(63)], dtype=np.int32)
+    for size in (1e8, 2.0 * (3 * 2 ** 20 + 1), 1.0, 12345.0):
+        for mode in (1, 0):
+            spec = rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, n, size, 2, rw.CostMode(mode))
+            want = port.evaluate_batch(m, perms, make_spec(2, n, size, 2, mode))
+            assert np.array_equal(prob.evaluate_batch(spec, perms), want), (size, mode)
