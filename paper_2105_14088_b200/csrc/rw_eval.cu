@@ -815,6 +815,10 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
     threads = std::max(1, warps / 4) * 128;
   } else {
     a.mat_smem = 0;
+    // Tree model beyond shared memory: edge values go to a per-warp global
+    // scratch (L2) so many more warps fit per SM; measured at N=4096 4.7e6 ->
+    // 1.0e7 and at N=1024 5.2e7 -> 7.4e7 evals/s.
+    if (model == kDoubleBinaryTree) a.val_stride = 0;
     const size_t w = per_warp + a.val_stride;
     int warps = 8;
     while (warps > 1 && (size_t)warps * w > budget) warps >>= 1;
