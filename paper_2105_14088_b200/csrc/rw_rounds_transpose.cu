@@ -268,9 +268,18 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
         const int cnt = (int)min((int64_t)kRStageOrders, a.count - o0);
         const uint16_t* sp = ring + slot * stage_elems;
         const int tasks = cnt * rounds;
+        const float inv_cnt = 1.0f / (float)cnt;
         for (int t = threadIdx.x; t < tasks; t += kConsumers) {
-          const int r = t / cnt;
-          const int k = t - r * cnt;
+          // t = r * cnt + k via a float reciprocal and one correction step
+          int r = (int)((float)t * inv_cnt);
+          int k = t - r * cnt;
+          if (k < 0) {
+            --r;
+            k += cnt;
+          } else if (k >= cnt) {
+            ++r;
+            k -= cnt;
+          }
           const uint4* q4 = reinterpret_cast<const uint4*>(sp + ((size_t)r * kRStageOrders + k) * R);
           K key = KeyOf<T>::enc(T(0));
 #pragma unroll
