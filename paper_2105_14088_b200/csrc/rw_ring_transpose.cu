@@ -11,15 +11,19 @@
 //       shared-memory "predecessor by host" array, pred[cur] = prev, then
 //       writes it out in 16-byte chunks grouped by row block of the matrix:
 //       predbuf[block][order][row-in-block].  Every global access is
-//       coalesced; the per-chunk buffer (tens of MB) stays in the 126 MB L2.
-//       The same pass validates the order: a host that is never `cur` keeps
-//       the 0xFFFF sentinel (duplicates imply a missing host).
+//       coalesced.  The same pass validates the order: a host that is never
+//       `cur` keeps the 0xFFFF sentinel (duplicates imply a missing host).
 //   pass 2 (k_ring_score)  a CTA holds a row block of the matrix in shared
-//       memory and scores a range of orders against it: it reads that block's
-//       predecessor slice (contiguous) and does shared-memory lookups
-//       blk[row][pred[row]].  Per-(order, block) partial sums are combined by
-//       the last-arriving CTA in block order (deterministic, exact for
-//       integer codes).
+//       memory (one TMA bulk copy); a producer warp streams the block's
+//       predecessor slices through a two-stage TMA bulk-copy ring (full /
+//       empty mbarriers) and 31 consumer warps do the shared-memory lookups
+//       blk[row][pred[row]].  (row block, stage) units are split stream-K
+//       over every SM.  u16 codes: per-(order, block) integer partials are
+//       added atomically into the cost array (exact, order-independent) and
+//       scaled once by k_ring_finalize; FP32/FP64 matrices: partials go to
+//       part[block][order] and k_ring_combine sums them in block order.
+//   Chunks of up to 512 MB of predecessor buffer: the per-chunk fixed cost
+//   (launches, row-block staging, ring fill) outweighs L2 residency.
 //
 // Reference semantics: ring_cost (proj/src/cost_model.cpp:59-69), hop i =
 // rtt[perm[i]][perm[i-1]]; every host is `cur` of exactly one hop, so
@@ -135,9 +139,8 @@ struct ScoreArgs {
   int n;
   int R;           // rows per block
   int nblocks;
-  int cpb;
   int stages;        // TMA ring depth
-  int stage_orders;  // orders per TMA stage         // CTAs per block (nblocks < gridDim) ; 0: CTAs loop over blocks
+  int stage_orders;  // orders per TMA stage
   double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
   unsigned long long* acc;  // u16 codes: per-order integer sums accumulated atomically (exact)
 };
@@ -322,7 +325,6 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   auto set = [](auto kern, size_t bytes) {
     if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   };
-  const int cpb = 0;  // unused: the score pass splits (block, stage) units stream-K
   const bool int_sums = p.storage == RW_STORAGE_U16;
   if (int_sums) RW_CUDA(cudaMemsetAsync(d_costs, 0, (size_t)batch * 8, st));
   for (int64_t off = 0; off < batch; off += kmax) {
@@ -339,7 +341,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
-    ScoreArgs sa{cnt_o, n, R, nblocks, cpb, kStages, kStageOrders, part,
+    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
     const int sgrid = (int)std::min<int64_t>(sms, (int64_t)nblocks * ((cnt_o + kStageOrders - 1) / kStageOrders));
     switch (p.storage) {
