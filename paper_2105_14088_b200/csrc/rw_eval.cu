@@ -14,7 +14,9 @@
 // the max of raw matrix codes and do exactly the reference's FP64 multiply /
 // add sequence per round -> identical bits for every matrix.  The double
 // binary tree does the reference's per-edge multiply and add in the same
-// operand order.  Ring sums are order-sensitive: with u16 fixed-point storage
+// operand order, or -- on u16 storage when every term, sum and max of that
+// recursion is exact (EvalPlan::dbt_int) -- sums raw codes along the critical
+// path and scales once, which yields the same bits.  Ring sums are order-sensitive: with u16 fixed-point storage
 // the kernel sums integer codes (exact, and equal to the reference whenever
 // its own arithmetic is exact -- EvalPlan::bit_exact); otherwise the fast
 // kernel's FP64 tree sum is within a few ulps, and K0 sorts the hops and sums
