@@ -458,3 +458,34 @@ def test_dbt_integer_path_with_non_dyadic_sizes(port, n):
             spec = rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, n, size, 2, rw.CostMode(mode))
             want = port.evaluate_batch(m, perms, make_spec(2, n, size, 2, mode))
             assert np.array_equal(prob.evaluate_batch(spec, perms), want), (size, mode)
+
+
+def test_empty_batches_and_smallest_sizes(port):
+    """Edge cases the reference tests (test_cost_model.cpp:204-223): empty
+    batches on every path (host int32, device uint16, transpose paths) and the
+    smallest N of every model, against the oracle."""
+    import torch
+    for cfg in ("C1", "C4"):
+        m = fixtures.config_matrix(cfg, "fixed")
+        n = m.shape[0]
+        prob = rw.Problem(m)
+        for alg in range(4):
+            spec = rw.CollectiveSpec(rw.Algorithm(alg), n, fixtures.SIZE_FIXED)
+            got = prob.evaluate_batch(spec, np.zeros((0, n), dtype=np.int32))
+            assert got.shape == (0,)
+            c = torch.empty(1, dtype=torch.float64, device="cuda")
+            d = torch.empty((1, n), dtype=torch.int16, device="cuda")
+            prob.evaluate_batch_device(spec, d.data_ptr(), 2, 0, c.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            prob.sync_errors()
+    for n, algs in ((1, (0, 1, 2, 3)), (2, (0, 1, 2, 3)), (3, (0,)), (4, (0, 1, 2, 3))):
+        m = np.arange(n * n, dtype=np.float64).reshape(n, n) % 7
+        np.fill_diagonal(m, 0.0)
+        prob = rw.Problem(m)
+        perms = np.array(list(__import__("itertools").permutations(range(n))), dtype=np.int32)
+        for alg in algs:
+            for mode in (0, 1):
+                spec = rw.CollectiveSpec(rw.Algorithm(alg), n, 10.0, 2, rw.CostMode(mode))
+                want = port.evaluate_batch(m, perms, make_spec(alg, n, 10.0, 2, mode))
+                assert np.array_equal(prob.evaluate_batch(spec, perms), want), (n, alg, mode)
+                assert np.array_equal(prob.evaluate_batch(spec, perms, exact=True), want), (n, alg, mode)
