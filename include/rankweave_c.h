@@ -155,14 +155,17 @@ rw_status rw_problem_create(const double* rtt_us, int32_t n, int32_t storage_hin
                             rw_problem** out);
 rw_status rw_problem_destroy(rw_problem* p);
 rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out);
-/* Ring kernel-path override for A/B measurements and tests, used when the
- * matrix exceeds one CTA's shared memory:
- *   RW_PATH_AUTO       default: RW_PATH_TRANSPOSE when supported, else L2 gather
+/* Kernel-path override for A/B measurements and tests, used when the matrix
+ * exceeds one CTA's shared memory (results are identical on every path):
+ *   RW_PATH_AUTO       default: the transpose path for ring up to N = 1536 and
+ *                      for halving-doubling (512 <= N <= 16384, power of 2),
+ *                      the L2-gather kernels otherwise
  *   RW_PATH_L2_GATHER  one warp per order, random gathers from the L2-resident matrix
- *   RW_PATH_CLUSTER    row-partitioned thread-block cluster, DSMEM hop routing
- *                      (u16 matrices, N = 64*C, C <= 16)
- *   RW_PATH_TRANSPOSE  two passes through an L2-resident predecessor buffer;
- *                      lookups from a shared-memory row block (N % 8 == 0, 256 <= N <= 8192) */
+ *   RW_PATH_CLUSTER    ring only: row-partitioned thread-block cluster, DSMEM hop
+ *                      routing (u16 matrices, N = 64*C, C <= 16)
+ *   RW_PATH_TRANSPOSE  two passes through an HBM exchange buffer (predecessor /
+ *                      partner by host, grouped by matrix row block); lookups from
+ *                      a shared-memory row block (ring: N % 8 == 0, 256 <= N <= 8192) */
 enum { RW_PATH_AUTO = 0, RW_PATH_L2_GATHER = 1, RW_PATH_CLUSTER = 2, RW_PATH_TRANSPOSE = 3 };
 rw_status rw_problem_set_path(rw_problem* p, int32_t path);
 
@@ -200,7 +203,8 @@ rw_status rw_unrank(const rw_spec* spec, uint64_t index, int32_t* perm_out);
 rw_status rw_anneal(const rw_problem* p, const rw_spec* spec, const rw_solver_config* cfg,
                     const rw_gpu_config* gpu, int32_t* perm_out, double* cost_out, uint64_t* evals_out,
                     rw_search_report* report);
-/* Batched best-improvement local search (2-opt + swap + or-opt for ring):
+/* Batched best-improvement local search (ring: 2-opt + swap + or-opt with O(1)
+ * deltas; tree / halving-doubling / BCube: swap + 2-opt by full evaluation):
  * orders are improved in place; costs_out receives reference-exact costs. */
 rw_status rw_local_search(const rw_problem* p, const rw_spec* spec, int32_t* perms_inout, int64_t batch,
                           int32_t max_rounds, double* costs_out, uint64_t* evals_out);
