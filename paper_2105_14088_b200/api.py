@@ -280,14 +280,22 @@ def validate_spec(spec: CollectiveSpec) -> None:
     check(lib.rw_validate_spec(C.byref(spec._c())))
 
 
-def validate_order(order: RankOrder, n: int) -> None:
+def _order_array(order: RankOrder, n: int) -> np.ndarray:
+    """validate(RankOrder, n) (types.cpp:100-110) on a NumPy copy of the order;
+    returns the int32 array the C ABI takes."""
     if order.size() != n:
         raise DomainError(f"rank order has {order.size()} entries, expected {n}")
-    seen = [False] * n
-    for v in order.perm:
-        if v < 0 or v >= n or seen[v]:
-            raise DomainError(f"rank order is not a permutation of [0, {n})")
-        seen[v] = True
+    try:
+        a = np.asarray(order.perm, dtype=np.int64)
+    except (OverflowError, ValueError, TypeError):
+        raise DomainError(f"rank order is not a permutation of [0, {n})")
+    if n and (a.ndim != 1 or a.min() < 0 or a.max() >= n or np.bincount(a, minlength=n).max() != 1):
+        raise DomainError(f"rank order is not a permutation of [0, {n})")
+    return a.astype(np.int32)
+
+
+def validate_order(order: RankOrder, n: int) -> None:
+    _order_array(order, n)
 
 
 def validate_matrix(m: CostMatrix) -> None:
@@ -338,17 +346,16 @@ def transfer_cost(m: CostMatrix, i: int, j: int, nbytes: float, mode: CostMode) 
 
 
 # ------------------------------------------------------------- cost model --
-def _check_inputs(m: CostMatrix, order: RankOrder, spec: CollectiveSpec) -> None:
+def _check_inputs(m: CostMatrix, order: RankOrder, spec: CollectiveSpec) -> np.ndarray:
     validate_spec(spec)
     if m.n() != spec.n:
         raise DomainError(f"matrix is {m.n()}x{m.n()} but spec has N={spec.n}")
-    validate_order(order, spec.n)
+    return _order_array(order, spec.n)
 
 
 def evaluate(m: CostMatrix, order: RankOrder, spec: CollectiveSpec) -> float:
     """evaluate (cost_model.hpp:28): reference-identical FP64 bits."""
-    _check_inputs(m, order, spec)
-    perm = np.asarray(order.perm, dtype=np.int32)
+    perm = np.ascontiguousarray(_check_inputs(m, order, spec))
     out = C.c_double()
     check(lib.rw_evaluate(m.problem().handle, C.byref(spec._c()), ptr(perm, C.c_int32), C.byref(out)))
     return out.value

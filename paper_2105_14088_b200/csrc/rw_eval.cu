@@ -976,6 +976,10 @@ void launch_evaluate(const Problem& p, const EvalPlan& plan, const void* d_perms
                      double* d_costs, bool exact, bool validate, int* err_slot, cudaStream_t st, int slot) {
   if (batch <= 0) return;
   if (perm_bytes != 2 && perm_bytes != 4) fail_domain("perm_bytes must be 2 or 4");
+  // The sorted-sum kernel (K0) is only needed when the fast ring sum could
+  // differ from the reference: with EvalPlan::bit_exact the fast integer sum
+  // already yields the reference's bits (config goldens assert it).
+  if (exact && plan.bit_exact && plan.model == kRing) exact = false;
   switch (p.storage) {
     case RW_STORAGE_U16:
       launch_storage<uint16_t>(p, plan, d_perms, perm_bytes, batch, d_costs, exact, validate, err_slot, st, slot);
@@ -995,6 +999,25 @@ void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms
   DeviceGuard g(p.device);
   ThreadCtx& c = thread_ctx(p.device);
   const int n = plan.n;
+  if (batch * (int64_t)n <= (1 << 16)) {
+    // small batches (single evaluate() calls): one stream, one synchronisation
+    cudaStream_t st = c.stream[0];
+    const size_t pb = align16((size_t)batch * n * 4);
+    char* base = static_cast<char*>(c.scratch(0, pb + (size_t)batch * 8 + 64));
+    auto* d_perm = reinterpret_cast<int32_t*>(base);
+    auto* d_cost = reinterpret_cast<double*>(base + pb);
+    RW_CUDA(cudaMemcpyAsync(d_perm, perms, (size_t)batch * n * 4, cudaMemcpyHostToDevice, st));
+    launch_evaluate(p, plan, d_perm, 4, batch, d_cost, exact, validate, c.d_err, st, 2);
+    RW_CUDA(cudaMemcpyAsync(costs, d_cost, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+    if (validate) raise_order_errors(c.d_err, c.h_err, st);  // synchronises st
+    else RW_CUDA(cudaStreamSynchronize(st));
+    if (report) {
+      report->bit_exact = (plan.bit_exact || exact) ? 1 : 0;
+      report->kernel = plan.model;
+      report->lookups = lookups_per_eval(plan) * batch;
+    }
+    return;
+  }
   // Chunked double-buffered pipeline: H2D(k+1) overlaps scoring(k) on the
   // other stream; costs come back per chunk.
   const int64_t row = (int64_t)n * 4;
