@@ -489,3 +489,27 @@ def test_empty_batches_and_smallest_sizes(port):
                 want = port.evaluate_batch(m, perms, make_spec(alg, n, 10.0, 2, mode))
                 assert np.array_equal(prob.evaluate_batch(spec, perms), want), (n, alg, mode)
                 assert np.array_equal(prob.evaluate_batch(spec, perms, exact=True), want), (n, alg, mode)
+
+
+@pytest.mark.parametrize("path", ["l2", "transpose"])
+def test_unvalidated_matrices_nan_and_negative(port, path):
+    """evaluate() does not validate the matrix, so FP64
+    matrices may hold NaN and negative entries.  The round maxima follow the
+    reference's running std::max from 0 (cost_model.cpp:83): NaN never wins and
+    negatives never beat the initial 0.  The transpose path's order-preserving
+    keys must agree with the oracle; the tree model and ring carry NaN / negative
+    values through their sums."""
+    n = 1024
+    rng = np.random.default_rng(99)
+    m = rng.random((n, n)) * 50.0
+    m[rng.random((n, n)) < 0.02] = np.nan
+    m[rng.random((n, n)) < 0.05] *= -1.0
+    prob = rw.Problem(m)
+    assert prob.info["storage"] == 3  # f64
+    prob.set_path(path)
+    perms = np.array([rng.permutation(n) for _ in range(24)], dtype=np.int32)
+    for alg, pair in ((1, 0), (1, 1), (2, 0), (0, 0)):
+        spec = rw.CollectiveSpec(rw.Algorithm(alg), n, 1e6, 2, rw.CostMode.LatencyTimesSize, rw.HdPairing(pair))
+        want = port.evaluate_batch(m, perms, make_spec(alg, n, 1e6, 2, 1, pair))
+        got = prob.evaluate_batch(spec, perms, exact=True)
+        np.testing.assert_array_equal(got, want)  # NaN positions must agree too
