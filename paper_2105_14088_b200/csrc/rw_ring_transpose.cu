@@ -30,6 +30,7 @@
 // sum over hosts h of rtt[h][pred(h)] is the same multiset of hops.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
@@ -51,6 +52,9 @@ struct RouteArgs {
   int nblocks;
   unsigned long long* err;
 };
+
+// Zeroes each 16-bit half of w that has bit 15 set (the route's sentinel).
+__device__ __forceinline__ uint32_t clear_sentinels(uint32_t w) { return w & ~(((w & 0x80008000u) >> 15) * 0xFFFFu); }
 
 template <typename P, bool kValidate>
 __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __restrict__ perms,
@@ -117,16 +121,18 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
     __syncwarp();
     // write pred by row block (16-byte chunks), check the sentinel, reset
     for (int c = lane; c < chunks8; c += 32) {
-      const uint4 v = buf4[c];
+      uint4 v = buf4[c];
       const int h0 = c << 3;
       const int b = h0 / a.R;
       const int s0 = h0 - b * a.R;
-      *reinterpret_cast<uint4*>(pred + ((size_t)b * a.count + o) * a.R + s0) = v;
-      if (kValidate) {
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) bad |= (w[k] & 0xFFFFu) == 0xFFFFu || (w[k] >> 16) == 0xFFFFu;
+      // Valid entries are < n <= 8192, so only the 0xFFFF sentinel has bit 15
+      // set.  A chunk holding one is a bad order; its sentinels are zeroed so
+      // the score pass can index rows without clamping (in range either way).
+      if ((v.x | v.y | v.z | v.w) & 0x80008000u) {
+        bad = true;
+        v = make_uint4(clear_sentinels(v.x), clear_sentinels(v.y), clear_sentinels(v.z), clear_sentinels(v.w));
       }
+      *reinterpret_cast<uint4*>(pred + ((size_t)b * a.count + o) * a.R + s0) = v;
       buf4[c] = ones;
     }
     __syncwarp();
@@ -142,11 +148,79 @@ struct ScoreArgs {
   int stages;        // TMA ring depth
   int stage_orders;  // orders per TMA stage
   int vec;           // multi-order warp step (R in {32, 64, 128, 256}, n % R == 0)
+  int unroll;        // orders per lane group per step (C4 specialisation: 1 or 2)
   double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
   unsigned long long* acc;  // u16 codes: per-order integer sums accumulated atomically (exact)
 };
 
 constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// Multi-order warp step over one stage (u16 codes, whole row blocks, R = 8*LPO):
+// LPO lanes per order take 8 rows each -- one conflict-free 16-byte
+// predecessor load, 8 shared-memory lookups, a segmented shuffle sum -- so a
+// warp scores 32/LPO orders per step.  The route leaves every predecessor
+// < n (sentinels zeroed), so the lookups need no clamp: the row addresses are
+// hoisted and each lookup is extract + add + LDS.  The high half is (w >> 15):
+// bit 15 of the low half is clear, so that is exactly 2 * (w >> 16).
+// N > 0 fixes the row length at compile time (row offsets become LDS
+// immediates); N == 0 takes it from `n`.
+__device__ __forceinline__ uint32_t lo16(uint32_t w) {
+  uint32_t r;
+  asm("and.b32 %0, %1, 65535;" : "=r"(r) : "r"(w));  // opaque: keeps (w & 0xFFFF) * 2 + row a single LEA
+  return r;
+}
+
+template <int LPO, int N, int U>
+__device__ __forceinline__ void score_stage_vec(const uint16_t* sp, const uint16_t* blk, int n, int cnt, int warp,
+                                                int cw, int lane, unsigned long long* __restrict__ accp) {
+  constexpr int OPW = 32 / LPO, R = 8 * LPO;
+  const int sub = lane & (LPO - 1), kk = lane / LPO;
+  const uint32_t rstep = N > 0 ? (uint32_t)N * 2u : (uint32_t)n * 2u;
+  const uint32_t row0 = (uint32_t)__cvta_generic_to_shared(blk) + (uint32_t)(sub * 8) * rstep;
+  const uint32_t src = (uint32_t)__cvta_generic_to_shared(sp) + (uint32_t)(kk * R + sub * 8) * 2u;
+  // U orders per lane group per step: more lookups in flight, loop and
+  // atomic-address overhead shared.
+  for (int k0 = warp * OPW * U; k0 < cnt; k0 += cw * OPW * U) {
+    uint32_t acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * OPW + kk;
+      acc[u] = 0;
+      if (k < cnt) {
+        const uint4 w4 = lds_v4(src + (uint32_t)(k0 + u * OPW) * (R * 2));
+        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+        uint32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[2 * q] = lds_u16(row0 + lo16(w[q]) * 2u + (2 * q) * rstep);
+          v[2 * q + 1] = lds_u16(row0 + (w[q] >> 15) + (2 * q + 1) * rstep);
+        }
+        acc[u] = (v[0] + v[1] + v[2]) + (v[3] + v[4] + v[5]) + (v[6] + v[7]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int off = LPO >> 1; off > 0; off >>= 1) acc[u] += __shfl_xor_sync(kFull, acc[u], off);
+    }
+    if (sub == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k0 + u * OPW + kk < cnt) atomicAdd(accp + k0 + u * OPW + kk, (unsigned long long)acc[u]);
+    }
+  }
+}
 
 // Pass 2: a CTA keeps rows [b*R, b*R + rows) in shared memory and streams the
 // block's predecessor slices (contiguous in predbuf) through a 4-stage TMA
@@ -220,31 +294,15 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
         const uint16_t* sp = ring + slot * stage_elems;
         if constexpr (kInt) {
           if (a.vec) {
-            // R/8 lanes per order take 8 rows each: one conflict-free 16-byte
-            // predecessor load, 8 lookups, a segmented shuffle sum; 32/(R/8)
-            // orders per warp step.  About a third of the instructions of the
-            // per-order loop below (bench: 5.2e8 -> 6.4e8 evals/s at N=1024).
-            // Only with whole row blocks (n % R == 0): no tail rows to mask.
-            const int lpo = R >> 3, opw = 32 / lpo;
-            const int sub = lane & (lpo - 1), kk = lane / lpo;
-            const int s0 = sub * 8;
-            const T* brow = blk + (size_t)s0 * n;
             unsigned long long* accp = a.acc + o0 + st * kStageOrders;
-            for (int k0 = warp * opw; k0 < cnt; k0 += cw * opw) {
-              const int k = k0 + kk;
-              uint32_t acc = 0;
-              if (k < cnt) {
-                const uint4 w4 = *reinterpret_cast<const uint4*>(sp + (size_t)k * R + s0);
-                const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                for (int h = 0; h < 8; ++h) {
-                  const uint32_t col = min((h & 1) ? (w[h >> 1] >> 16) : (w[h >> 1] & 0xFFFFu), nm1);
-                  acc += (uint32_t)brow[h * n + col];
-                }
-              }
-              for (int off = lpo >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
-              if (sub == 0 && k < cnt) atomicAdd(accp + k, (unsigned long long)acc);
-            }
+            const int c = (int)cnt;
+            if (R == 64 && n == 1024) {  // C4
+              if (a.unroll == 2) score_stage_vec<8, 1024, 2>(sp, blk, n, c, warp, cw, lane, accp);
+              else score_stage_vec<8, 1024, 1>(sp, blk, n, c, warp, cw, lane, accp);
+            } else if (R == 32) score_stage_vec<4, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
+            else if (R == 64) score_stage_vec<8, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
+            else if (R == 128) score_stage_vec<16, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
+            else score_stage_vec<32, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
           } else
           // u16 codes: a block partial is < R * 65536 <= 2^32 (R <= 1024 here)
           for (int k = warp; k < cnt; k += cw) {
@@ -353,6 +411,10 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   auto set = [](auto kern, size_t bytes) {
     if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   };
+  static const int score_unroll = [] {
+    const char* e = std::getenv("RW_RING_SCORE_UNROLL");
+    return e && std::atoi(e) == 2 ? 2 : 1;
+  }();
   const bool int_sums = p.storage == RW_STORAGE_U16;
   if (int_sums) RW_CUDA(cudaMemsetAsync(d_costs, 0, (size_t)batch * 8, st));
   for (int64_t off = 0; off < batch; off += kmax) {
@@ -370,7 +432,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
     }
     RW_CUDA(cudaGetLastError());
     const int vec = (R == 32 || R == 64 || R == 128 || R == 256) && n % R == 0 ? 1 : 0;
-    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, part,
+    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, score_unroll, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
     const int sgrid = (int)std::min<int64_t>(sms, (int64_t)nblocks * ((cnt_o + kStageOrders - 1) / kStageOrders));
     switch (p.storage) {
