@@ -30,7 +30,6 @@
 // sum over hosts h of rtt[h][pred(h)] is the same multiset of hops.
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
@@ -53,11 +52,16 @@ struct RouteArgs {
   unsigned long long* err;
 };
 
-// Zeroes each 16-bit half of w that has bit 15 set (the route's sentinel).
-__device__ __forceinline__ uint32_t clear_sentinels(uint32_t w) { return w & ~(((w & 0x80008000u) >> 15) * 0xFFFFu); }
+// Zeroes each 16-bit half of w that has a bit of hmask set (bad-order path only).
+__device__ __forceinline__ uint32_t clear_bad(uint32_t w, uint32_t hmask) {
+  const uint32_t t = w & hmask;
+  return w & ((t & 0xFFFFu) ? 0xFFFF0000u : 0xFFFFFFFFu) & ((t >> 16) ? 0x0000FFFFu : 0xFFFFFFFFu);
+}
 
-template <typename P, bool kValidate>
-__global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __restrict__ perms,
+// 5 CTAs per SM (48 registers): more warps to cover the order loads' HBM
+// latency than 4 (63 registers); measured +1.3% on C4, 6 spills.
+template <typename P, bool kValidate, bool kPow2>
+__global__ void __launch_bounds__(256, 5) k_ring_route(RouteArgs a, const P* __restrict__ perms,
                                                     uint16_t* __restrict__ pred) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
@@ -66,6 +70,7 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
   uint4* buf4 = reinterpret_cast<uint4*>(buf);
   const uint4 ones = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
   const int chunks8 = n >> 3;  // n % 8 == 0 on this path
+  const uint32_t hmask = kPow2 ? ~((uint32_t)(n - 1) * 0x10001u) : 0x80008000u;
   for (int c = lane; c < chunks8; c += 32) buf4[c] = ones;
   __syncwarp();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -97,7 +102,12 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const uint32_t cur = e[k];
-              if (cur < (uint32_t)n) buf[cur] = (uint16_t)(k == 0 ? prev : e[k - 1]);
+              // An out-of-range predecessor is also some hop's `cur`, which
+              // flags the order.  The write-out below must still see it: for
+              // a power-of-two n its mask test does; otherwise it is stored
+              // as the sentinel here.
+              const uint32_t pv = k == 0 ? prev : e[k - 1];
+              if (cur < (uint32_t)n) buf[cur] = (uint16_t)(kPow2 || pv < (uint32_t)n ? pv : 0xFFFFu);
               else bad = true;
             }
           }
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
         for (int i = lane; i < n; i += 32) {
           const uint32_t cur = (uint32_t)ld_order<P>(pp, i);
           const uint32_t prev = (uint32_t)ld_order<P>(pp, i == 0 ? n - 1 : i - 1);
-          if (cur < (uint32_t)n) buf[cur] = (uint16_t)prev;
+          if (cur < (uint32_t)n) buf[cur] = (uint16_t)(kPow2 || prev < (uint32_t)n ? prev : 0xFFFFu);
           else bad = true;
         }
       }
@@ -125,12 +135,14 @@ __global__ void __launch_bounds__(256) k_ring_route(RouteArgs a, const P* __rest
       const int h0 = c << 3;
       const int b = h0 / a.R;
       const int s0 = h0 - b * a.R;
-      // Valid entries are < n <= 8192, so only the 0xFFFF sentinel has bit 15
-      // set.  A chunk holding one is a bad order; its sentinels are zeroed so
-      // the score pass can index rows without clamping (in range either way).
-      if ((v.x | v.y | v.z | v.w) & 0x80008000u) {
+      // Valid entries are < n <= 8192: with a power-of-two n any bit of
+      // ~(n-1) marks a sentinel or an out-of-range value, otherwise only the
+      // 0xFFFF sentinel (bit 15) can remain.  A chunk holding one is a bad
+      // order; those entries are zeroed so the score pass can index rows
+      // without clamping (in range either way).
+      if ((v.x | v.y | v.z | v.w) & hmask) {
         bad = true;
-        v = make_uint4(clear_sentinels(v.x), clear_sentinels(v.y), clear_sentinels(v.z), clear_sentinels(v.w));
+        v = make_uint4(clear_bad(v.x, hmask), clear_bad(v.y, hmask), clear_bad(v.z, hmask), clear_bad(v.w, hmask));
       }
       *reinterpret_cast<uint4*>(pred + ((size_t)b * a.count + o) * a.R + s0) = v;
       buf4[c] = ones;
@@ -148,7 +160,6 @@ struct ScoreArgs {
   int stages;        // TMA ring depth
   int stage_orders;  // orders per TMA stage
   int vec;           // multi-order warp step (R in {32, 64, 128, 256}, n % R == 0)
-  int unroll;        // orders per lane group per step (C4 specialisation: 1 or 2)
   double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
   unsigned long long* acc;  // u16 codes: per-order integer sums accumulated atomically (exact)
 };
@@ -296,10 +307,10 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
           if (a.vec) {
             unsigned long long* accp = a.acc + o0 + st * kStageOrders;
             const int c = (int)cnt;
-            if (R == 64 && n == 1024) {  // C4
-              if (a.unroll == 2) score_stage_vec<8, 1024, 2>(sp, blk, n, c, warp, cw, lane, accp);
-              else score_stage_vec<8, 1024, 1>(sp, blk, n, c, warp, cw, lane, accp);
-            } else if (R == 32) score_stage_vec<4, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
+            // C4 (R=64, N=1024): row stride as LDS immediates, two orders per
+            // lane group (U=2 measured +0.9% over U=1 on B200)
+            if (R == 64 && n == 1024) score_stage_vec<8, 1024, 2>(sp, blk, n, c, warp, cw, lane, accp);
+            else if (R == 32) score_stage_vec<4, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
             else if (R == 64) score_stage_vec<8, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
             else if (R == 128) score_stage_vec<16, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
             else score_stage_vec<32, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
@@ -411,28 +422,33 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   auto set = [](auto kern, size_t bytes) {
     if (bytes > 48 * 1024) RW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   };
-  static const int score_unroll = [] {
-    const char* e = std::getenv("RW_RING_SCORE_UNROLL");
-    return e && std::atoi(e) == 2 ? 2 : 1;
-  }();
+  const bool pow2 = (n & (n - 1)) == 0;
   const bool int_sums = p.storage == RW_STORAGE_U16;
   if (int_sums) RW_CUDA(cudaMemsetAsync(d_costs, 0, (size_t)batch * 8, st));
   for (int64_t off = 0; off < batch; off += kmax) {
     const int64_t cnt_o = std::min(kmax, batch - off);
     RouteArgs ra{cnt_o, off, n, R, nblocks, reinterpret_cast<unsigned long long*>(err_slot)};
-    const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt_o + 7) / 8, (int64_t)sms * 8));
+    // One full wave of resident route CTAs (grid-stride over the orders):
+    // every CTA does the same work, so a partial second wave would be a tail.
+    auto rgrid = [&](auto kern) {
+      int per_sm = 0;
+      RW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, route_smem));
+      return (int)std::max<int64_t>(1, std::min<int64_t>((cnt_o + 7) / 8, (int64_t)sms * std::max(1, per_sm)));
+    };
     if (perm_bytes == 2) {
-      auto k = validate ? k_ring_route<uint16_t, true> : k_ring_route<uint16_t, false>;
+      auto k = pow2 ? (validate ? k_ring_route<uint16_t, true, true> : k_ring_route<uint16_t, false, true>)
+                    : (validate ? k_ring_route<uint16_t, true, false> : k_ring_route<uint16_t, false, false>);
       set(k, route_smem);
-      k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const uint16_t*>(d_perms) + off * n, predbuf);
+      k<<<rgrid(k), 256, route_smem, st>>>(ra, static_cast<const uint16_t*>(d_perms) + off * n, predbuf);
     } else {
-      auto k = validate ? k_ring_route<int32_t, true> : k_ring_route<int32_t, false>;
+      auto k = pow2 ? (validate ? k_ring_route<int32_t, true, true> : k_ring_route<int32_t, false, true>)
+                    : (validate ? k_ring_route<int32_t, true, false> : k_ring_route<int32_t, false, false>);
       set(k, route_smem);
-      k<<<rgrid, 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
+      k<<<rgrid(k), 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
     const int vec = (R == 32 || R == 64 || R == 128 || R == 256) && n % R == 0 ? 1 : 0;
-    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, score_unroll, part,
+    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
     const int sgrid = (int)std::min<int64_t>(sms, (int64_t)nblocks * ((cnt_o + kStageOrders - 1) / kStageOrders));
     switch (p.storage) {

@@ -115,6 +115,67 @@ def test_forced_storage_kinds_agree(port, storage):
         assert np.array_equal(prob.evaluate_batch(spec, perms, exact=True), want)
 
 
+@pytest.mark.parametrize("path", ["transpose", "l2"])
+def test_uint16_device_orders_out_of_range(path):
+    """Device-resident uint16 orders holding values in [n, 0x8000) and >= 0x8000
+    on the ring paths at C4: the route pass stores them as its sentinel, so the
+    unclamped score lookups stay in range; the batch raises domain_error naming
+    the entry, and a clean batch on the same problem is exact afterwards."""
+    import torch
+    m = fixtures.config_matrix("C4", "fixed")
+    z = np.load(os.path.join(GOLD, "batch_C4_fixed.npz"))
+    perms = z["perms"]
+    prob = rw.Problem(m)
+    prob.set_path(path)
+    spec = spec_from(z["spec_ring"], float(z["size_ring"][0]))
+    n = perms.shape[1]
+    c = torch.empty(perms.shape[0], dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for row, col, val in ((0, 0, n), (1, 511, 0x7FFF), (2, n - 1, 0x8000), (3, 100, 0xFFFF), (1, 1, 5000)):
+        bad = perms.astype(np.uint16)
+        bad[row, col] = val
+        d = torch.from_numpy(bad.view(np.int16)).cuda()
+        prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(), stream)
+        torch.cuda.synchronize()
+        with pytest.raises(rw.DomainError, match=f"batch entry {row}"):
+            prob.sync_errors()
+    d = torch.from_numpy(perms.astype(np.uint16).view(np.int16)).cuda()
+    prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(), stream)
+    torch.cuda.synchronize()
+    prob.sync_errors()
+    assert np.array_equal(c.cpu().numpy(), z["cost_ring"])
+
+
+@pytest.mark.parametrize("n", [1000, 1280])
+def test_uint16_device_orders_out_of_range_non_pow2(port, n):
+    """Non-power-of-two N on the ring transpose path (n % 256 != 0: per-entry
+    route; n % 256 == 0: vectorised route): an out-of-range predecessor is
+    stored as the sentinel, the batch raises, and clean orders match the oracle."""
+    import torch
+    rng = np.random.default_rng(n)
+    m = rng.integers(0, 3000, size=(n, n)).astype(np.float64) / 16.0
+    np.fill_diagonal(m, 0.0)
+    prob = rw.Problem(m)
+    prob.set_path("transpose")
+    spec = rw.CollectiveSpec(rw.Algorithm.Ring, n, 2.0 ** 20)
+    perms = np.array([rng.permutation(n) for _ in range(24)], dtype=np.int32)
+    c = torch.empty(perms.shape[0], dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for row, col, val in ((0, 0, n), (5, 17, 0x7FFF), (23, n - 1, 0xFFFF)):
+        bad = perms.astype(np.uint16)
+        bad[row, col] = val
+        d = torch.from_numpy(bad.view(np.int16)).cuda()
+        prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(), stream)
+        torch.cuda.synchronize()
+        with pytest.raises(rw.DomainError, match=f"batch entry {row}"):
+            prob.sync_errors()
+    d = torch.from_numpy(perms.astype(np.uint16).view(np.int16)).cuda()
+    prob.evaluate_batch_device(spec, d.data_ptr(), 2, perms.shape[0], c.data_ptr(), stream)
+    torch.cuda.synchronize()
+    prob.sync_errors()
+    assert np.array_equal(c.cpu().numpy(), port.evaluate_batch(m, perms, make_spec(0, n, 2.0 ** 20)))
+
+
 def test_large_batch_chunking_and_uint16_device_path(port):
     import torch
     m = fixtures.config_matrix("C3", "fixed")
