@@ -205,7 +205,10 @@ struct RScoreArgs {
   void* keys;   // [round][order]
 };
 
-template <typename T, int R>
+// kAll: every host is a source (xor pairing), so the route wrote no
+// sentinels and every partner is < n (stage_order_vec masks entries into
+// range): the per-lookup range test is dropped.
+template <typename T, int R, bool kAll>
 __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, const uint16_t* __restrict__ buf,
                                                                const T* __restrict__ gmat) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
               const uint32_t col = (h & 1) ? (w[h >> 1] >> 16) : (w[h >> 1] & 0xFFFFu);
-              if (col < (uint32_t)n) {
+              if (kAll || col < (uint32_t)n) {
                 const K v = KeyOf<T>::enc(blk[(c * 8 + h) * n + col]);
                 key = v > key ? v : key;
               }
@@ -330,18 +333,19 @@ __global__ void k_rounds_finalize(RFinalArgs a, const void* __restrict__ keys_v,
 }
 
 template <typename T, int R>
-void launch_score(const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat, cudaStream_t st) {
-  auto k = k_rounds_score<T, R>;
+void launch_score(const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat, cudaStream_t st,
+                  bool all) {
+  auto k = all ? k_rounds_score<T, R, true> : k_rounds_score<T, R, false>;
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, kRThreads, smem, st>>>(sa, buf, static_cast<const T*>(mat));
 }
 
 template <typename T>
 void launch_score_r(int R, const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat,
-                    cudaStream_t st) {
-  if (R == 32) launch_score<T, 32>(sa, grid, smem, buf, mat, st);
-  else if (R == 16) launch_score<T, 16>(sa, grid, smem, buf, mat, st);
-  else launch_score<T, 8>(sa, grid, smem, buf, mat, st);
+                    cudaStream_t st, bool all) {
+  if (R == 32) launch_score<T, 32>(sa, grid, smem, buf, mat, st, all);
+  else if (R == 16) launch_score<T, 16>(sa, grid, smem, buf, mat, st, all);
+  else launch_score<T, 8>(sa, grid, smem, buf, mat, st, all);
 }
 
 }  // namespace
@@ -414,11 +418,12 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
     void* args[] = {&ra, (void*)&perms, (void*)&buf};
     RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), args, route_smem, st));
     RScoreArgs sa{cnt_o, n, rounds, nblocks, stages, kRStageOrders, keys};
+    const bool xor_all = plan.pairing == RW_PAIRING_XOR;
     const int sgrid = (int)std::min<int64_t>(sms, nblocks * ((cnt_o + kRStageOrders - 1) / kRStageOrders));
     switch (p.storage) {
-      case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
-      case RW_STORAGE_F32: launch_score_r<float>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
-      default: launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st); break;
+      case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all); break;
+      case RW_STORAGE_F32: launch_score_r<float>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all); break;
+      default: launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all); break;
     }
     RW_CUDA(cudaGetLastError());
     fa.count = cnt_o;
