@@ -24,7 +24,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
-#include <type_traits>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
@@ -209,14 +208,12 @@ struct RScoreArgs {
 // kAll: every host is a source (xor pairing), so the route wrote no
 // sentinels and every partner is < n (stage_order_vec masks entries into
 // range): the per-lookup range test is dropped.
-// NN > 0 fixes the row length at compile time (C5: the row offsets become
-// LDS immediates); NN == 0 reads it from the arguments.
-template <typename T, int R, bool kAll, int NN = 0>
+template <typename T, int R, bool kAll>
 __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, const uint16_t* __restrict__ buf,
                                                                const T* __restrict__ gmat) {
   extern __shared__ __align__(16) unsigned char smem[];
   using K = typename KeyOf<T>::type;
-  const int n = NN > 0 ? NN : a.n, rounds = a.rounds;
+  const int n = a.n, rounds = a.rounds;
   T* blk = reinterpret_cast<T*>(smem);
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem + al16((size_t)R * n * sizeof(T)));
   __shared__ __align__(8) uint64_t full[kRMaxStages], empty[kRMaxStages], mat_bar;
@@ -339,8 +336,6 @@ template <typename T, int R>
 void launch_score(const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat, cudaStream_t st,
                   bool all) {
   auto k = all ? k_rounds_score<T, R, true> : k_rounds_score<T, R, false>;
-  if constexpr (std::is_same<T, uint16_t>::value && R == 16)
-    if (sa.n == 4096) k = all ? k_rounds_score<T, R, true, 4096> : k_rounds_score<T, R, false, 4096>;
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, kRThreads, smem, st>>>(sa, buf, static_cast<const T*>(mat));
 }
