@@ -160,6 +160,7 @@ struct ScoreArgs {
   int stages;        // TMA ring depth
   int stage_orders;  // orders per TMA stage
   int vec;           // multi-order warp step (R in {32, 64, 128, 256}, n % R == 0)
+  int rotate;        // rotate the consumer deal per stage (1; 0 = fixed warp-0-first deal, -1.9% at C4)
   double* part;    // [nblocks][count] partial sums (coalesced for the combine pass)
   unsigned long long* acc;  // u16 codes: per-order integer sums accumulated atomically (exact)
 };
@@ -193,7 +194,8 @@ __device__ __forceinline__ uint32_t lo16(uint32_t w) {
 }
 
 template <int LPO, int N, int U>
-__device__ __forceinline__ void score_stage_vec(const uint16_t* sp, const uint16_t* blk, int n, int cnt, int warp,
+__device__ __forceinline__ void score_stage_vec(uint32_t gi, int stage_orders, bool rotate, const uint16_t* sp,
+                                                const uint16_t* blk, int n, int cnt, int warp,
                                                 int cw, int lane, unsigned long long* __restrict__ accp) {
   constexpr int OPW = 32 / LPO, R = 8 * LPO;
   const int sub = lane & (LPO - 1), kk = lane / LPO;
@@ -202,7 +204,13 @@ __device__ __forceinline__ void score_stage_vec(const uint16_t* sp, const uint16
   const uint32_t src = (uint32_t)__cvta_generic_to_shared(sp) + (uint32_t)(kk * R + sub * 8) * 2u;
   // U orders per lane group per step: more lookups in flight, loop and
   // atomic-address overhead shared.
-  for (int k0 = warp * OPW * U; k0 < cnt; k0 += cw * OPW * U) {
+  // Lane-group steps are dealt round-robin over the consumer warps as one
+  // continuous stream across stages (rotated by the stage counter gi): a
+  // 384-order stage is 48 steps of 8 orders for 31 warps, and a fixed
+  // warp-0-first deal would give the same 17 warps the extra step every stage.
+  const int rot = rotate ? (int)((uint64_t)gi * (uint32_t)(stage_orders / (OPW * U)) % (uint32_t)cw) : 0;
+  const int w0 = warp - rot < 0 ? warp - rot + cw : warp - rot;
+  for (int k0 = w0 * OPW * U; k0 < cnt; k0 += cw * OPW * U) {
     uint32_t acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -306,14 +314,15 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
         if constexpr (kInt) {
           if (a.vec) {
             unsigned long long* accp = a.acc + o0 + st * kStageOrders;
+            const bool rot = a.rotate != 0;
             const int c = (int)cnt;
             // C4 (R=64, N=1024): row stride as LDS immediates, two orders per
             // lane group (U=2 measured +0.9% over U=1 on B200)
-            if (R == 64 && n == 1024) score_stage_vec<8, 1024, 2>(sp, blk, n, c, warp, cw, lane, accp);
-            else if (R == 32) score_stage_vec<4, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
-            else if (R == 64) score_stage_vec<8, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
-            else if (R == 128) score_stage_vec<16, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
-            else score_stage_vec<32, 0, 1>(sp, blk, n, c, warp, cw, lane, accp);
+            if (R == 64 && n == 1024) score_stage_vec<8, 1024, 2>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, accp);
+            else if (R == 32) score_stage_vec<4, 0, 1>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, accp);
+            else if (R == 64) score_stage_vec<8, 0, 1>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, accp);
+            else if (R == 128) score_stage_vec<16, 0, 1>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, accp);
+            else score_stage_vec<32, 0, 1>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, accp);
           } else
           // u16 codes: a block partial is < R * 65536 <= 2^32 (R <= 1024 here)
           for (int k = warp; k < cnt; k += cw) {
@@ -448,7 +457,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
     }
     RW_CUDA(cudaGetLastError());
     const int vec = (R == 32 || R == 64 || R == 128 || R == 256) && n % R == 0 ? 1 : 0;
-    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, part,
+    ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, 1, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
     const int sgrid = (int)std::min<int64_t>(sms, (int64_t)nblocks * ((cnt_o + kStageOrders - 1) / kStageOrders));
     switch (p.storage) {
