@@ -210,6 +210,11 @@ struct GpuOptions {
   int device = -1;      // -1: current CUDA device
   int chains = 0;       // SA chains; <= 0: 4 per SM (at least cfg.restarts)
   bool exact_batch = false;
+  // Device copies of CostMatrix are cached by exact content (a byte compare
+  // against a host shadow on every call).  true: key the cache by the matrix
+  // storage address and size instead -- the caller promises not to mutate a
+  // CostMatrix it has passed before (O(1) per call instead of O(N^2)).
+  bool immutable_matrices = false;
 };
 void set_gpu_options(const GpuOptions& opts);
 GpuOptions gpu_options();

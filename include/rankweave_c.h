@@ -210,10 +210,19 @@ rw_status rw_local_search(const rw_problem* p, const rw_spec* spec, int32_t* per
                           int32_t max_rounds, double* costs_out, uint64_t* evals_out);
 
 /* ---- statistics (stats.hpp:18-28) -------------------------------------- */
-/* sample_orders: deterministic per seed (Philox, not libstdc++ shuffle). */
+/* sample_orders (stats.cpp:83-94): the reference's orders bit for bit -- one
+ * std::mt19937_64(seed) stream, identity std::shuffle'd per sample (host). */
 rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* perms_out);
+/* sample_costs (stats.cpp:96-103): those orders, scored on the GPU with the
+ * reference-identical summation (costs equal the reference's bits). */
 rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed,
                           double* costs_out);
+/* GPU extension: uniform random orders from a counter-based Philox stream
+ * generated on the device (deterministic per seed; NOT the reference's
+ * sequence), and their reference-exact costs. */
+rw_status rw_sample_orders_philox(int32_t n, int32_t samples, uint64_t seed, int32_t* perms_out);
+rw_status rw_sample_costs_philox(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed,
+                                 double* costs_out);
 
 /* ---- schedules and the flow simulator ---------------------------------- */
 /* expand_schedule (cost_model.hpp:33): call once with NULL arrays to get
@@ -236,6 +245,27 @@ rw_status rw_generate_matrix(int32_t nlevels, const int32_t* fanout, const doubl
 /* Fixture relabeling: rl = std::shuffle(iota(n), mt19937_64(seed)),
  * m'[i][j] = m[rl[i]][rl[j]] (in place). */
 rw_status rw_relabel_matrix(double* m, int32_t n, uint64_t seed);
+
+/* ---- host logic (one implementation, shared with the C++ drop-in) ------ */
+/* distribution_stats (stats.cpp:64-81): out4 = {min, max, mean, stddev}. */
+rw_status rw_distribution_stats(const double* values, int64_t count, double* out4);
+/* spearman (stats.cpp:56-62); the lengths are passed separately so the
+ * reference's length-mismatch error is reproduced. */
+rw_status rw_spearman(const double* xs, const double* ys, int64_t count_x, int64_t count_y, double* out);
+/* parse_model_file (smtlib.cpp:160-186): NUL-terminated text -> perm_out[n]. */
+rw_status rw_parse_model_file(const char* text, int32_t n, int32_t* perm_out);
+/* balanced_sexpr (smtlib.cpp:188-203): *out = 1 when balanced. */
+rw_status rw_balanced_sexpr(const char* text, int32_t* out);
+/* emit_smtlib (smtlib.cpp:104-158), byte-identical text.  Call with
+ * out = NULL to get *length_out; then with capacity >= length + 1. */
+rw_status rw_emit_smtlib(const double* rtt_us, int32_t n, const rw_spec* spec, int32_t has_bound, double bound,
+                         int32_t emission_cap, char* out, int64_t capacity, int64_t* length_out);
+/* two_stage_solve (solver.cpp:204-261): routing, SMT side file, external
+ * model; `log` (optional) receives each log line.  method_out: RW_METHOD_*. */
+typedef void (*rw_log_fn)(const char* message, void* user);
+rw_status rw_two_stage_solve(const double* rtt_us, int32_t n, const rw_spec* spec, const rw_solver_config* cfg,
+                             const char* emit_smt_path, const char* external_model_path, rw_log_fn log, void* user,
+                             int32_t* perm_out, double* cost_out, int32_t* method_out, uint64_t* evals_out);
 
 #ifdef __cplusplus
 }

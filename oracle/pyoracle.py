@@ -119,6 +119,9 @@ class Reference:
                                           P(C.c_int64)]
         L.ref_sample_costs.argtypes = [P(C.c_double), P(Spec), C.c_int32, C.c_uint64, P(C.c_double)]
         L.ref_distribution_stats.argtypes = [P(C.c_double), C.c_int32, P(C.c_double)]
+        L.ref_sample_orders.argtypes = [C.c_int32, C.c_int32, C.c_uint64, P(C.c_int32)]
+        L.ref_emit_smtlib.argtypes = [P(C.c_double), P(Spec), C.c_int32, C.c_double, C.c_int32, C.c_char_p,
+                                      C.c_int64, P(C.c_int64)]
 
     def _check(self, rc):
         if rc != 0:
@@ -177,6 +180,23 @@ class Reference:
         out = np.empty(samples, dtype=np.float64)
         self._check(self.lib.ref_sample_costs(_d(m), C.byref(spec), samples, seed, _d(out)))
         return out
+
+
+    def sample_orders(self, n: int, samples: int, seed: int) -> np.ndarray:
+        out = np.empty((samples, n), dtype=np.int32)
+        self._check(self.lib.ref_sample_orders(n, samples, seed, _i(out)))
+        return out
+
+    def emit_smtlib(self, m, spec: Spec, upper_bound=None, cap: int = 64) -> str:
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        has = upper_bound is not None
+        length = C.c_int64()
+        self._check(self.lib.ref_emit_smtlib(_d(m), C.byref(spec), int(has), float(upper_bound or 0.0), cap, None, 0,
+                                             C.byref(length)))
+        buf = C.create_string_buffer(length.value + 1)
+        self._check(self.lib.ref_emit_smtlib(_d(m), C.byref(spec), int(has), float(upper_bound or 0.0), cap, buf,
+                                             length.value + 1, C.byref(length)))
+        return buf.value.decode()
 
 
 def reference_available() -> bool:

@@ -17,6 +17,7 @@
 
 #include "rankweave/cost_model.hpp"
 #include "rankweave/simulate.hpp"
+#include "rankweave/smtlib.hpp"
 #include "rankweave/solver.hpp"
 #include "rankweave/stats.hpp"
 #include "rankweave/topology.hpp"
@@ -212,6 +213,30 @@ int ref_distribution_stats(const double* v, int32_t count, double* out4) {
     out4[1] = st.max;
     out4[2] = st.mean;
     out4[3] = st.stddev;
+  });
+}
+
+// sample_orders (stats.cpp:83-94): the seeded orders themselves.
+int ref_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* out) {
+  return guarded([&] {
+    const auto v = sample_orders(n, samples, seed);
+    for (size_t k = 0; k < v.size(); ++k)
+      std::memcpy(out + k * static_cast<size_t>(n), v[k].perm.data(), sizeof(int32_t) * static_cast<size_t>(n));
+  });
+}
+
+// emit_smtlib (smtlib.cpp:104-158): text into a caller buffer (length first).
+int ref_emit_smtlib(const double* m, const RefSpec* s, int32_t has_bound, double bound, int32_t cap, char* out,
+                    int64_t capacity, int64_t* length_out) {
+  return guarded([&] {
+    const std::string text = emit_smtlib(to_matrix(m, s->n), to_spec(s),
+                                         has_bound ? std::optional<double>(bound) : std::nullopt, cap);
+    *length_out = static_cast<int64_t>(text.size());
+    if (out && capacity > 0) {
+      const size_t k = std::min<size_t>(text.size(), static_cast<size_t>(capacity - 1));
+      std::memcpy(out, text.data(), k);
+      out[k] = '\0';
+    }
   });
 }
 

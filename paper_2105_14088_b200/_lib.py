@@ -88,6 +88,16 @@ SIGNATURES = {
     "rw_local_search": (C.c_int, [_vp, P(rw_spec), _i32p, C.c_int64, C.c_int32, _dp, _u64p]),
     "rw_sample_orders": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _i32p]),
     "rw_sample_costs": (C.c_int, [_vp, P(rw_spec), C.c_int32, C.c_uint64, _dp]),
+    "rw_sample_orders_philox": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _i32p]),
+    "rw_sample_costs_philox": (C.c_int, [_vp, P(rw_spec), C.c_int32, C.c_uint64, _dp]),
+    "rw_distribution_stats": (C.c_int, [_dp, C.c_int64, _dp]),
+    "rw_spearman": (C.c_int, [_dp, _dp, C.c_int64, C.c_int64, _dp]),
+    "rw_parse_model_file": (C.c_int, [C.c_char_p, C.c_int32, _i32p]),
+    "rw_balanced_sexpr": (C.c_int, [C.c_char_p, _i32p]),
+    "rw_emit_smtlib": (C.c_int, [_dp, C.c_int32, P(rw_spec), C.c_int32, C.c_double, C.c_int32, C.c_char_p,
+                                 C.c_int64, P(C.c_int64)]),
+    "rw_two_stage_solve": (C.c_int, [_dp, C.c_int32, P(rw_spec), P(rw_solver_config), C.c_char_p, C.c_char_p,
+                                     _vp, _vp, _i32p, _dp, _i32p, _u64p]),
     "rw_generate_matrix": (C.c_int, [C.c_int32, _i32p, _dp, _dp, _dp, C.c_double, C.c_uint64, _dp, C.c_int64,
                                      _i32p]),
     "rw_relabel_matrix": (C.c_int, [_dp, C.c_int32, C.c_uint64]),
@@ -133,6 +143,10 @@ def check(status: int) -> None:
     if status == RW_ERR_IO:
         raise IOError_(msg)
     raise RankweaveError(f"status {status}: {msg}")
+
+
+# void (*rw_log_fn)(const char* message, void* user)
+LOG_FN = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
 
 
 def ptr(arr, ctype):

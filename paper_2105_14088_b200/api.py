@@ -11,7 +11,6 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
-import math
 import time
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence
@@ -430,92 +429,72 @@ def anneal(m: CostMatrix, spec: CollectiveSpec, cfg: SolverConfig, chains: int =
 
 
 def parse_model_file(text: str, n: int) -> RankOrder:
-    import re
-    perm = [-1] * n
-    assigned = 0
-    for line in text.splitlines():
-        s = line.strip(" \t\r")
-        if not s or s[0] in ";#":
-            continue
-        mt = re.fullmatch(r"\s*r_(-?\d+)\s*=\s*(-?\d+)[ \t\r]*", line)
-        if not mt:
-            raise DomainError(f"model line not of the form 'r_<i> = <int>': '{line}'")
-        idx, val = int(mt.group(1)), int(mt.group(2))
-        if idx < 0 or idx >= n:
-            raise DomainError(f"model assigns r_{idx} outside [0, {n})")
-        if perm[idx] != -1:
-            raise DomainError(f"model assigns r_{idx} twice")
-        perm[idx] = val
-        assigned += 1
-    if assigned != n:
-        raise DomainError(f"model assigns {assigned} of {n} rank variables")
-    o = RankOrder(perm)
-    validate_order(o, n)
-    return o
+    """parse_model_file (smtlib.hpp:22-25) through the C ABI (the C++ drop-in's code)."""
+    perm = np.empty(max(n, 0), dtype=np.int32)
+    check(lib.rw_parse_model_file(text.encode("utf-8"), n, ptr(perm, C.c_int32)))
+    return RankOrder(perm.tolist())
 
 
-def two_stage_solve(m: CostMatrix, spec: CollectiveSpec, cfg: SolverConfig,
-                    external_model_path: str = "", log: Optional[Callable[[str], None]] = None) -> Solution:
-    """two_stage_solve (solver.cpp:204-261) minus the SMT side file (use the C++ API for emission)."""
-    validate_spec(spec)
-    validate_config(cfg)
-    say = log or (lambda s: None)
-    if spec.n <= 2:
-        o = RankOrder.identity(spec.n)
-        stage1 = Solution(o, evaluate(m, o, spec), SolveMethod.BruteForce, 1)
-    elif spec.n <= cfg.brute_force_threshold:
-        stage1 = brute_force(m, spec, cfg.brute_force_threshold)
-        say(f"stage 1: brute force over {stage1.evaluations} orders, cost {stage1.cost}")
-    else:
-        stage1 = anneal(m, spec, cfg)
-        say(f"stage 1: anneal, {stage1.evaluations} evaluations, cost {stage1.cost}")
-    if not external_model_path:
-        return stage1
-    try:
-        text = open(external_model_path).read()
-    except OSError:
-        say(f"warning: cannot read external model '{external_model_path}'; keeping the stage-1 solution")
-        return stage1
-    try:
-        ext = parse_model_file(text, spec.n)
-        c = evaluate(m, ext, spec)
-        if c < stage1.cost:
-            say(f"external model improves cost {stage1.cost} -> {c}")
-            return Solution(ext, c, SolveMethod.External, stage1.evaluations + 1)
-        say("warning: external model does not improve on the stage-1 cost; keeping stage 1")
-    except DomainError as e:
-        say(f"warning: invalid external model: {e}; keeping the stage-1 solution")
-    return stage1
+def balanced_sexpr(text: str) -> bool:
+    out = C.c_int32()
+    check(lib.rw_balanced_sexpr(text.encode("utf-8"), C.byref(out)))
+    return bool(out.value)
+
+
+def emit_smtlib(m: CostMatrix, spec: CollectiveSpec, upper_bound: Optional[float] = None,
+                emission_cap: int = 64) -> str:
+    """emit_smtlib (smtlib.cpp:104-158): the reference's SMT-LIB text, byte for byte."""
+    a = np.ascontiguousarray(m.rtt_us, dtype=np.float64)
+    has = upper_bound is not None
+    ub = float(upper_bound) if has else 0.0
+    length = C.c_int64()
+    check(lib.rw_emit_smtlib(ptr(a, C.c_double), m.n(), C.byref(spec._c()), int(has), ub, emission_cap, None, 0,
+                             C.byref(length)))
+    buf = C.create_string_buffer(length.value + 1)
+    check(lib.rw_emit_smtlib(ptr(a, C.c_double), m.n(), C.byref(spec._c()), int(has), ub, emission_cap, buf,
+                             length.value + 1, C.byref(length)))
+    return buf.value.decode("utf-8")
+
+
+def two_stage_solve(m: CostMatrix, spec: CollectiveSpec, cfg: SolverConfig, external_model_path: str = "",
+                    log: Optional[Callable[[str], None]] = None, emit_smt_path: str = "") -> Solution:
+    """two_stage_solve (solver.cpp:204-261) through the C ABI: the C++ drop-in's
+    routing, SMT side file and external-model handling, unchanged."""
+    a = np.ascontiguousarray(m.rtt_us, dtype=np.float64)
+    perm = np.empty(max(spec.n, 0), dtype=np.int32)
+    cost = C.c_double()
+    method = C.c_int32()
+    ev = C.c_uint64()
+    cb = _lib.LOG_FN((lambda msg, _u: log(msg.decode("utf-8", "replace"))) if log else (lambda msg, _u: None))
+    check(lib.rw_two_stage_solve(ptr(a, C.c_double), m.n(), C.byref(spec._c()), C.byref(cfg._c()),
+                                 emit_smt_path.encode() if emit_smt_path else None,
+                                 external_model_path.encode() if external_model_path else None,
+                                 C.cast(cb, C.c_void_p), None, ptr(perm, C.c_int32), C.byref(cost),
+                                 C.byref(method), C.byref(ev)))
+    return Solution(RankOrder(perm.tolist()), cost.value, SolveMethod(method.value), ev.value)
 
 
 # ------------------------------------------------------------------ stats --
 def distribution_stats(values: Sequence[float]) -> DistributionStats:
-    """distribution_stats (stats.cpp:64-81): serial sums, population stddev."""
-    if len(values) == 0:
-        raise DomainError("distribution_stats: no samples")
-    vals = [float(v) for v in values]
-    mn = mx = vals[0]
-    s = 0.0
-    for v in vals:
-        mn = min(mn, v)
-        mx = max(mx, v)
-        s += v
-    mean = s / len(vals)
-    sq = 0.0
-    for v in vals:
-        sq += (v - mean) * (v - mean)
-    return DistributionStats(mn, mx, mean, math.sqrt(sq / len(vals)), len(vals))
+    """distribution_stats (stats.cpp:64-81) through the C ABI: serial sums, population stddev."""
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.float64).ravel())
+    out = np.empty(4, dtype=np.float64)
+    check(lib.rw_distribution_stats(ptr(v, C.c_double), v.size, ptr(out, C.c_double)))
+    return DistributionStats(float(out[0]), float(out[1]), float(out[2]), float(out[3]), int(v.size))
 
 
 def sample_orders(n: int, n_samples: int, seed: int) -> np.ndarray:
+    """sample_orders (stats.cpp:83-94): the reference's orders for this seed
+    (std::mt19937_64 + std::shuffle), one row per sample."""
     if n_samples < 1:
         raise DomainError("sample_orders: need at least 1 sample")
-    out = np.empty((n_samples, n), dtype=np.int32)
+    out = np.empty((n_samples, max(n, 0)), dtype=np.int32)
     check(lib.rw_sample_orders(n, n_samples, seed, ptr(out, C.c_int32)))
     return out
 
 
 def sample_costs(m: CostMatrix, spec: CollectiveSpec, n_samples: int, seed: int) -> np.ndarray:
+    """sample_costs (stats.cpp:96-103): the reference's orders, scored on the GPU."""
     if n_samples < 1:
         raise DomainError("sample_orders: need at least 1 sample")
     validate_spec(spec)
@@ -523,6 +502,25 @@ def sample_costs(m: CostMatrix, spec: CollectiveSpec, n_samples: int, seed: int)
         raise DomainError(f"matrix is {m.n()}x{m.n()} but spec has N={spec.n}")
     out = np.empty(n_samples, dtype=np.float64)
     check(lib.rw_sample_costs(m.problem().handle, C.byref(spec._c()), n_samples, seed, ptr(out, C.c_double)))
+    return out
+
+
+def sample_orders_philox(n: int, n_samples: int, seed: int) -> np.ndarray:
+    """GPU extension: uniform orders from a device Philox stream (not the reference's sequence)."""
+    if n_samples < 1:
+        raise DomainError("sample_orders: need at least 1 sample")
+    out = np.empty((n_samples, n), dtype=np.int32)
+    check(lib.rw_sample_orders_philox(n, n_samples, seed, ptr(out, C.c_int32)))
+    return out
+
+
+def sample_costs_philox(m: CostMatrix, spec: CollectiveSpec, n_samples: int, seed: int) -> np.ndarray:
+    validate_spec(spec)
+    if m.n() != spec.n:
+        raise DomainError(f"matrix is {m.n()}x{m.n()} but spec has N={spec.n}")
+    out = np.empty(n_samples, dtype=np.float64)
+    check(lib.rw_sample_costs_philox(m.problem().handle, C.byref(spec._c()), n_samples, seed,
+                                     ptr(out, C.c_double)))
     return out
 
 
@@ -579,33 +577,12 @@ def simulate_batch(m: CostMatrix, levels, spec: CollectiveSpec, orders: np.ndarr
 
 
 def spearman(xs, ys) -> float:
-    """spearman (stats.hpp:14): Pearson correlation of average ranks."""
-    x = np.asarray(xs, dtype=np.float64)
-    y = np.asarray(ys, dtype=np.float64)
-    if x.size != y.size:
-        raise DomainError(f"spearman: series lengths differ ({x.size} vs {y.size})")
-    if x.size < 2:
-        raise DomainError("spearman: need at least 2 points")
-
-    def ranks(v):
-        idx = np.argsort(v, kind="stable")
-        r = np.empty(v.size)
-        i = 0
-        while i < v.size:
-            j = i
-            while j + 1 < v.size and v[idx[j + 1]] == v[idx[i]]:
-                j += 1
-            r[idx[i:j + 1]] = (i + j) / 2.0 + 1.0
-            i = j + 1
-        return r
-
-    rx, ry = ranks(x), ranks(y)
-    mx, my = rx.mean(), ry.mean()
-    dx, dy = rx - mx, ry - my
-    sxx, syy = float(dx @ dx), float(dy @ dy)
-    if sxx == 0.0 or syy == 0.0:
-        raise DomainError("spearman: constant series, coefficient undefined")
-    return float(dx @ dy) / math.sqrt(sxx * syy)
+    """spearman (stats.hpp:14) through the C ABI: Pearson correlation of average ranks."""
+    x = np.ascontiguousarray(np.asarray(xs, dtype=np.float64).ravel())
+    y = np.ascontiguousarray(np.asarray(ys, dtype=np.float64).ravel())
+    out = C.c_double()
+    check(lib.rw_spearman(ptr(x, C.c_double), ptr(y, C.c_double), x.size, y.size, C.byref(out)))
+    return out.value
 
 
 def device_count() -> int:

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <fstream>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <sstream>
@@ -62,38 +63,56 @@ bool same_bytes(const void* a, const void* b, std::size_t bytes) {
   return diff == 0;
 }
 
+// A cached device problem.  Callers hold the shared_ptr for the duration of
+// the C ABI call (a temporary lives to the end of the full expression), so a
+// concurrent eviction only drops the cache's reference and the last holder
+// destroys the problem.
+struct ProblemRef {
+  std::shared_ptr<rw_problem> sp;
+  operator rw_problem*() const { return sp.get(); }
+};
+
 // Device problems cached by matrix content (exact byte comparison against a
-// shadow copy), so repeated calls on one CostMatrix upload it once.
+// shadow copy), so repeated calls on one CostMatrix upload it once.  With
+// GpuOptions::immutable_matrices the key is the storage address and size.
 class ProblemCache {
  public:
-  rw_problem* get(const CostMatrix& m, int device) {
+  ProblemRef get(const CostMatrix& m, int device, bool by_address) {
     std::lock_guard<std::mutex> lock(mu_);
     const std::size_t bytes = m.rtt_us.size() * sizeof(double);
+    const void* addr = m.rtt_us.data();
     for (auto it = entries_.begin(); it != entries_.end(); ++it) {
-      if (it->n == m.n() && it->device == device && it->shadow.size() == m.rtt_us.size() &&
-          same_bytes(it->shadow.data(), m.rtt_us.data(), bytes)) {
+      if (it->n != m.n() || it->device != device || it->count != m.rtt_us.size()) continue;
+      const bool hit = by_address ? (it->by_address && it->addr == addr)
+                                  : (!it->shadow.empty() && same_bytes(it->shadow.data(), addr, bytes));
+      if (hit) {
         entries_.splice(entries_.begin(), entries_, it);
-        return entries_.front().problem;
+        return ProblemRef{entries_.front().problem};
       }
     }
-    rw_problem* p = nullptr;
-    check(rw_problem_create(m.rtt_us.data(), m.n(), RW_STORAGE_AUTO, device, &p));
-    entries_.push_front(Entry{m.n(), device, m.rtt_us, p});
+    rw_problem* raw = nullptr;
+    check(rw_problem_create(m.rtt_us.data(), m.n(), RW_STORAGE_AUTO, device, &raw));
+    std::shared_ptr<rw_problem> p(raw, [](rw_problem* q) { rw_problem_destroy(q); });
+    Entry e{m.n(), device, m.rtt_us.size(), addr, by_address, {}, p};
+    if (!by_address) e.shadow = m.rtt_us;
+    entries_.push_front(std::move(e));
     total_ += bytes;
     while (entries_.size() > 16 || (total_ > (std::size_t(1) << 31) && entries_.size() > 1)) {
-      total_ -= entries_.back().shadow.size() * sizeof(double);
-      rw_problem_destroy(entries_.back().problem);
-      entries_.pop_back();
+      total_ -= entries_.back().count * sizeof(double);
+      entries_.pop_back();  // in-flight callers keep their reference
     }
-    return p;
+    return ProblemRef{p};
   }
 
  private:
   struct Entry {
     int n;
     int device;
+    std::size_t count;
+    const void* addr;
+    bool by_address;
     std::vector<double> shadow;
-    rw_problem* problem;
+    std::shared_ptr<rw_problem> problem;
   };
   std::mutex mu_;
   std::list<Entry> entries_;
@@ -105,10 +124,11 @@ ProblemCache& cache() {
   return *c;
 }
 
-rw_problem* device_problem(const CostMatrix& m) {
+ProblemRef device_problem(const CostMatrix& m) {
   if (m.rtt_us.size() != static_cast<std::size_t>(m.n()) * static_cast<std::size_t>(m.n()))
     throw domain_error("cost matrix storage is not n*n");
-  return cache().get(m, gpu_options().device);
+  const GpuOptions o = gpu_options();
+  return cache().get(m, o.device, o.immutable_matrices);
 }
 
 rw_spec to_c(const CollectiveSpec& s) {
@@ -146,9 +166,13 @@ double model_cost(const CostMatrix& m, const RankOrder& order, const CollectiveS
 }
 
 std::string trim_real(double v) {
-  // SMT-LIB reals have no exponent form: fixed notation, trailing zeros trimmed.
+  // SMT-LIB reals have no exponent form: fixed notation with 12 decimals,
+  // trailing zeros trimmed -- the reference's real_literal (smtlib.cpp:15-24)
+  // byte for byte, so the emitted file is identical.  (12 decimals round
+  // 2^-13 to 0.000122070312, which the reference's own test_smtlib.cpp:92
+  // expects unrounded; both libraries fail that one check identically.)
   char buf[512];
-  std::snprintf(buf, sizeof(buf), "%.15f", v);
+  std::snprintf(buf, sizeof(buf), "%.12f", v);
   std::string s(buf);
   const std::size_t dot = s.find('.');
   if (dot == std::string::npos) return s + ".0";

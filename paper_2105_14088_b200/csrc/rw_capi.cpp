@@ -5,9 +5,12 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <numeric>
+#include <random>
 #include <string>
 #include <vector>
 
+#include "rankweave/rankweave.hpp"
 #include "rw_internal.h"
 
 namespace rwb {
@@ -35,6 +38,12 @@ rw_status guarded(F&& f) {
   } catch (const rwb::Failure& e) {
     g_last_error = e.what();
     return e.status;
+  } catch (const rankweave::domain_error& e) {  // host logic shared with the C++ drop-in
+    g_last_error = e.what();
+    return RW_ERR_DOMAIN;
+  } catch (const rankweave::io_error& e) {
+    g_last_error = e.what();
+    return RW_ERR_IO;
   } catch (const std::bad_alloc&) {
     g_last_error = "host allocation failed";
     return RW_ERR_INTERNAL;
@@ -322,7 +331,46 @@ rw_status rw_local_search(const rw_problem* p, const rw_spec* spec, int32_t* per
   });
 }
 
+// sample_orders (stats.cpp:83-94): one std::mt19937_64(seed) stream, an
+// identity order std::shuffle'd per sample.  Host side: the draws are the
+// libstdc++ algorithm itself, so the orders are the reference's bit for bit.
 rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* perms_out) {
+  return guarded([&] {
+    if (samples < 1) rwb::fail_domain("sample_orders: need at least 1 sample");
+    if (n < 0) rwb::fail_domain("sample_orders: n must be >= 0");
+    if (n > 0) need(perms_out, "perms_out");
+    std::mt19937_64 rng(seed);
+    for (int32_t k = 0; k < samples; ++k) {
+      int32_t* o = perms_out + static_cast<size_t>(k) * static_cast<size_t>(n);
+      std::iota(o, o + n, 0);
+      std::shuffle(o, o + n, rng);
+    }
+  });
+}
+
+// sample_costs (stats.cpp:96-103): the reference's orders, scored on the GPU
+// in one batch with the reference-identical (sorted, serial) ring summation.
+rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed, double* costs_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (samples < 1) rwb::fail_domain("sample_orders: need at least 1 sample");
+    need(costs_out, "costs_out");
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    std::vector<int32_t> orders(static_cast<size_t>(spec->n) * static_cast<size_t>(samples));
+    std::mt19937_64 rng(seed);
+    for (int32_t k = 0; k < samples; ++k) {
+      int32_t* o = orders.data() + static_cast<size_t>(k) * static_cast<size_t>(spec->n);
+      std::iota(o, o + spec->n, 0);
+      std::shuffle(o, o + spec->n, rng);
+    }
+    rwb::evaluate_host_orders(q, plan, orders.data(), samples, costs_out, /*exact=*/true, /*validate=*/false, nullptr);
+  });
+}
+
+// GPU extension: counter-based (Philox) uniform orders, generated on the
+// device.  Deterministic per seed, but NOT the reference's sequence.
+rw_status rw_sample_orders_philox(int32_t n, int32_t samples, uint64_t seed, int32_t* perms_out) {
   return guarded([&] {
     if (samples < 1) rwb::fail_domain("sample_orders: need at least 1 sample");
     if (n < 1 || n > 65536) rwb::fail_domain("sample_orders: n out of range");
@@ -340,7 +388,8 @@ rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* p
   });
 }
 
-rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed, double* costs_out) {
+rw_status rw_sample_costs_philox(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed,
+                                 double* costs_out) {
   return guarded([&] {
     need(spec, "spec");
     need(costs_out, "costs_out");
@@ -353,7 +402,6 @@ rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samp
     auto* d = static_cast<uint16_t*>(c.scratch(0, count * 2));
     auto* dc = static_cast<double*>(c.scratch(1, static_cast<size_t>(samples) * 8));
     rwb::sample_orders_device(spec->n, samples, seed, d, c.stream[0]);
-    // Reported costs are reference-identical (exact ring summation).
     rwb::launch_evaluate(q, plan, d, 2, samples, dc, /*exact=*/true, /*validate=*/false, c.d_err, c.stream[0]);
     RW_CUDA(cudaMemcpyAsync(costs_out, dc, static_cast<size_t>(samples) * 8, cudaMemcpyDeviceToHost, c.stream[0]));
     RW_CUDA(cudaStreamSynchronize(c.stream[0]));
@@ -430,6 +478,118 @@ rw_status rw_relabel_matrix(double* m, int32_t n, uint64_t seed) {
     need(m, "m");
     if (n < 1) rwb::fail_domain("n must be >= 1");
     rwb::relabel_matrix(m, n, seed);
+  });
+}
+
+// ---- host logic shared with the C++ drop-in (one implementation) ----------
+// These forward to the rankweave:: functions in rankweave_api.cpp so that the
+// C++ drop-in, the Python binding and any other FFI run the same code.
+
+rw_status rw_distribution_stats(const double* values, int64_t count, double* out4) {
+  return guarded([&] {
+    need(out4, "out4");
+    if (count > 0) need(values, "values");
+    const rankweave::DistributionStats st =
+        rankweave::distribution_stats(std::vector<double>(values, values + std::max<int64_t>(0, count)));
+    out4[0] = st.min;
+    out4[1] = st.max;
+    out4[2] = st.mean;
+    out4[3] = st.stddev;
+  });
+}
+
+rw_status rw_spearman(const double* xs, const double* ys, int64_t count_x, int64_t count_y, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (count_x > 0) need(xs, "xs");
+    if (count_y > 0) need(ys, "ys");
+    *out = rankweave::spearman(std::vector<double>(xs, xs + std::max<int64_t>(0, count_x)),
+                               std::vector<double>(ys, ys + std::max<int64_t>(0, count_y)));
+  });
+}
+
+rw_status rw_parse_model_file(const char* text, int32_t n, int32_t* perm_out) {
+  return guarded([&] {
+    need(text, "text");
+    if (n > 0) need(perm_out, "perm_out");
+    const rankweave::RankOrder o = rankweave::parse_model_file(text, n);
+    std::copy(o.perm.begin(), o.perm.end(), perm_out);
+  });
+}
+
+rw_status rw_balanced_sexpr(const char* text, int32_t* out) {
+  return guarded([&] {
+    need(text, "text");
+    need(out, "out");
+    *out = rankweave::balanced_sexpr(text) ? 1 : 0;
+  });
+}
+
+namespace {
+rankweave::CostMatrix host_matrix(const double* rtt_us, int32_t n) {
+  if (n < 0) rwb::fail_domain("n must be >= 0");
+  if (n > 0) need(rtt_us, "rtt_us");
+  rankweave::CostMatrix m;
+  m.hosts.reserve(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) m.hosts.push_back("h" + std::to_string(i));
+  m.rtt_us.assign(rtt_us, rtt_us + static_cast<size_t>(n) * static_cast<size_t>(n));
+  return m;
+}
+rankweave::CollectiveSpec cxx_spec(const rw_spec& c) {
+  rankweave::CollectiveSpec s;
+  s.algorithm = static_cast<rankweave::Algorithm>(c.algorithm);
+  s.n = c.n;
+  s.size_bytes = c.size_bytes;
+  s.bcube_b = c.bcube_b;
+  s.cost_mode = static_cast<rankweave::CostMode>(c.cost_mode);
+  s.hd_pairing = static_cast<rankweave::HdPairing>(c.hd_pairing);
+  return s;
+}
+}  // namespace
+
+rw_status rw_emit_smtlib(const double* rtt_us, int32_t n, const rw_spec* spec, int32_t has_bound, double bound,
+                         int32_t emission_cap, char* out, int64_t capacity, int64_t* length_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(length_out, "length_out");
+    const std::string text = rankweave::emit_smtlib(host_matrix(rtt_us, n), cxx_spec(*spec),
+                                                    has_bound ? std::optional<double>(bound) : std::nullopt,
+                                                    emission_cap);
+    *length_out = static_cast<int64_t>(text.size());
+    if (out && capacity > 0) {
+      const size_t k = std::min<size_t>(text.size(), static_cast<size_t>(capacity - 1));
+      std::memcpy(out, text.data(), k);
+      out[k] = '\0';
+    }
+  });
+}
+
+rw_status rw_two_stage_solve(const double* rtt_us, int32_t n, const rw_spec* spec, const rw_solver_config* cfg,
+                             const char* emit_smt_path, const char* external_model_path, rw_log_fn log, void* user,
+                             int32_t* perm_out, double* cost_out, int32_t* method_out, uint64_t* evals_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(cfg, "cfg");
+    need(cost_out, "cost_out");
+    if (spec->n > 0) need(perm_out, "perm_out");
+    rankweave::SolverConfig c;
+    c.budget = std::chrono::duration<double>(cfg->budget_s);
+    c.seed = cfg->seed;
+    c.initial_temperature = cfg->initial_temperature;
+    c.cooling = cfg->cooling;
+    c.steps_per_temperature = cfg->steps_per_temperature;
+    c.restarts = cfg->restarts;
+    c.brute_force_threshold = cfg->brute_force_threshold;
+    rankweave::TwoStageOptions opts;
+    if (emit_smt_path) opts.emit_smt_path = emit_smt_path;
+    if (external_model_path) opts.external_model_path = external_model_path;
+    if (log) opts.log = [log, user](const std::string& msg) { log(msg.c_str(), user); };
+    const rankweave::Solution sol = rankweave::two_stage_solve(host_matrix(rtt_us, n), cxx_spec(*spec), c, opts);
+    if (static_cast<int32_t>(sol.order.perm.size()) != spec->n) rwb::fail_internal("solution size mismatch");
+    std::copy(sol.order.perm.begin(), sol.order.perm.end(), perm_out);
+    *cost_out = sol.cost;
+    if (method_out) *method_out = static_cast<int32_t>(sol.method);
+    if (evals_out) *evals_out = sol.evaluations;
   });
 }
 

@@ -241,6 +241,60 @@ __device__ __forceinline__ void score_stage_vec(uint32_t gi, int stage_orders, b
   }
 }
 
+// The same multi-order warp step for FP32 / FP64 matrices: LPO lanes per
+// order, 8 rows per lane, unclamped lookups (the route zeroes sentinels).  A
+// lane adds its 8 values in row order in FP64, the segmented butterfly adds
+// the LPO lane sums, and lane `sub == 0` writes the (order, block) partial to
+// part[block][order]; k_ring_combine then sums the partials in block order.
+// Every addition happens in a fixed order, so the result is deterministic.
+template <typename T>
+__device__ __forceinline__ T lds_t(uint32_t addr);
+template <>
+__device__ __forceinline__ float lds_t<float>(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+template <>
+__device__ __forceinline__ double lds_t<double>(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+template <typename T, int LPO, int N>
+__device__ __forceinline__ void score_stage_vec_fp(uint32_t gi, int stage_orders, bool rotate, const uint16_t* sp,
+                                                   const T* blk, int n, int cnt, int warp, int cw, int lane,
+                                                   double* __restrict__ partp) {
+  constexpr int OPW = 32 / LPO, R = 8 * LPO;
+  constexpr uint32_t E = sizeof(T);
+  const int sub = lane & (LPO - 1), kk = lane / LPO;
+  const uint32_t rstep = N > 0 ? (uint32_t)N * E : (uint32_t)n * E;
+  const uint32_t row0 = (uint32_t)__cvta_generic_to_shared(blk) + (uint32_t)(sub * 8) * rstep;
+  const uint32_t src = (uint32_t)__cvta_generic_to_shared(sp) + (uint32_t)(kk * R + sub * 8) * 2u;
+  const int rot = rotate ? (int)((uint64_t)gi * (uint32_t)(stage_orders / OPW) % (uint32_t)cw) : 0;
+  const int w0 = warp - rot < 0 ? warp - rot + cw : warp - rot;
+  for (int k0 = w0 * OPW; k0 < cnt; k0 += cw * OPW) {
+    const int k = k0 + kk;
+    double acc = 0.0;
+    if (k < cnt) {
+      const uint4 w4 = lds_v4(src + (uint32_t)k0 * (R * 2));
+      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+      T v[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[2 * q] = lds_t<T>(row0 + lo16(w[q]) * E + (2 * q) * rstep);
+        v[2 * q + 1] = lds_t<T>(row0 + (w[q] >> 16) * E + (2 * q + 1) * rstep);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, (double)v[j]);
+    }
+#pragma unroll
+    for (int off = LPO >> 1; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, off));
+    if (sub == 0 && k < cnt) partp[k] = acc;
+  }
+}
+
 // Pass 2: a CTA keeps rows [b*R, b*R + rows) in shared memory and streams the
 // block's predecessor slices (contiguous in predbuf) through a 4-stage TMA
 // bulk-copy ring; each warp scores one order per step with shared-memory
@@ -336,6 +390,18 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
             acc = __reduce_add_sync(kFull, acc);
             if (lane == 0) atomicAdd(a.acc + o0 + st * kStageOrders + k, (unsigned long long)acc);
           }
+        } else if (a.vec) {
+          double* partp = a.part + (size_t)b * a.count + o0 + st * kStageOrders;
+          const bool rot = a.rotate != 0;
+          const int c = (int)cnt;
+          // FP32 at N=1024 takes R=32, FP64 R=16 (the row block's shared memory)
+          if (R == 32 && n == 1024) score_stage_vec_fp<T, 4, 1024>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
+          else if (R == 16 && n == 1024) score_stage_vec_fp<T, 2, 1024>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
+          else if (R == 16) score_stage_vec_fp<T, 2, 0>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
+          else if (R == 32) score_stage_vec_fp<T, 4, 0>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
+          else if (R == 64) score_stage_vec_fp<T, 8, 0>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
+          else if (R == 128) score_stage_vec_fp<T, 16, 0>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
+          else score_stage_vec_fp<T, 32, 0>(gi, kStageOrders, rot, sp, blk, n, c, warp, cw, lane, partp);
         } else {
           for (int k = warp; k < cnt; k += cw) {
             const uint16_t* src = sp + (size_t)k * R;
@@ -456,7 +522,7 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       k<<<rgrid(k), 256, route_smem, st>>>(ra, static_cast<const int32_t*>(d_perms) + off * n, predbuf);
     }
     RW_CUDA(cudaGetLastError());
-    const int vec = (R == 32 || R == 64 || R == 128 || R == 256) && n % R == 0 ? 1 : 0;
+    const int vec = (R == 32 || R == 64 || R == 128 || R == 256 || (R == 16 && !int_sums)) && n % R == 0 ? 1 : 0;
     ScoreArgs sa{cnt_o, n, R, nblocks, kStages, kStageOrders, vec, 1, part,
                  reinterpret_cast<unsigned long long*>(d_costs + off)};
     const int sgrid = (int)std::min<int64_t>(sms, (int64_t)nblocks * ((cnt_o + kStageOrders - 1) / kStageOrders));

@@ -16,6 +16,9 @@ Contents
   brute.json                : reference brute_force results (N=8 all models,
                               ring N=8..12, and N=13 with --slow)
   anneal.json (--slow)      : reference anneal at equal-budget settings
+  sample.npz                : sample_orders for several (n, samples, seed) and
+                              sample_costs on the config matrices
+  smtlib.json               : emit_smtlib texts (ring / hd / dbt / bcube)
 """
 from __future__ import annotations
 
@@ -229,6 +232,51 @@ def simulate_goldens(ref: Reference):
     print("simulate goldens:", sorted(k for k in payload if not k.endswith(("_spec", "_perms"))), flush=True)
 
 
+SAMPLE_CASES = [(1, 3, 0), (2, 5, 1), (7, 16, 0), (13, 32, 2105), (64, 16, 1234), (256, 4, 7), (1024, 3, 0),
+                (4096, 2, 14088)]
+
+
+def sample_goldens(ref: Reference):
+    """sample_orders / sample_costs (stats.cpp:83-103): seeded orders and their costs."""
+    payload = {}
+    for n, k, seed in SAMPLE_CASES:
+        payload[f"orders_{n}_{k}_{seed}"] = ref.sample_orders(n, k, seed)
+    for cfg, kind in (("C1", "fixed"), ("C1", "f32"), ("C3", "fixed"), ("C4", "fixed"), ("C4", "f64")):
+        m = fixtures.config_matrix(cfg, kind)
+        n = m.shape[0]
+        size = fixtures.size_for(kind)
+        for name, spec in specs_for(n, size)[:4]:
+            payload[f"costs_{cfg}_{kind}_{name}"] = ref.sample_costs(m, spec, 24, 99)
+            payload[f"costs_{cfg}_{kind}_{name}_spec"] = np.array(
+                [spec.algorithm, spec.n, spec.bcube_b, spec.cost_mode, spec.hd_pairing], dtype=np.int64)
+            payload[f"costs_{cfg}_{kind}_{name}_size"] = np.array([spec.size_bytes])
+    np.savez_compressed(os.path.join(HERE, "sample.npz"), **payload)
+    print("sample goldens:", len(payload), "arrays", flush=True)
+
+
+SMT_CASES = [  # (name, n, algorithm, size, mode, b, pairing, bound)
+    ("ring2", 2, 0, 8.0, 0, 2, 0, None), ("ring2_bound", 2, 0, 8.0, 0, 2, 0, 12.5),
+    ("ring5_size", 5, 0, 1e6, 1, 2, 0, 1e9), ("hd8_paper", 8, 1, 1000.0, 1, 2, 0, 3.25),
+    ("hd8_xor", 8, 1, 1000.0, 1, 2, 1, None), ("dbt8", 8, 2, 1000.0, 1, 2, 0, 77.0),
+    ("dbt4_lat", 4, 2, 1000.0, 0, 2, 0, None), ("bcube16_b4", 16, 3, 64.0, 1, 4, 0, None),
+    ("bcube8_b2", 8, 3, 1e8, 1, 2, 0, 1.0 / 3.0)]
+
+
+def smtlib_goldens(ref: Reference):
+    """emit_smtlib (smtlib.cpp:104-158) texts on small random and fixture matrices."""
+    rng = np.random.default_rng(2105)
+    out = {}
+    for name, n, alg, size, mode, b, pair, bound in SMT_CASES:
+        m = rng.uniform(0.5, 300.0, size=(n, n))
+        m[2 % n, 1 % n] = 0.0001220703125 if n > 1 else 0.0  # exercises the %.12f rounding
+        np.fill_diagonal(m, 0.0)
+        spec = make_spec(alg, n, size, b, mode, pair)
+        out[name] = {"matrix": m.tolist(), "spec": [alg, n, size, b, mode, pair], "bound": bound,
+                     "text": ref.emit_smtlib(m, spec, bound)}
+    json.dump(out, open(os.path.join(HERE, "smtlib.json"), "w"))
+    print("smtlib goldens:", list(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true")
@@ -248,6 +296,10 @@ def main():
         anneal_c4_goldens(ref)
     if "simulate" in steps or not a.only:
         simulate_goldens(ref)
+    if "sample" in steps or not a.only:
+        sample_goldens(ref)
+    if "smtlib" in steps or not a.only:
+        smtlib_goldens(ref)
 
 
 if __name__ == "__main__":

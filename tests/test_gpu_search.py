@@ -180,8 +180,7 @@ def test_anneal_quality_vs_reference_equal_budget():
     (2,823,272), against the reference's ten runs (tests/golden/anneal.json).
     Equal budget per run: the GPU median must not be worse than the
     reference median, and the GPU best of ten must not be worse than the
-    reference best of ten by more than 0.05 % (the reference best is within
-    0.01 % of the best ring 300M-evaluation runs find)."""
+    reference best of ten (<= the minimum over seeds 0-9)."""
     path = os.path.join(GOLD, "anneal.json")
     if not os.path.exists(path):
         pytest.skip("anneal goldens not generated")
@@ -202,7 +201,26 @@ def test_anneal_quality_vs_reference_equal_budget():
     gpu_med, ref_med = (costs[4] + costs[5]) / 2, (ref_costs[4] + ref_costs[5]) / 2
     print("gpu", costs, "ref", ref_costs)
     assert gpu_med <= ref_med, (gpu_med, ref_med)
-    assert costs[0] <= ref_costs[0] * 1.0005, (costs[0], ref_costs[0])
+    assert costs[0] <= ref_costs[0], (costs[0], ref_costs[0])
+
+
+def test_anneal_quality_c3_ring_equal_budget():
+    """C3 ring (N=256, fixed point; BASELINE config 3 names ring and tree):
+    one GPU chain held to the reference run's evaluation count (11,292,776:
+    the full default schedule, solver.cpp:141-202) must end at a cost <= the
+    reference's (tests/golden/anneal.json, 170 s on the host)."""
+    g = json.load(open(os.path.join(GOLD, "anneal.json")))
+    ref = [r for r in g["results"] if r["config"] == "C3" and r["model"] == "ring"][0]
+    m = fixtures.config_matrix("C3", "fixed")
+    prob = rw.Problem(m)
+    spec = fixtures.ring_spec(256, fixtures.SIZE_FIXED)
+    order, cost, ev, rep = prob.anneal(spec, rw.SolverConfig(seed=0, budget=1e6), chains=1,
+                                       max_proposals=ref["evaluations"], schedule="calibrated")
+    assert ev <= ref["evaluations"]
+    assert sorted(order.tolist()) == list(range(256))
+    assert cost == Port().evaluate(m, order.astype(np.int32), make_spec(0, 256, fixtures.SIZE_FIXED))
+    print("gpu", cost, "ref", ref["cost"], "evals", ev)
+    assert cost <= ref["cost"], (cost, ref["cost"])
 
 
 def test_anneal_quality_c4_equal_budget():
@@ -312,3 +330,34 @@ def test_sample_costs_match_sample_orders():  # test_stats.cpp:65-89 semantics
     np.fill_diagonal(u, 0)
     st = rw.sample_cost_distribution(cm(u), rw.CollectiveSpec(rw.Algorithm.Ring, 6, 10.0), 100, 7)
     assert st.min == st.max == st.mean and st.stddev == 0.0 and st.count == 100
+
+
+def test_sample_costs_are_the_references_for_the_same_seed():
+    """sample_costs (stats.cpp:96-103): the reference's mt19937_64 +
+    std::shuffle orders scored on the GPU -- bit-equal to the reference's
+    sample_costs for the same seed (tests/golden/sample.npz, from oracle/_ref)."""
+    g = np.load(os.path.join(GOLD, "sample.npz"))
+    keys = [k for k in g.files if k.startswith("costs_") and not k.endswith(("_spec", "_size"))]
+    assert len(keys) >= 16
+    for k in keys:
+        _, cfg, kind, _name = k.split("_", 3)
+        m = fixtures.config_matrix(cfg, kind)
+        a, n, b, mode, pair = (int(x) for x in g[k + "_spec"])
+        spec = rw.CollectiveSpec(rw.Algorithm(a), n, float(g[k + "_size"][0]), b, rw.CostMode(mode),
+                                 rw.HdPairing(pair))
+        got = rw.sample_costs(rw.CostMatrix.from_array(m), spec, len(g[k]), 99)
+        assert np.array_equal(got, g[k]), k
+        st = rw.sample_cost_distribution(rw.CostMatrix.from_array(m), spec, len(g[k]), 99)
+        ref = Port().distribution_stats(g[k])
+        assert (st.min, st.max, st.mean, st.stddev) == ref, k
+
+
+def test_sample_philox_extension_is_deterministic():
+    m = fixtures.config_matrix("C1", "fixed")
+    M = rw.CostMatrix.from_array(m)
+    spec = fixtures.ring_spec(64, fixtures.SIZE_FIXED)
+    a = rw.sample_costs_philox(M, spec, 256, 3)
+    assert np.array_equal(a, rw.sample_costs_philox(M, spec, 256, 3))
+    orders = rw.sample_orders_philox(64, 256, 3)
+    assert all(sorted(o) == list(range(64)) for o in orders)
+    assert np.array_equal(a, Port().evaluate_batch(m, orders, make_spec(0, 64, fixtures.SIZE_FIXED)))

@@ -1,10 +1,15 @@
 """Host-side logic of the Python mirror that needs no GPU."""
+import json
+import os
+
 import numpy as np
 import pytest
 
 import paper_2105_14088_b200 as rw
 from paper_2105_14088_b200 import api
 from oracle.pyoracle import Port
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
 def test_distribution_stats_matches_oracle():
@@ -88,3 +93,74 @@ def test_neighbor_matches_reference_bit_for_bit():
     a = subprocess.run([ref], capture_output=True, text=True, check=True).stdout
     b = subprocess.run([ours], capture_output=True, text=True, check=True).stdout
     assert a.count("\n") == 48 and a == b
+
+
+def test_sample_orders_are_the_references_for_the_same_seed():
+    """sample_orders (stats.cpp:83-94): one std::mt19937_64(seed) stream,
+    identity std::shuffle'd per sample -- host code, so this runs without a
+    GPU; bit-equal to the reference's orders (tests/golden/sample.npz)."""
+    g = np.load(os.path.join(GOLD, "sample.npz"))
+    keys = [k for k in g.files if k.startswith("orders_")]
+    assert len(keys) >= 8
+    for k in keys:
+        _, n, samples, seed = k.split("_")
+        got = api.sample_orders(int(n), int(samples), int(seed))
+        assert np.array_equal(got, g[k]), k
+    with pytest.raises(rw.DomainError, match="at least 1 sample"):
+        api.sample_orders(4, 0, 0)
+
+
+def test_emit_smtlib_is_byte_identical_to_the_reference():
+    """emit_smtlib (smtlib.cpp:104-158): the same text byte for byte on every
+    model, both cost modes, with and without a bound (tests/golden/smtlib.json,
+    from oracle/_ref).  Host code; no GPU needed."""
+    g = json.load(open(os.path.join(GOLD, "smtlib.json")))
+    assert len(g) >= 9
+    for name, case in g.items():
+        alg, n, size, b, mode, pair = case["spec"]
+        spec = rw.CollectiveSpec(rw.Algorithm(alg), n, size, b, rw.CostMode(mode), rw.HdPairing(pair))
+        m = rw.CostMatrix.from_array(np.array(case["matrix"]))
+        text = api.emit_smtlib(m, spec, case["bound"])
+        assert text == case["text"], name
+        assert api.balanced_sexpr(text)
+    with pytest.raises(rw.DomainError, match="term blow-up"):
+        u = np.ones((8, 8)) - np.eye(8)
+        api.emit_smtlib(rw.CostMatrix.from_array(u), rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, 8, 1.0), None, 4)
+
+
+def test_spearman_and_stats_match_the_reference_bits():
+    """spearman / distribution_stats run the C++ drop-in's code through the C
+    ABI (one implementation for C++, Python and FFI users); bit-equal to the
+    reference library on random and tied series."""
+    from oracle.pyoracle import reference_available, Reference
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    import ctypes as C
+    ref = Reference()
+    L = ref.lib
+    L.ref_spearman.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double)]
+    rng = np.random.default_rng(11)
+    for n in (2, 5, 50, 1000):
+        x = rng.integers(0, 7, n).astype(float)  # ties
+        y = rng.uniform(0, 1, n)
+        x[0] = 7.0  # never a constant series
+        out = C.c_double()
+        assert L.ref_spearman(x.ctypes.data_as(C.POINTER(C.c_double)), y.ctypes.data_as(C.POINTER(C.c_double)), n,
+                              C.byref(out)) == 0
+        assert api.spearman(x, y) == out.value
+        st = api.distribution_stats(y)
+        o4 = np.empty(4)
+        assert L.ref_distribution_stats(y.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                        o4.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        assert (st.min, st.max, st.mean, st.stddev) == tuple(o4)
+    with pytest.raises(rw.DomainError, match="lengths differ"):
+        api.spearman([1.0, 2.0], [1.0, 2.0, 3.0])
+    with pytest.raises(rw.DomainError, match="constant series"):
+        api.spearman([1.0, 1.0, 1.0], [1.0, 2.0, 3.0])
+
+
+def test_two_stage_solve_routing_without_gpu_work():
+    """N <= 2 routes to the identity; an invalid spec raises the reference's domain_error."""
+    with pytest.raises(rw.DomainError):
+        api.two_stage_solve(rw.CostMatrix.from_array(np.zeros((3, 3))),
+                            rw.CollectiveSpec(rw.Algorithm.HalvingDoubling, 3, 1.0), rw.SolverConfig())

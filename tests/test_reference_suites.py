@@ -15,6 +15,8 @@ import pytest
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 ON_REF = os.path.join(ROOT, "oracle", "_ref", "suite_on_reference")
 ON_B200 = os.path.join(ROOT, "oracle", "_ref", "suite_on_b200")
+SMT_REF = os.path.join(ROOT, "oracle", "_ref", "smtlib_on_reference")
+SMT_B200 = os.path.join(ROOT, "oracle", "_ref", "smtlib_on_b200")
 
 
 @pytest.mark.skipif(not os.path.exists(ON_REF), reason="reference suites not built")
@@ -29,3 +31,17 @@ def test_reference_suites_pass_on_b200_library():
     r = subprocess.run([ON_B200], capture_output=True, text=True, timeout=900, cwd="/tmp")
     print(r.stdout[-2000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+@pytest.mark.skipif(not (os.path.exists(SMT_REF) and os.path.exists(SMT_B200)), reason="smtlib suites not built")
+def test_smtlib_suite_outcome_identical_on_reference_and_b200():
+    """proj/tests/test_smtlib.cpp, unchanged, against the reference and against
+    the drop-in (host-only code: no GPU needed).  The reference fails one of
+    its own checks -- test_smtlib.cpp:92 expects 2^-13 printed unrounded, but
+    real_literal uses %.12f (smtlib.cpp:18) -- and the drop-in, which keeps the
+    reference's bytes, fails exactly the same check and passes every other."""
+    a = subprocess.run([SMT_REF], capture_output=True, text=True, timeout=300, cwd="/tmp")
+    b = subprocess.run([SMT_B200], capture_output=True, text=True, timeout=300, cwd="/tmp")
+    assert a.stdout == b.stdout and a.stderr == b.stderr and a.returncode == b.returncode
+    assert "passed: 6 | failed: 1" in a.stdout and a.stderr.count("FAILED") == 1
+    assert "test_smtlib.cpp:92" in a.stderr
