@@ -5,7 +5,7 @@ Workload (BASELINE.json target: ">= 100x the host CPU in permutation
 evaluations/sec on one B200 for N=1024 ring cost"): config C4 -- the
 1024-host synthetic hierarchical matrix (fixtures.py, fixed-point variant so
 every cost is bit-exact vs the reference), ring all-reduce cost model.  A step
-scores one batch of random orders that is resident in HBM (2 GiB of uint16
+scores one batch of random orders that is resident in HBM (32 GiB of uint16
 orders per GPU, far larger than the 126 MB L2), with the per-order bijection
 check on, exactly as the reference's evaluate() validates every order.
 
@@ -16,9 +16,13 @@ Arms
   --impl reference   the reference's own evaluate() (oracle/_ref, compiled from
                      the unmodified sources) on all host threads, rank 0 only.
 
-Extra keys: roofline (dominant kernel), cpu_baseline, e2e (host buffers through
-the C ABI rw_evaluate_batch, H2D/D2H inside the timed region), clocks,
-gpu_launches, and `extras` (N=13 exhaustive time, C1 time-to-best-ring).
+Extra keys: roofline (dominant kernel, against its binding level -- random
+shared-memory accesses -- with the HBM algorithmic-bytes view beside it),
+cpu_baseline, e2e (host buffers through the C ABI, H2D/D2H inside every step;
+packed, uint16 and int32 wire layouts), clocks (NVML, sampled during the
+timed region), gpu_launches, and `extras` (N=13 exhaustive time,
+time-to-best-ring, FP32/FP64 storage paths, the reference's searches timed in
+the same run).
 """
 from __future__ import annotations
 
@@ -40,10 +44,18 @@ METRIC = "permutation cost evals/sec (ring, N=1024, U1 = one reference evaluate(
 UNIT = "evals/s"
 WORKLOAD = "C4: N=1024 ring all-reduce cost, synthetic 3-level hierarchical matrix (fixed-point q/16 us, S=2^27)"
 N = 1024
-BATCH = 1 << 21  # orders per GPU per step: 2M x 1024 x 2 B = 4 GiB of uint16 orders in HBM
-E2E_BATCH = 1 << 16
+BATCH = 1 << 24  # orders per GPU per step: 16 Mi x 1024 x 2 B = 32 GiB of uint16 orders in HBM (~24 ms/step)
+E2E_BATCH = 1 << 18  # orders per e2e step (host buffers through the C ABI)
 C4_CHAINS = 592  # time-to-best-ring at C4: 4 chains (warps) per SM, the fastest per chain; DESIGN.md 5
 CPU_SECONDS = 10.0
+
+
+def bench_config(world: int) -> dict:
+    """The workload both arms report (identical dicts: the driver compares them)."""
+    return {"workload": WORKLOAD, "n": N, "model": "ring", "matrix": "C4 fixed point (bit-exact)",
+            "orders_per_gpu_per_step": BATCH, "order_bytes_in_hbm": BATCH * N * 2,
+            "l2_policy": "inputs larger than L2 (2 B x N x batch per step)",
+            "validation": "bijection check on every order", "parallelism": f"dp{world} (independent batches)"}
 
 
 def env_rank():
@@ -52,61 +64,67 @@ def env_rank():
 
 # ----------------------------------------------------------------- clocks --
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+    """SM clock and clock-event reasons sampled through NVML every `period`
+    seconds on a background thread while the timed region runs (nvidia-smi's
+    100 ms loop is too coarse for a sub-second region)."""
+    REASONS = (("sw_power_cap", 0x4), ("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, cuda_index: int, period: float = 0.004):
+        self.cuda_index = cuda_index
+        self.period = period
+        self.samples = []
+        self.error = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.cuda_index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            deadline = time.time() + 5.0  # start timing only once sampling is live
-            while not self.lines and time.time() < deadline and self.proc.poll() is None:
-                time.sleep(0.02)
-            self.lines.clear()
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = self._handle(nv)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # no NVML: report it instead of failing the run
+            self.error = f"NVML unavailable: {e}"
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception as e:
+                self.error = str(e)
+                return
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) != 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
-                    "error": (self.lines[0][:200] if self.lines else "nvidia-smi produced no samples")}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                    "error": self.error or "no samples"}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({name for _, r in self.samples for name, bit in self.REASONS if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "sm_mhz_min": min(sm), "period_ms": self.period * 1e3, "source": "NVML"}
 
 
 # -------------------------------------------------------------- reference --
@@ -138,12 +156,38 @@ def cpu_reference_rate(m: np.ndarray, seconds: float, threads: int):
                        "sample": f"{done} evaluations of random C4 orders (pool of {pool.shape[0]}), {dt:.1f} s"}
 
 
+def reference_matrix(name: str, kind: str = "fixed") -> np.ndarray:
+    """BASELINE config matrix built by the reference library alone (no product import)."""
+    from oracle.pyoracle import Reference, reference_available, reference_config_matrix
+    if not reference_available():
+        raise RuntimeError("oracle/_ref is missing")
+    return reference_config_matrix(Reference(), name, kind)
+
+
+def reference_search_same_run():
+    """The reference's searches timed on this box in this run (single thread,
+    as shipped): ring brute force at N=12 on the C2 block (11! orders) and
+    the C1 anneal at seed 0 (default schedule, 2,823,272 evaluations)."""
+    from oracle.pyoracle import Reference, make_spec
+    ref = Reference()
+    out = {}
+    m13 = reference_matrix("C2")
+    t = time.perf_counter()
+    perm, cost, ev = ref.brute_force(np.ascontiguousarray(m13[:12, :12]), make_spec(0, 12, 1.0), threshold=12)
+    out["brute_force_n12"] = {"seconds": time.perf_counter() - t, "cost": cost, "evaluations": ev,
+                              "order": perm.tolist(), "threads": 1}
+    m1 = reference_matrix("C1", "fixed")
+    t = time.perf_counter()
+    perm, cost, ev = ref.anneal(m1, make_spec(0, 64, float(2 ** 27)), budget_s=1e6, seed=0)
+    out["anneal_c1_seed0"] = {"seconds": time.perf_counter() - t, "cost": cost, "evaluations": ev, "threads": 1}
+    return out
+
+
 def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    import paper_2105_14088_b200 as rw  # fixture generator only (host code)
-    m = rw.fixtures.config_matrix("C4", "fixed")
+    m = reference_matrix("C4", "fixed")
     threads = os.cpu_count() or 1
     per_step = max(1.0, 20.0 / max(1, args.steps))
     for _ in range(args.warmup):
@@ -159,7 +203,7 @@ def run_reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": N, "model": "ring", "threads": threads},
+            "config": bench_config(world),
             "cpu_baseline": dict(info, value=value, unit=UNIT),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -209,19 +253,28 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     m = rw.fixtures.config_matrix("C4", "fixed")
     prob = rw.Problem(m, device=local)
     spec = rw.fixtures.ring_spec(N, rw.fixtures.SIZE_FIXED)
     batch = args.batch
     orders = make_orders_device(torch, batch, N, seed=1234 + rank)
     costs = torch.empty(batch, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream()
+    # One side stream for warm-up, capture and replay: the library's
+    # stream-ordered scratch for this stream is then sized before capture.
+    stream = torch.cuda.Stream()
 
-    def step(p=prob):
-        p.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), stream.cuda_stream)
+    def step(p=prob, st=None):
+        p.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), (st or stream).cuda_stream)
 
-    for _ in range(max(3, args.warmup)):
-        step()
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            step()
     torch.cuda.synchronize()
     prob.sync_errors()
 
@@ -235,9 +288,8 @@ def run_ours(args):
     # One step (the route/score kernel pairs of every chunk) captured as a CUDA
     # graph; the timed loop replays it.
     graph = torch.cuda.CUDAGraph(keep_graph=True)
-    with torch.cuda.graph(graph):
-        cap = torch.cuda.current_stream()
-        prob.evaluate_batch_device(spec, orders.data_ptr(), 2, batch, costs.data_ptr(), cap.cuda_stream)
+    with torch.cuda.graph(graph, stream=stream):
+        step()
     graph.replay()
     torch.cuda.synchronize()
     prob.sync_errors()
@@ -247,61 +299,37 @@ def run_ours(args):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
     with ClockSampler(local) as clocks:
-        ev[0].record(stream)
-        for k in range(args.steps):
-            graph.replay()
-            ev[k + 1].record(stream)
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for k in range(args.steps):
+                graph.replay()
+                ev[k + 1].record(stream)
         barrier()
     prob.sync_errors()
     per_launch_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = max_over_ranks(total_ms)
     value = world * batch * args.steps / (max_ms / 1000.0)
 
-    def time_path(path, reps=10):
+    def time_path(path, reps=10, count=1 << 21):
         alt = rw.Problem(m, device=local)
         alt.set_path(path)
-        step(alt)
+        cst = torch.cuda.current_stream()
+
+        def run():
+            alt.evaluate_batch_device(spec, orders.data_ptr(), 2, count, costs.data_ptr(), cst.cuda_stream)
+        run()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        e0.record(cst)
         for _ in range(reps):
-            step(alt)
-        e1.record(stream)
+            run()
+        e1.record(cst)
         torch.cuda.synchronize()
         alt.sync_errors()
-        return batch * reps / (e0.elapsed_time(e1) / 1000.0)
+        return count * reps / (e0.elapsed_time(e1) / 1000.0)
 
-    # ---- e2e: host int32 orders through rw_evaluate_batch (H2D + D2H inside) ----
-    e2e_batch = args.e2e_batch
-    host_orders = torch.empty((e2e_batch, N), dtype=torch.int32, pin_memory=True)
-    host_orders.copy_(orders[:e2e_batch].to(torch.int32).cpu())
-    host_np = host_orders.numpy()
-    host_costs_t = torch.empty(e2e_batch, dtype=torch.float64, pin_memory=True)
-    host_costs = host_costs_t.numpy()
-    import ctypes as C
-    from paper_2105_14088_b200 import _lib
-    cs = spec._c()
-
-    def e2e_step():
-        _lib.check(_lib.lib.rw_evaluate_batch(prob.handle, C.byref(cs), _lib.ptr(host_np, C.c_int32), e2e_batch,
-                                              _lib.ptr(host_costs, C.c_double), 0, None))
-
-    for _ in range(2):
-        e2e_step()
-    e2e_steps = max(3, min(args.steps, 20))
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    barrier()
-    e2e_dt = time.perf_counter() - t0
-    te = torch.tensor([e2e_dt], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * e2e_batch * e2e_steps / float(te.item())
+    # ---- e2e: host orders through the C ABI (H2D + D2H inside every step) ----
+    e2e = run_e2e(rw, torch, args, prob, spec, orders, barrier, max_over_ranks, world, local)
 
     multi = {}
     if not args.no_extras:
@@ -315,28 +343,24 @@ def run_ours(args):
 
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     bytes_per_eval = 2 * N + N * 2 + 8  # order read + L*e lookups (u16) + cost write
     launch_ms = statistics.mean(per_launch_ms)
-    achieved = bytes_per_eval * batch / (launch_ms / 1000.0) / 1e9
+    hbm_achieved = bytes_per_eval * batch / (launch_ms / 1000.0) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         bpo = json.load(open(tpath)).get("bytes_per_order")
-        traffic = bpo * batch if bpo else None  # per bench step (one graph replay)
+        traffic = bpo * batch if bpo else None  # DRAM bytes per bench step (one graph replay), from ncu
     clock = clocks.summary()
-    # The lookups run against shared memory: one random 2-byte scatter (route) and
-    # one random 2-byte gather (score) per hop, against the measured random-gather
-    # peak (profiles/gather_peaks.json, scripts/microbench/gather_peaks.cu).
-    smem_access = None
-    gpath_peaks = os.path.join(ROOT, "profiles", "gather_peaks.json")
-    if os.path.exists(gpath_peaks):
-        gp = json.load(open(gpath_peaks))
-        acc_per_s = 2 * N * batch / (launch_ms / 1000.0)
-        smem_access = {"accesses_per_s": acc_per_s, "peak_per_s": gp["smem_random_u16_lookups_per_s"],
-                       "frac": acc_per_s / gp["smem_random_u16_lookups_per_s"],
-                       "note": "route scatter + score gather, 2 random u16 shared-memory accesses per hop"}
+    # The binding level: shared-memory random accesses -- one random 2-byte
+    # scatter (route) and one random 2-byte gather (score) per hop -- against
+    # the measured random-access peak (profiles/gather_peaks.json,
+    # scripts/microbench/gather_peaks.cu).  ncu: both passes at 90-91% L1TEX.
+    gp = json.load(open(os.path.join(ROOT, "profiles", "gather_peaks.json")))
+    smem_peak = gp["smem_random_u16_lookups_per_s"]
+    acc_per_s = 2 * N * batch / (launch_ms / 1000.0)
 
     cpu_value, cpu_info = (None, {"kind": "skipped", "cores": 0, "sample": "--no-cpu"})
     if not args.no_cpu:
@@ -345,10 +369,13 @@ def run_ours(args):
     extras = {}
     if not args.no_extras:
         extras = run_extras(rw, torch)
-        # A/B: the same batch through the alternative ring kernels (not the default path)
+        extras["storage_kinds"] = run_storage_extras(rw, torch, hbm_peak)
+        if not args.no_cpu:
+            extras["reference_search_same_run"] = reference_search_same_run()
+        # A/B: the same orders through the alternative ring kernels (not the default path)
         extras["ring_kernel_ab"] = {
-            "unit": UNIT,
-            "transpose_default": value / world,
+            "unit": UNIT, "orders": 1 << 21,
+            "transpose_default": time_path("auto"),
             "l2_gather": time_path("l2"),
             "cluster_dsmem": time_path("cluster"),
             "note": "l2_gather: one warp per order, random sector gathers (L1TEX-wavefront bound); "
@@ -359,21 +386,24 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": max_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": N, "model": "ring", "orders_per_gpu_per_step": batch,
-                   "order_bytes_in_hbm": batch * N * 2, "l2_policy": "inputs larger than L2 (2 B x N x batch)",
-                   "validation": "bijection check on every order", "parallelism": f"dp{world} (independent batches)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src,
-                     "smem_random_access": smem_access,
-                     "kernel": "k_ring_route + k_ring_score (transpose ring path, one pair per chunk)",
-                     "algorithmic_bytes_per_eval": bytes_per_eval,
-                     "lookups_per_s": N * batch / (launch_ms / 1000.0),
-                     "note": "achieved = SURVEY 8(d) algorithmic bytes (2N order + N x 2 B lookups + 8) x evals/s "
-                             "over the step's CUDA-event time; the path streams the orders from HBM once and "
-                             "keeps its predecessor exchange buffer in L2 -- DESIGN.md 4"},
+        "config": bench_config(world),
+        "roofline": {"bound": "smem", "achieved": acc_per_s / 1e9, "peak": smem_peak / 1e9,
+                     "unit": "G random shared-memory accesses/s", "frac": acc_per_s / smem_peak,
+                     "traffic": traffic, "peak_source": "measured (profiles/gather_peaks.json: random 2-byte "
+                                                        "shared-memory accesses, all SMs)",
+                     "kernel": "k_ring_route + k_ring_score (transpose ring path, one pair per 262,144-order chunk)",
+                     "accesses_per_eval": 2 * N,
+                     "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": hbm_achieved / hbm_peak, "peak_source": peak_src,
+                             "algorithmic_bytes_per_eval": bytes_per_eval,
+                             "note": "SURVEY 8(d) algorithmic bytes (2N order + N x 2 B lookups + 8 B cost) per "
+                                     "evaluation over the step's CUDA-event time"},
+                     "note": "the lookups are served from shared memory (route scatter + score gather: 2 random "
+                             "accesses per hop); both passes run at 90-91% of L1TEX throughput (ncu, profiles/). "
+                             "The predecessor exchange buffer (2N B per order) is written and re-read through "
+                             "HBM; `traffic` is the ncu DRAM bytes per step -- DESIGN.md 4, 7"},
         "cpu_baseline": dict(cpu_info, value=cpu_value, unit=UNIT),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_batch * N * 4,
-                "d2h_bytes_per_step": e2e_batch * 8, "api": "rw_evaluate_batch (C ABI, pinned host int32 orders)"},
+        "e2e": e2e,
         "clocks": clock,
         "gpu_launches": args.steps * launches_per_step,
         "extras": extras,
@@ -384,6 +414,119 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def run_e2e(rw, torch, args, prob, spec, orders, barrier, max_over_ranks, world, local):
+    """The metric through the public C ABI with HOST buffers: every step copies
+    that step's orders host -> device (pinned memory) and reads the costs back.
+    Three wire layouts of the same orders: packed (10 bits per host at N=1024,
+    rw_evaluate_batch_packed -- the headline), uint16 (rw_evaluate_batch_u16)
+    and int32 (rw_evaluate_batch, the reference's RankOrder element type)."""
+    import ctypes as C
+    from paper_2105_14088_b200 import _lib
+    eb = args.e2e_batch
+    host16 = orders[:eb].cpu().numpy().view(np.uint16)
+    bits = rw.api.packed_bits(N)
+    variants = {
+        "packed": (torch.from_numpy(rw.api.pack_orders(host16.astype(np.int32), bits)).pin_memory(),
+                   rw.api.packed_row_bytes(N, bits)),
+        "u16": (torch.from_numpy(host16.copy().view(np.int16)).pin_memory(), 2 * N),
+        "int32": (torch.from_numpy(host16.astype(np.int32)).pin_memory(), 4 * N),
+    }
+    costs_t = torch.empty(eb, dtype=torch.float64).pin_memory()
+    cptr = C.cast(costs_t.data_ptr(), C.POINTER(C.c_double))
+    cs = spec._c()
+
+    def call(kind, buf):
+        if kind == "packed":
+            return _lib.lib.rw_evaluate_batch_packed(prob.handle, C.byref(cs), C.c_void_p(buf.data_ptr()), bits, eb,
+                                                     cptr, 0, None)
+        if kind == "u16":
+            return _lib.lib.rw_evaluate_batch_u16(prob.handle, C.byref(cs), C.cast(buf.data_ptr(),
+                                                  C.POINTER(C.c_uint16)), eb, cptr, 0, None)
+        return _lib.lib.rw_evaluate_batch(prob.handle, C.byref(cs), C.cast(buf.data_ptr(), C.POINTER(C.c_int32)),
+                                          eb, cptr, 0, None)
+
+    steps = max(3, min(args.steps, 20))
+    out = {}
+    ref_costs = None
+    for kind, (buf, row) in variants.items():
+        for _ in range(2):
+            _lib.check(call(kind, buf))
+        got = costs_t.numpy().copy()
+        if ref_costs is None:
+            ref_costs = got
+        assert np.array_equal(got, ref_costs), f"e2e {kind}: costs differ between wire layouts"
+        barrier()
+        with ClockSampler(local, period=0.01) as clk:
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                _lib.check(call(kind, buf))
+            dt = time.perf_counter() - t0
+        barrier()
+        dt = max_over_ranks(dt)
+        out[kind] = {"value": world * eb * steps / dt, "unit": UNIT, "steps": steps, "orders_per_step": eb,
+                     "h2d_bytes_per_step": eb * row, "d2h_bytes_per_step": eb * 8,
+                     "h2d_GBps": eb * row * steps / dt / 1e9, "clocks": clk.summary()}
+    head = out["packed"]
+    return {"value": head["value"], "unit": UNIT, "h2d_bytes_per_step": head["h2d_bytes_per_step"],
+            "d2h_bytes_per_step": head["d2h_bytes_per_step"],
+            "api": f"rw_evaluate_batch_packed (C ABI; pinned host orders, {bits} bits per host, "
+                   f"{rw.api.packed_row_bytes(N, bits)} B per order; H2D + device unpack + score + D2H of the costs "
+                   f"inside every step, wall clock, max over ranks)",
+            "variants": out}
+
+
+def run_storage_extras(rw, torch, hbm_peak):
+    """A probed CostMatrix is FP64 (types.hpp:42-53): throughput of the FP32
+    and FP64 storage paths a real matrix takes, next to the fixed-point one,
+    with a parity assert on every case (north star: FP32 within 1e-6)."""
+    from oracle.pyoracle import Port, make_spec
+    port = Port()
+    A, P = rw.Algorithm, rw.HdPairing
+    cases = [("C4", "ring", 0, 0, 1 << 21), ("C5", "hd_xor", 1, 1, 1 << 15), ("C5", "hd_paper", 1, 0, 1 << 15)]
+    names = {1: "u16", 2: "f32", 3: "f64"}
+    out = {"unit": "evals/s", "orders": "uint16, device resident"}
+    for cfg, model, alg, pair, count in cases:
+        for kind in ("fixed", "f32", "f64"):
+            m = rw.fixtures.config_matrix(cfg, kind)
+            n = m.shape[0]
+            size = rw.fixtures.size_for(kind)
+            spec = rw.CollectiveSpec(A(alg), n, size, 2, rw.CostMode.LatencyTimesSize, P(pair))
+            prob = rw.Problem(m)
+            g = torch.Generator(device="cuda")
+            g.manual_seed(5)
+            o = torch.rand((count, n), device="cuda", generator=g).argsort(dim=1).to(torch.int16)
+            c = torch.empty(count, dtype=torch.float64, device="cuda")
+            st = torch.cuda.current_stream()
+            for _ in range(2):
+                prob.evaluate_batch_device(spec, o.data_ptr(), 2, count, c.data_ptr(), st.cuda_stream)
+            torch.cuda.synchronize()
+            prob.sync_errors()
+            rows = o[:8].cpu().numpy().view(np.uint16).astype(np.int32)
+            want = port.evaluate_batch(m, rows, make_spec(alg, n, size, 2, 1, pair))
+            rel = float(np.max(np.abs(c[:8].cpu().numpy() - want) / np.abs(want)))
+            assert rel <= (0.0 if kind == "fixed" else 1e-6), (cfg, model, kind, rel)
+            reps = 5
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                prob.evaluate_batch_device(spec, o.data_ptr(), 2, count, c.data_ptr(), st.cuda_stream)
+            e1.record(st)
+            torch.cuda.synchronize()
+            prob.sync_errors()
+            rate = count * reps / (e0.elapsed_time(e1) / 1000.0)
+            e = prob.info["storage"]
+            esz = {1: 2, 2: 4, 3: 8}[e]
+            lookups = port.lookups(make_spec(alg, n, size, 2, 1, pair))
+            alg_bytes = 2 * n + lookups * esz + 8
+            out[f"{cfg}_{model}_{kind}"] = {
+                "storage": names[e], "evals_per_s": rate, "max_rel_err_vs_oracle": rel,
+                "roofline_hbm": {"algorithmic_bytes_per_eval": alg_bytes, "achieved_GBps": rate * alg_bytes / 1e9,
+                                 "frac": rate * alg_bytes / 1e9 / hbm_peak}}
+            del prob, o, c
+            torch.cuda.empty_cache()
+    return out
 
 
 def run_multi_extras(rw, torch, dist, rank, world, local, prob4, spec4, barrier):

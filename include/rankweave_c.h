@@ -175,6 +175,19 @@ rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* p
 /* B orders (row-major B x n int32, host) -> B costs (host). */
 rw_status rw_evaluate_batch(const rw_problem* p, const rw_spec* spec, const int32_t* perms, int64_t batch,
                             double* costs, uint32_t flags, rw_eval_report* report);
+/* Host orders as uint16 (n <= 65536): half the host-to-device bytes of int32. */
+rw_status rw_evaluate_batch_u16(const rw_problem* p, const rw_spec* spec, const uint16_t* perms, int64_t batch,
+                                double* costs, uint32_t flags, rw_eval_report* report);
+/* Packed host orders: `bits` per element (1..16, 2^bits >= n); element i of
+ * an order occupies bits [i*bits, (i+1)*bits) of the order's little-endian
+ * 32-bit word stream, and every order starts on a 16-byte boundary:
+ * rw_packed_row_bytes(n, bits) bytes per order (-1 for invalid arguments).
+ * At n = 1024 and 10 bits an order is 1280 bytes, 5/16 of int32.  The
+ * orders are unpacked on the device; costs and errors as rw_evaluate_batch. */
+int64_t rw_packed_row_bytes(int32_t n, int32_t bits);
+rw_status rw_pack_orders(const int32_t* perms, int32_t n, int64_t batch, int32_t bits, void* out);
+rw_status rw_evaluate_batch_packed(const rw_problem* p, const rw_spec* spec, const void* packed, int32_t bits,
+                                   int64_t batch, double* costs, uint32_t flags, rw_eval_report* report);
 /* Same with device buffers; perm_bytes is 2 (uint16) or 4 (int32). Async on
  * `stream`.  Validation failures are reported by the next rw_sync_errors(). */
 rw_status rw_evaluate_batch_device(const rw_problem* p, const rw_spec* spec, const void* d_perms,

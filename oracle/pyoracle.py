@@ -199,5 +199,39 @@ class Reference:
         return buf.value.decode()
 
 
+# The BASELINE config recipe, built from the reference alone --
+# generate_matrix (topology.cpp:40-64) + the relabeling shuffle, which is
+# sample_orders(n, 1, 14088) (stats.cpp:83-94: std::shuffle of the identity
+# with mt19937_64(seed)) -- so the bench's reference arm never loads the
+# product library.  Equal to paper_2105_14088_b200.fixtures.config_matrix
+# (tests/test_oracle.py checks it).
+CONFIG_LEVELS = {
+    "C1": ([(8, 5, 1000, 1), (8, 25, 1000, 4)], True, None),
+    "C2": ([(4, 5, 1000, 1), (4, 25, 1000, 4)], False, 13),
+    "C3": ([(8, 5, 1000, 1), (16, 25, 1000, 4), (2, 100, 1000, 4)], True, None),
+    "C4": ([(8, 5, 1000, 1), (16, 25, 1000, 4), (8, 100, 1000, 4)], True, None),
+    "C5": ([(8, 5, 1000, 1), (16, 25, 1000, 4), (32, 100, 1000, 4)], True, None),
+}
+
+
+def reference_config_matrix(ref: "Reference", name: str, kind: str = "fixed") -> np.ndarray:
+    levels, relabel, trunc = CONFIG_LEVELS[name]
+    m = ref.generate_matrix(levels, jitter=0.1, seed=2105)
+    if trunc is not None:
+        m = np.ascontiguousarray(m[:trunc, :trunc])
+    if relabel:
+        rl = ref.sample_orders(m.shape[0], 1, 14088)[0]
+        m = np.ascontiguousarray(m[np.ix_(rl, rl)])
+    if name == "C2":
+        kind = "int"
+    if kind == "f32":
+        return m.astype(np.float32).astype(np.float64)
+    if kind == "fixed":
+        return np.clip(np.floor(m * 16.0 + 0.5), 0, 65535) / 16.0
+    if kind == "int":
+        return np.floor(m + 0.5)
+    return m
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_PATH)

@@ -75,6 +75,12 @@ SIGNATURES = {
     "rw_problem_set_path": (C.c_int, [_vp, C.c_int32]),
     "rw_evaluate": (C.c_int, [_vp, P(rw_spec), _i32p, _dp]),
     "rw_evaluate_batch": (C.c_int, [_vp, P(rw_spec), _i32p, C.c_int64, _dp, C.c_uint32, P(rw_eval_report)]),
+    "rw_evaluate_batch_u16": (C.c_int, [_vp, P(rw_spec), P(C.c_uint16), C.c_int64, _dp, C.c_uint32,
+                                        P(rw_eval_report)]),
+    "rw_packed_row_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
+    "rw_pack_orders": (C.c_int, [_i32p, C.c_int32, C.c_int64, C.c_int32, _vp]),
+    "rw_evaluate_batch_packed": (C.c_int, [_vp, P(rw_spec), _vp, C.c_int32, C.c_int64, _dp, C.c_uint32,
+                                           P(rw_eval_report)]),
     "rw_evaluate_batch_device": (C.c_int, [_vp, P(rw_spec), _vp, C.c_int32, C.c_int64, _vp, _vp, C.c_uint32]),
     "rw_sync_errors": (C.c_int, [_vp, _vp]),
     "rw_schedule_cost": (C.c_int, [_vp, C.c_int32, C.c_int32, _i32p, _i32p, _i32p, _dp, _i32p, C.c_int32,

@@ -114,7 +114,11 @@ class Problem:
     # batch scoring ---------------------------------------------------------
     def evaluate_batch(self, spec: "CollectiveSpec", orders: np.ndarray, exact: bool = False,
                        validate: bool = True, report: Optional[dict] = None) -> np.ndarray:
-        o = np.ascontiguousarray(orders, dtype=np.int32)
+        """(B, n) host orders -> B costs.  uint16 arrays go through
+        rw_evaluate_batch_u16 (half the host-to-device bytes); anything else
+        as int32 through rw_evaluate_batch."""
+        u16 = isinstance(orders, np.ndarray) and orders.dtype == np.uint16
+        o = np.ascontiguousarray(orders, dtype=np.uint16 if u16 else np.int32)
         if o.ndim == 1:
             o = o[None, :]
         if o.shape[1] != spec.n:
@@ -122,10 +126,27 @@ class Problem:
         out = np.empty(o.shape[0], dtype=np.float64)
         flags = (_lib.RW_EVAL_EXACT if exact else 0) | (0 if validate else _lib.RW_EVAL_NO_VALIDATE)
         rep = _lib.rw_eval_report()
-        check(lib.rw_evaluate_batch(self._h, C.byref(spec._c()), ptr(o, C.c_int32), o.shape[0],
-                                    ptr(out, C.c_double), flags, C.byref(rep)))
+        if u16:
+            check(lib.rw_evaluate_batch_u16(self._h, C.byref(spec._c()), ptr(o, C.c_uint16), o.shape[0],
+                                            ptr(out, C.c_double), flags, C.byref(rep)))
+        else:
+            check(lib.rw_evaluate_batch(self._h, C.byref(spec._c()), ptr(o, C.c_int32), o.shape[0],
+                                        ptr(out, C.c_double), flags, C.byref(rep)))
         if report is not None:
             report.update({f: getattr(rep, f) for f, _ in rep._fields_})
+        return out
+
+    def evaluate_batch_packed(self, spec: "CollectiveSpec", packed: np.ndarray, bits: int, batch: int,
+                              exact: bool = False, validate: bool = True) -> np.ndarray:
+        """Packed host orders (pack_orders) -> costs through rw_evaluate_batch_packed."""
+        row = packed_row_bytes(spec.n, bits)
+        p = np.ascontiguousarray(packed)
+        if p.nbytes < row * batch:
+            raise DomainError(f"packed buffer holds {p.nbytes} bytes, need {row * batch}")
+        out = np.empty(batch, dtype=np.float64)
+        flags = (_lib.RW_EVAL_EXACT if exact else 0) | (0 if validate else _lib.RW_EVAL_NO_VALIDATE)
+        check(lib.rw_evaluate_batch_packed(self._h, C.byref(spec._c()), C.c_void_p(p.ctypes.data), bits, batch,
+                                           ptr(out, C.c_double), flags, None))
         return out
 
     def evaluate_batch_device(self, spec: "CollectiveSpec", d_orders: int, perm_bytes: int, batch: int,
@@ -583,6 +604,29 @@ def spearman(xs, ys) -> float:
     out = C.c_double()
     check(lib.rw_spearman(ptr(x, C.c_double), ptr(y, C.c_double), x.size, y.size, C.byref(out)))
     return out.value
+
+
+def packed_row_bytes(n: int, bits: int) -> int:
+    r = int(lib.rw_packed_row_bytes(n, bits))
+    if r < 0:
+        raise DomainError("packed orders need n >= 1 and 1 <= bits <= 16")
+    return r
+
+
+def packed_bits(n: int) -> int:
+    """Smallest width that holds every host index of an n-host order."""
+    return max(1, (max(n, 2) - 1).bit_length())
+
+
+def pack_orders(orders: np.ndarray, bits: Optional[int] = None) -> np.ndarray:
+    """(B, n) orders -> the packed wire layout of rw_evaluate_batch_packed, as bytes."""
+    o = np.ascontiguousarray(orders, dtype=np.int32)
+    if o.ndim == 1:
+        o = o[None, :]
+    b = packed_bits(o.shape[1]) if bits is None else int(bits)
+    out = np.empty(packed_row_bytes(o.shape[1], b) * o.shape[0], dtype=np.uint8)
+    check(lib.rw_pack_orders(ptr(o, C.c_int32), o.shape[1], o.shape[0], b, C.c_void_p(out.ctypes.data)))
+    return out
 
 
 def device_count() -> int:

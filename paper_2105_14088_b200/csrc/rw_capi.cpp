@@ -174,6 +174,72 @@ rw_status rw_evaluate_batch(const rw_problem* p, const rw_spec* spec, const int3
   });
 }
 
+rw_status rw_evaluate_batch_u16(const rw_problem* p, const rw_spec* spec, const uint16_t* perms, int64_t batch,
+                                double* costs, uint32_t flags, rw_eval_report* report) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(perms, "perms");
+      need(costs, "costs");
+    }
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    rwb::evaluate_host_orders_fmt(q, plan, perms, 2, 0, batch, costs, (flags & RW_EVAL_EXACT) != 0,
+                                  (flags & RW_EVAL_NO_VALIDATE) == 0, report);
+  });
+}
+
+int64_t rw_packed_row_bytes(int32_t n, int32_t bits) {
+  if (n < 1 || bits < 1 || bits > 16) return -1;
+  return rwb::packed_row_bytes(n, bits);
+}
+
+rw_status rw_pack_orders(const int32_t* perms, int32_t n, int64_t batch, int32_t bits, void* out) {
+  return guarded([&] {
+    if (n < 1) rwb::fail_domain("n must be >= 1");
+    if (bits < 1 || bits > 16 || (n > 1 && (1ll << bits) < n))
+      rwb::fail_domain("packed orders need 1 <= bits <= 16 and 2^bits >= n");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch == 0) return;
+    need(perms, "perms");
+    need(out, "out");
+    const int64_t row = rwb::packed_row_bytes(n, bits);
+    auto* w = static_cast<uint32_t*>(out);
+    std::memset(out, 0, static_cast<size_t>(row * batch));
+    for (int64_t b = 0; b < batch; ++b) {
+      uint32_t* r = w + b * (row / 4);
+      const int32_t* o = perms + b * n;
+      for (int i = 0; i < n; ++i) {
+        const uint32_t v = static_cast<uint32_t>(o[i]) & ((1u << bits) - 1u);
+        if (static_cast<uint32_t>(o[i]) != v) rwb::fail_domain("rank order value does not fit the packed width");
+        const uint64_t bit = static_cast<uint64_t>(i) * static_cast<uint64_t>(bits);
+        const uint32_t q = static_cast<uint32_t>(bit >> 5), sh = static_cast<uint32_t>(bit & 31);
+        r[q] |= v << sh;
+        if (sh + static_cast<uint32_t>(bits) > 32u) r[q + 1] |= v >> (32u - sh);
+      }
+    }
+  });
+}
+
+rw_status rw_evaluate_batch_packed(const rw_problem* p, const rw_spec* spec, const void* packed, int32_t bits,
+                                   int64_t batch, double* costs, uint32_t flags, rw_eval_report* report) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(packed, "packed");
+      need(costs, "costs");
+    }
+    rwb::Problem& q = get(p);
+    const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
+    if (bits < 1 || bits > 16 || (spec->n > 1 && (1ll << bits) < spec->n))
+      rwb::fail_domain("packed orders need 1 <= bits <= 16 and 2^bits >= n");
+    rwb::evaluate_host_orders_fmt(q, plan, packed, 0, bits, batch, costs, (flags & RW_EVAL_EXACT) != 0,
+                                  (flags & RW_EVAL_NO_VALIDATE) == 0, report);
+  });
+}
+
 rw_status rw_evaluate_batch_device(const rw_problem* p, const rw_spec* spec, const void* d_perms, int32_t perm_bytes,
                                    int64_t batch, double* d_costs, void* stream, uint32_t flags) {
   return guarded([&] {
@@ -186,6 +252,7 @@ rw_status rw_evaluate_batch_device(const rw_problem* p, const rw_spec* spec, con
     rwb::Problem& q = get(p);
     const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
     rwb::DeviceGuard g(q.device);
+    rwb::StreamScratch scope(q.device, static_cast<cudaStream_t>(stream));
     rwb::launch_evaluate(q, plan, d_perms, perm_bytes, batch, d_costs, (flags & RW_EVAL_EXACT) != 0,
                          (flags & RW_EVAL_NO_VALIDATE) == 0, q.d_err, static_cast<cudaStream_t>(stream));
   });

@@ -995,42 +995,92 @@ void launch_evaluate(const Problem& p, const EvalPlan& plan, const void* d_perms
   }
 }
 
-void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms, int64_t batch, double* costs,
-                          bool exact, bool validate, rw_eval_report* report) {
+namespace {
+
+// Packed host orders (rw_evaluate_batch_packed): element i of an order sits at
+// bits [i*bits, (i+1)*bits) of the order's little-endian 32-bit word stream.
+// One warp per order; the words are L1-resident across the warp's lanes.
+__global__ void __launch_bounds__(256) k_unpack_orders(const uint32_t* __restrict__ in, int64_t count, int n, int bits,
+                                                       int row_words, uint16_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t mask = (1u << bits) - 1u;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < count; o += nwarps) {
+    const uint32_t* w = in + o * row_words;
+    uint16_t* dst = out + o * n;
+    for (int i = lane; i < n; i += 32) {
+      const uint32_t bit = (uint32_t)i * (uint32_t)bits;
+      const uint32_t q = bit >> 5, sh = bit & 31u;
+      uint32_t v = __ldg(w + q) >> sh;
+      if (sh + (uint32_t)bits > 32u) v |= __ldg(w + q + 1) << (32u - sh);
+      dst[i] = (uint16_t)(v & mask);
+    }
+  }
+}
+
+}  // namespace
+
+int64_t packed_row_bytes(int n, int bits) { return 16 * (((int64_t)n * bits + 127) / 128); }
+
+// Host orders -> costs through a chunked, double-buffered pipeline: the H2D
+// copy of chunk k+1 overlaps the scoring of chunk k on the other stream, and
+// costs come back per chunk.  fmt: 4 = int32, 2 = uint16, 0 = packed (`bits`
+// per element; unpacked on the device into uint16 before scoring).
+void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perms, int fmt, int bits, int64_t batch,
+                              double* costs, bool exact, bool validate, rw_eval_report* report) {
   if (batch <= 0) return;
   DeviceGuard g(p.device);
   ThreadCtx& c = thread_ctx(p.device);
   const int n = plan.n;
-  if (batch * (int64_t)n <= (1 << 16)) {
-    // small batches (single evaluate() calls): one stream, one synchronisation
-    cudaStream_t st = c.stream[0];
-    const size_t pb = align16((size_t)batch * n * 4);
-    char* base = static_cast<char*>(c.scratch(0, pb + (size_t)batch * 8 + 64));
-    auto* d_perm = reinterpret_cast<int32_t*>(base);
-    auto* d_cost = reinterpret_cast<double*>(base + pb);
-    RW_CUDA(cudaMemcpyAsync(d_perm, perms, (size_t)batch * n * 4, cudaMemcpyHostToDevice, st));
-    launch_evaluate(p, plan, d_perm, 4, batch, d_cost, exact, validate, c.d_err, st, 2);
-    RW_CUDA(cudaMemcpyAsync(costs, d_cost, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
-    if (validate) raise_order_errors(c.d_err, c.h_err, st);  // synchronises st
-    else RW_CUDA(cudaStreamSynchronize(st));
+  const int64_t row = fmt == 0 ? packed_row_bytes(n, bits) : (int64_t)n * fmt;
+  const int eval_bytes = fmt == 4 ? 4 : 2;
+  const auto* hp = static_cast<const char*>(perms);
+  auto stage = [&](cudaStream_t st, const char* host, int64_t cnt, void* d_in, uint16_t* d_u16) -> const void* {
+    RW_CUDA(cudaMemcpyAsync(d_in, host, (size_t)(cnt * row), cudaMemcpyHostToDevice, st));
+    if (fmt != 0) return d_in;
+    const int64_t blocks = std::min<int64_t>((cnt + 7) / 8, 148 * 16);
+    k_unpack_orders<<<(int)std::max<int64_t>(1, blocks), 256, 0, st>>>(static_cast<const uint32_t*>(d_in), cnt, n,
+                                                                      bits, (int)(row / 4), d_u16);
+    RW_CUDA(cudaGetLastError());
+    return d_u16;
+  };
+  auto finish = [&] {
     if (report) {
       report->bit_exact = (plan.bit_exact || exact) ? 1 : 0;
       report->kernel = plan.model;
       report->lookups = lookups_per_eval(plan) * batch;
     }
+  };
+  const size_t u16_bytes = fmt == 0 ? align16((size_t)n * 2) : 0;  // per order, packed only
+  if (batch * (int64_t)n <= (1 << 16)) {
+    // small batches (single evaluate() calls): one stream, one synchronisation
+    cudaStream_t st = c.stream[0];
+    const size_t pb = align16((size_t)(batch * row));
+    const size_t ub = align16(u16_bytes * batch);
+    char* base = static_cast<char*>(c.scratch(0, pb + ub + (size_t)batch * 8 + 64));
+    auto* d_cost = reinterpret_cast<double*>(base + pb + ub);
+    const void* d_eval = stage(st, hp, batch, base, reinterpret_cast<uint16_t*>(base + pb));
+    launch_evaluate(p, plan, d_eval, eval_bytes, batch, d_cost, exact, validate, c.d_err, st, 2);
+    RW_CUDA(cudaMemcpyAsync(costs, d_cost, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+    if (validate) raise_order_errors(c.d_err, c.h_err, st);  // synchronises st
+    else RW_CUDA(cudaStreamSynchronize(st));
+    finish();
     return;
   }
-  // Chunked double-buffered pipeline: H2D(k+1) overlaps scoring(k) on the
-  // other stream; costs come back per chunk.
-  const int64_t row = (int64_t)n * 4;
+  // Chunks of 4-48 MB of host data, at least 8 per call when the batch
+  // allows, so the first copy (not overlapped) is a small share of the call.
   int64_t chunk = std::max<int64_t>(1, ((int64_t)48 << 20) / row);
-  if (batch <= chunk) chunk = batch;
-  else if (batch < 4 * chunk) chunk = (batch + 3) / 4;
-  int32_t* d_perm[2];
+  const int64_t min_chunk = std::max<int64_t>(1, ((int64_t)4 << 20) / row);
+  if (batch < 8 * chunk) chunk = std::max(min_chunk, (batch + 7) / 8);
+  chunk = std::min(chunk, batch);
+  char* d_in[2];
+  uint16_t* d_u16[2];
   double* d_cost[2];
   for (int s = 0; s < 2; ++s) {
-    d_perm[s] = static_cast<int32_t*>(c.scratch(s, (size_t)chunk * row + (size_t)chunk * 8 + 64));
-    d_cost[s] = reinterpret_cast<double*>(reinterpret_cast<char*>(d_perm[s]) + align16((size_t)chunk * row));
+    const size_t pb = align16((size_t)(chunk * row)), ub = align16(u16_bytes * chunk);
+    d_in[s] = static_cast<char*>(c.scratch(s, pb + ub + (size_t)chunk * 8 + 64));
+    d_u16[s] = reinterpret_cast<uint16_t*>(d_in[s] + pb);
+    d_cost[s] = reinterpret_cast<double*>(d_in[s] + pb + ub);
   }
   RW_CUDA(cudaEventRecord(c.ev[0], c.stream[0]));
   RW_CUDA(cudaStreamWaitEvent(c.stream[1], c.ev[0], 0));
@@ -1039,19 +1089,20 @@ void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms
     const int s = k & 1;
     const int64_t cnt = std::min(chunk, batch - off);
     cudaStream_t st = c.stream[s];
-    RW_CUDA(cudaMemcpyAsync(d_perm[s], perms + off * n, (size_t)cnt * row, cudaMemcpyHostToDevice, st));
-    launch_evaluate(p, plan, d_perm[s], 4, cnt, d_cost[s], exact, validate, c.d_err, st, 2 + 2 * s);
+    const void* d_eval = stage(st, hp + off * row, cnt, d_in[s], d_u16[s]);
+    launch_evaluate(p, plan, d_eval, eval_bytes, cnt, d_cost[s], exact, validate, c.d_err, st, 2 + 2 * s);
     RW_CUDA(cudaMemcpyAsync(costs + off, d_cost[s], (size_t)cnt * 8, cudaMemcpyDeviceToHost, st));
   }
   RW_CUDA(cudaEventRecord(c.ev[1], c.stream[1]));
   RW_CUDA(cudaStreamWaitEvent(c.stream[0], c.ev[1], 0));
   RW_CUDA(cudaStreamSynchronize(c.stream[0]));
   if (validate) raise_order_errors(c.d_err, c.h_err, c.stream[0]);
-  if (report) {
-    report->bit_exact = (plan.bit_exact || exact) ? 1 : 0;
-    report->kernel = plan.model;
-    report->lookups = lookups_per_eval(plan) * batch;
-  }
+  finish();
+}
+
+void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms, int64_t batch, double* costs,
+                          bool exact, bool validate, rw_eval_report* report) {
+  evaluate_host_orders_fmt(p, plan, perms, 4, 0, batch, costs, exact, validate, report);
 }
 
 double schedule_cost_device(const Problem& p, int semantics, int nrounds, const int32_t* round_offsets,

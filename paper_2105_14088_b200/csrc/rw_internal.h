@@ -132,6 +132,25 @@ struct ThreadCtx {
 };
 ThreadCtx& thread_ctx(int device);
 
+// Scope of one asynchronous *_device call on a caller's stream: every scratch
+// buffer the launch code asks for (ThreadCtx::scratch) comes from the
+// stream-ordered allocator on that stream and is freed, stream-ordered, when
+// the scope ends.  So concurrent device calls on different streams, or a
+// device call followed by a host-buffer call before the stream drains, never
+// share buffers; and the allocation is capturable into a CUDA graph.
+struct StreamScratch {
+  int device;
+  cudaStream_t stream;
+  StreamScratch* prev;
+  void* buf[8] = {};
+  size_t cap[8] = {};
+  StreamScratch(int device, cudaStream_t stream);
+  ~StreamScratch();
+  StreamScratch(const StreamScratch&) = delete;
+  StreamScratch& operator=(const StreamScratch&) = delete;
+  void* get(int slot, size_t bytes);
+};
+
 // Reads and clears an error slot; throws the reference's domain_error text.
 void raise_order_errors(int* d_err, int* h_err, cudaStream_t st);
 
@@ -183,6 +202,12 @@ void local_search_device(Problem& p, const EvalPlan& plan, int32_t* perms, int64
 
 // Random orders (Philox), device side.
 void sample_orders_device(int n, int64_t samples, uint64_t seed, uint16_t* d_out, cudaStream_t st);
+
+// Host orders of any accepted layout (fmt 4: int32, 2: uint16, 0: packed with
+// `bits` per element) through the chunked H2D / score / D2H pipeline.
+void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perms, int fmt, int bits, int64_t batch,
+                              double* costs, bool exact, bool validate, rw_eval_report* report);
+int64_t packed_row_bytes(int n, int bits);
 
 // Scores host orders and returns reference-exact costs (used by search code).
 void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms, int64_t batch, double* costs,

@@ -31,7 +31,47 @@ DeviceGuard::~DeviceGuard() {
 }
 
 // ------------------------------------------------------------ thread ctx --
+namespace {
+thread_local StreamScratch* t_stream_scratch = nullptr;
+}
+
+StreamScratch::StreamScratch(int dev, cudaStream_t s) : device(dev), stream(s), prev(t_stream_scratch) {
+  // Keep freed blocks in the device's default pool: a call's scratch is then
+  // a pool hit (microseconds), not a fresh cudaMalloc.
+  static thread_local int configured = -1;
+  if (configured != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    configured = dev;
+  }
+  t_stream_scratch = this;
+}
+
+StreamScratch::~StreamScratch() {
+  for (int i = 0; i < 8; ++i)
+    if (buf[i]) cudaFreeAsync(buf[i], stream);  // stream-ordered: after this call's kernels
+  t_stream_scratch = prev;
+}
+
+void* StreamScratch::get(int slot, size_t bytes) {
+  if (cap[slot] < bytes) {
+    if (buf[slot]) RW_CUDA(cudaFreeAsync(buf[slot], stream));
+    buf[slot] = nullptr;
+    RW_CUDA(cudaMallocAsync(&buf[slot], bytes, stream));
+    cap[slot] = bytes;
+  }
+  return buf[slot];
+}
+
 void* ThreadCtx::scratch(int slot, size_t bytes) {
+  // Inside an asynchronous *_device call the scratch is stream-ordered on the
+  // caller's stream (StreamScratch), never the per-thread buffers that the
+  // host-buffer calls use on the internal streams.
+  if (t_stream_scratch && t_stream_scratch->device == device) return t_stream_scratch->get(slot, bytes);
   if (d_cap[slot] < bytes) {
     if (d_buf[slot]) {
       RW_CUDA(cudaStreamSynchronize(stream[0]));

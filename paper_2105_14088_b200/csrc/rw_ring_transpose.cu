@@ -49,6 +49,7 @@ struct RouteArgs {
   int n;
   int R;          // rows per block (multiple of 8)
   int nblocks;
+  int aligned;    // 16-byte aligned uint16 orders: vector loads allowed
   unsigned long long* err;
 };
 
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(256, 5) k_ring_route(RouteArgs a, const P* __r
     const P* pp = perms + o * n;
     bool bad = false;
     if constexpr (sizeof(P) == 2) {
-      if ((n & 255) == 0) {
+      if ((n & 255) == 0 && a.aligned) {
         const uint4* pv = reinterpret_cast<const uint4*>(pp);
         uint32_t carry = ld_order<P>(pp, n - 1);
         const int nc = n >> 8;
@@ -502,7 +503,10 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   if (int_sums) RW_CUDA(cudaMemsetAsync(d_costs, 0, (size_t)batch * 8, st));
   for (int64_t off = 0; off < batch; off += kmax) {
     const int64_t cnt_o = std::min(kmax, batch - off);
-    RouteArgs ra{cnt_o, off, n, R, nblocks, reinterpret_cast<unsigned long long*>(err_slot)};
+    // 16-byte order loads need a 16-byte aligned base (an offset view of a
+    // caller's tensor may not be); n % 256 == 0 keeps every row aligned.
+    const int aligned = (reinterpret_cast<uintptr_t>(d_perms) % 16) == 0 ? 1 : 0;
+    RouteArgs ra{cnt_o, off, n, R, nblocks, aligned, reinterpret_cast<unsigned long long*>(err_slot)};
     // One full wave of resident route CTAs (grid-stride over the orders):
     // every CTA does the same work, so a partial second wave would be a tail.
     auto rgrid = [&](auto kern) {

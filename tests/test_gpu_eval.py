@@ -574,3 +574,87 @@ def test_unvalidated_matrices_nan_and_negative(port, path):
         want = port.evaluate_batch(m, perms, make_spec(alg, n, 1e6, 2, 1, pair))
         got = prob.evaluate_batch(spec, perms, exact=True)
         np.testing.assert_array_equal(got, want)  # NaN positions must agree too
+
+
+def test_device_calls_on_separate_streams_and_host_calls_do_not_share_scratch():
+    """rw_evaluate_batch_device takes its exchange buffers from the
+    stream-ordered allocator on the caller's stream: two device calls in
+    flight on different streams, and a host-buffer evaluate issued before
+    those streams drain, must each get the costs a serialized run gives."""
+    import torch
+    m = fixtures.config_matrix("C4", "fixed")
+    prob = rw.Problem(m)
+    spec = fixtures.ring_spec(1024, fixtures.SIZE_FIXED)
+    count = 1 << 15
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    oa = torch.rand((count, 1024), device="cuda", generator=g).argsort(dim=1).to(torch.int16)
+    ob = torch.rand((count, 1024), device="cuda", generator=g).argsort(dim=1).to(torch.int16)
+    host = np.ascontiguousarray(oa[:300].cpu().numpy().view(np.uint16).astype(np.int32)[:, ::-1])
+    want_a = torch.empty(count, dtype=torch.float64, device="cuda")
+    want_b = torch.empty(count, dtype=torch.float64, device="cuda")
+    prob.evaluate_batch_device(spec, oa.data_ptr(), 2, count, want_a.data_ptr())
+    prob.evaluate_batch_device(spec, ob.data_ptr(), 2, count, want_b.data_ptr())
+    torch.cuda.synchronize()
+    want_h = prob.evaluate_batch(spec, host)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        ca = torch.full((count,), -1.0, dtype=torch.float64, device="cuda")
+        cb = torch.full((count,), -1.0, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        prob.evaluate_batch_device(spec, oa.data_ptr(), 2, count, ca.data_ptr(), sa.cuda_stream)
+        prob.evaluate_batch_device(spec, ob.data_ptr(), 2, count, cb.data_ptr(), sb.cuda_stream)
+        got_h = prob.evaluate_batch(spec, host)  # before sa / sb drain
+        torch.cuda.synchronize()
+        prob.sync_errors()
+        assert torch.equal(ca, want_a) and torch.equal(cb, want_b)
+        assert np.array_equal(got_h, want_h)
+
+
+def test_unaligned_uint16_device_orders_take_the_scalar_loads(port):
+    """An offset view (data_ptr not 16-byte aligned) must not use the route's
+    16-byte vector loads; costs equal the aligned copy's and the oracle's."""
+    import torch
+    m = fixtures.config_matrix("C4", "fixed")
+    prob = rw.Problem(m)
+    spec = fixtures.ring_spec(1024, fixtures.SIZE_FIXED)
+    rng = np.random.default_rng(9)
+    rows = np.array([rng.permutation(1024) for _ in range(64)], dtype=np.uint16)
+    flat = torch.from_numpy(np.concatenate([[0], rows.ravel()]).astype(np.uint16).view(np.int16)).cuda()
+    view_ptr = flat.data_ptr() + 2  # one element in: 2-byte aligned only
+    assert view_ptr % 16 != 0
+    c = torch.empty(64, dtype=torch.float64, device="cuda")
+    prob.evaluate_batch_device(spec, view_ptr, 2, 64, c.data_ptr())
+    torch.cuda.synchronize()
+    prob.sync_errors()
+    want = port.evaluate_batch(m, rows.astype(np.int32), make_spec(0, 1024, fixtures.SIZE_FIXED))
+    assert np.array_equal(c.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n", [13, 64, 1024, 1000, 4096])
+def test_host_wire_layouts_agree(port, n):
+    """int32 (rw_evaluate_batch), uint16 (rw_evaluate_batch_u16) and packed
+    (rw_evaluate_batch_packed, ceil(log2 n) bits per host) host orders give the
+    same costs, equal to the oracle's; a packed order with a repeated host is
+    a domain_error like any other layout."""
+    rng = np.random.default_rng(n)
+    m = rng.integers(0, 4000, size=(n, n)).astype(float) / 16.0
+    np.fill_diagonal(m, 0.0)
+    prob = rw.Problem(m)
+    spec = rw.CollectiveSpec(rw.Algorithm.Ring, n, fixtures.SIZE_FIXED)
+    count = 3000 if n <= 1024 else 300
+    o = np.array([rng.permutation(n) for _ in range(count)], dtype=np.int32)
+    a = prob.evaluate_batch(spec, o)
+    b = prob.evaluate_batch(spec, o.astype(np.uint16))
+    bits = rw.api.packed_bits(n)
+    c = prob.evaluate_batch_packed(spec, rw.api.pack_orders(o, bits), bits, count)
+    d = prob.evaluate_batch_packed(spec, rw.api.pack_orders(o, 16), 16, count)
+    want = port.evaluate_batch(m, o[:50], make_spec(0, n, fixtures.SIZE_FIXED))
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
+    assert np.array_equal(a[:50], want)
+    bad = o[:5].copy()
+    bad[3, 1] = bad[3, 0]
+    with pytest.raises(rw.DomainError):
+        prob.evaluate_batch_packed(spec, rw.api.pack_orders(bad, bits), bits, 5)
+    with pytest.raises(rw.DomainError):
+        prob.evaluate_batch(spec, bad.astype(np.uint16))

@@ -205,3 +205,16 @@ def test_generator_matches_reference():
     ref = Reference()
     for levels in ([(4, 5, 1000, 1), (4, 25, 1000, 4)], [(8, 5, 1000, 1), (8, 25, 1000, 4)]):
         assert np.array_equal(ref.generate_matrix(levels, 0.1, 2105), api.generate_matrix(levels, 0.1, 2105))
+
+
+def test_reference_arm_builds_the_same_config_matrices():
+    """bench.py's reference arm builds the BASELINE matrices from oracle/_ref
+    alone (no product import); they must equal the product's fixtures."""
+    from oracle.pyoracle import Reference, reference_available, reference_config_matrix
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2105_14088_b200 import fixtures
+    ref = Reference()
+    for name in ("C1", "C2", "C3", "C4"):
+        for kind in ("fixed", "f32"):
+            assert np.array_equal(reference_config_matrix(ref, name, kind), fixtures.config_matrix(name, kind)), name
