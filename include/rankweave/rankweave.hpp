@@ -215,6 +215,12 @@ struct GpuOptions {
   // storage address and size instead -- the caller promises not to mutate a
   // CostMatrix it has passed before (O(1) per call instead of O(N^2)).
   bool immutable_matrices = false;
+  // > 1: brute_force, anneal, two_stage_solve and evaluate_batch run over that
+  // many devices of this process (the first num_devices visible ones, or all
+  // of them when the count exceeds the visible devices) through an
+  // in-process NCCL communicator; 0: every visible device.  Results do not
+  // depend on the device count for a fixed `chains`.
+  int num_devices = 1;
 };
 void set_gpu_options(const GpuOptions& opts);
 GpuOptions gpu_options();

@@ -259,6 +259,38 @@ rw_status rw_generate_matrix(int32_t nlevels, const int32_t* fanout, const doubl
  * m'[i][j] = m[rl[i]][rl[j]] (in place). */
 rw_status rw_relabel_matrix(double* m, int32_t n, uint64_t seed);
 
+/* ---- multi-GPU in one process (north star (4)) ------------- */
+/* A cost matrix replicated on a set of this process's devices (devices =
+ * NULL or ndevices <= 0: every visible device), with an in-process NCCL
+ * communicator over them (ncclCommInitAll; libnccl.so.2 is loaded on first
+ * use).  The matrix is analysed and uploaded once and ncclBroadcast from the
+ * first member.  Calls on one set are serialised. */
+typedef struct rw_problem_set rw_problem_set;
+enum { RW_LAYOUT_PACKED = 0, RW_LAYOUT_U16 = 2, RW_LAYOUT_INT32 = 4 };
+rw_status rw_problem_set_create(const double* rtt_us, int32_t n, int32_t storage_hint, const int32_t* devices,
+                                int32_t ndevices, rw_problem_set** out);
+rw_status rw_problem_set_destroy(rw_problem_set* s);
+rw_status rw_problem_set_devices(const rw_problem_set* s, int32_t* ndevices_out, int32_t* devices_out);
+/* Borrowed handle of member `index` (valid while the set lives). */
+rw_status rw_problem_set_member(const rw_problem_set* s, int32_t index, rw_problem** out);
+/* One host batch (layout RW_LAYOUT_*; `bits` for packed) split into
+ * contiguous slices, one per device, each over its own PCIe link. */
+rw_status rw_evaluate_batch_set(const rw_problem_set* s, const rw_spec* spec, const void* perms, int32_t layout,
+                                int32_t bits, int64_t batch, double* costs, uint32_t flags);
+/* brute_force over the set: the lexicographic range split evenly; winner by
+ * ncclAllReduce MIN on the cost, then MIN on the lex index at that cost --
+ * the same order, cost and evaluation count as one device. */
+rw_status rw_brute_force_set(const rw_problem_set* s, const rw_spec* spec, int32_t threshold, int32_t* perm_out,
+                             double* cost_out, uint64_t* evals_out);
+/* anneal over the set: global chain ids [0, chains) split over the members
+ * (gpu->chains <= 0: the single-device default per member); winner by
+ * ncclAllReduce MIN on the cost, MIN on the chain id, ncclBroadcast of the
+ * order from its owner.  For a fixed chain count the result does not depend
+ * on the number of devices. */
+rw_status rw_anneal_set(const rw_problem_set* s, const rw_spec* spec, const rw_solver_config* cfg,
+                        const rw_gpu_config* gpu, int32_t* perm_out, double* cost_out, uint64_t* evals_out,
+                        rw_search_report* report);
+
 /* ---- host logic (one implementation, shared with the C++ drop-in) ------ */
 /* distribution_stats (stats.cpp:64-81): out4 = {min, max, mean, stddev}. */
 rw_status rw_distribution_stats(const double* values, int64_t count, double* out4);

@@ -96,6 +96,14 @@ SIGNATURES = {
     "rw_sample_costs": (C.c_int, [_vp, P(rw_spec), C.c_int32, C.c_uint64, _dp]),
     "rw_sample_orders_philox": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _i32p]),
     "rw_sample_costs_philox": (C.c_int, [_vp, P(rw_spec), C.c_int32, C.c_uint64, _dp]),
+    "rw_problem_set_create": (C.c_int, [_dp, C.c_int32, C.c_int32, _i32p, C.c_int32, P(_vp)]),
+    "rw_problem_set_destroy": (C.c_int, [_vp]),
+    "rw_problem_set_devices": (C.c_int, [_vp, _i32p, _i32p]),
+    "rw_problem_set_member": (C.c_int, [_vp, C.c_int32, P(_vp)]),
+    "rw_evaluate_batch_set": (C.c_int, [_vp, P(rw_spec), _vp, C.c_int32, C.c_int32, C.c_int64, _dp, C.c_uint32]),
+    "rw_brute_force_set": (C.c_int, [_vp, P(rw_spec), C.c_int32, _i32p, _dp, _u64p]),
+    "rw_anneal_set": (C.c_int, [_vp, P(rw_spec), P(rw_solver_config), P(rw_gpu_config), _i32p, _dp, _u64p,
+                                P(rw_search_report)]),
     "rw_distribution_stats": (C.c_int, [_dp, C.c_int64, _dp]),
     "rw_spearman": (C.c_int, [_dp, _dp, C.c_int64, C.c_int64, _dp]),
     "rw_parse_model_file": (C.c_int, [C.c_char_p, C.c_int32, _i32p]),

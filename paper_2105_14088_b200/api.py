@@ -190,6 +190,73 @@ class Problem:
         return order, cost.value, ev.value, {f: getattr(rep, f) for f, _ in rep._fields_}
 
 
+class ProblemSet:
+    """A cost matrix replicated on several GPUs of this process with an
+    in-process NCCL communicator (the C ABI's rw_problem_set): sharded batch
+    scoring, exhaustive search and annealing, reduced with NCCL."""
+
+    def __init__(self, rtt_us: np.ndarray, devices: Optional[Sequence[int]] = None,
+                 storage: int = _lib.RW_STORAGE_AUTO):
+        m = np.ascontiguousarray(rtt_us, dtype=np.float64)
+        if m.ndim != 2 or m.shape[0] != m.shape[1]:
+            raise DomainError("matrix is not square")
+        self.n = int(m.shape[0])
+        devs = np.asarray(list(devices) if devices is not None else [], dtype=np.int32)
+        h = C.c_void_p()
+        check(lib.rw_problem_set_create(ptr(m, C.c_double), self.n, storage,
+                                        ptr(devs, C.c_int32) if devs.size else None, int(devs.size), C.byref(h)))
+        self._h = h
+        k = C.c_int32()
+        check(lib.rw_problem_set_devices(self._h, C.byref(k), None))
+        out = np.empty(k.value, dtype=np.int32)
+        check(lib.rw_problem_set_devices(self._h, C.byref(k), ptr(out, C.c_int32)))
+        self.devices = out.tolist()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.rw_problem_set_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def evaluate_batch(self, spec: "CollectiveSpec", orders: np.ndarray, exact: bool = False,
+                       validate: bool = True) -> np.ndarray:
+        u16 = isinstance(orders, np.ndarray) and orders.dtype == np.uint16
+        o = np.ascontiguousarray(orders, dtype=np.uint16 if u16 else np.int32)
+        if o.ndim == 1:
+            o = o[None, :]
+        if o.shape[1] != spec.n:
+            raise DomainError(f"rank order has {o.shape[1]} entries, expected {spec.n}")
+        out = np.empty(o.shape[0], dtype=np.float64)
+        flags = (_lib.RW_EVAL_EXACT if exact else 0) | (0 if validate else _lib.RW_EVAL_NO_VALIDATE)
+        check(lib.rw_evaluate_batch_set(self._h, C.byref(spec._c()), C.c_void_p(o.ctypes.data), 2 if u16 else 4, 0,
+                                        o.shape[0], ptr(out, C.c_double), flags))
+        return out
+
+    def brute_force(self, spec: "CollectiveSpec", threshold: int = 10) -> "Solution":
+        perm = np.empty(spec.n, dtype=np.int32)
+        cost = C.c_double()
+        ev = C.c_uint64()
+        check(lib.rw_brute_force_set(self._h, C.byref(spec._c()), threshold, ptr(perm, C.c_int32), C.byref(cost),
+                                     C.byref(ev)))
+        return Solution(RankOrder(perm.tolist()), cost.value, SolveMethod.BruteForce, ev.value)
+
+    def anneal(self, spec: "CollectiveSpec", cfg: "SolverConfig", chains: int = 0, max_proposals: int = 0,
+               schedule: str = "reference"):
+        order = np.empty(spec.n, dtype=np.int32)
+        cost = C.c_double()
+        ev = C.c_uint64()
+        rep = _lib.rw_search_report()
+        g = _lib.rw_gpu_config(chains, 0, 0, {"reference": 0, "calibrated": 1}[schedule], max_proposals)
+        check(lib.rw_anneal_set(self._h, C.byref(spec._c()), C.byref(cfg._c()), C.byref(g), ptr(order, C.c_int32),
+                                C.byref(cost), C.byref(ev), C.byref(rep)))
+        return order, cost.value, ev.value, {f: getattr(rep, f) for f, _ in rep._fields_}
+
+
 class CostMatrix:
     """N x N pairwise costs in microseconds (types.hpp:42-53).
 

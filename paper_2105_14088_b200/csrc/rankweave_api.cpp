@@ -131,6 +131,51 @@ ProblemRef device_problem(const CostMatrix& m) {
   return cache().get(m, o.device, o.immutable_matrices);
 }
 
+// Device sets (GpuOptions::num_devices != 1), cached by exact content like
+// the single-device problems.
+class SetCache {
+ public:
+  std::shared_ptr<rw_problem_set> get(const CostMatrix& m, int ndev) {
+    std::lock_guard<std::mutex> lock(mu_);
+    const std::size_t bytes = m.rtt_us.size() * sizeof(double);
+    for (auto it = entries_.begin(); it != entries_.end(); ++it)
+      if (it->ndev == ndev && it->shadow.size() == m.rtt_us.size() &&
+          same_bytes(it->shadow.data(), m.rtt_us.data(), bytes)) {
+        entries_.splice(entries_.begin(), entries_, it);
+        return entries_.front().set;
+      }
+    std::vector<int32_t> devs;
+    const int visible = rw_device_count();
+    const int k = ndev <= 0 ? visible : std::min(ndev, visible);
+    for (int d = 0; d < k; ++d) devs.push_back(d);
+    rw_problem_set* raw = nullptr;
+    check(rw_problem_set_create(m.rtt_us.data(), m.n(), RW_STORAGE_AUTO, devs.data(), static_cast<int32_t>(devs.size()),
+                                &raw));
+    std::shared_ptr<rw_problem_set> s(raw, [](rw_problem_set* q) { rw_problem_set_destroy(q); });
+    entries_.push_front(Entry{ndev, m.rtt_us, s});
+    while (entries_.size() > 4) entries_.pop_back();
+    return s;
+  }
+
+ private:
+  struct Entry {
+    int ndev;
+    std::vector<double> shadow;
+    std::shared_ptr<rw_problem_set> set;
+  };
+  std::mutex mu_;
+  std::list<Entry> entries_;
+};
+
+std::shared_ptr<rw_problem_set> device_set(const CostMatrix& m) {
+  static SetCache* c = new SetCache();  // never destroyed: CUDA may be gone at exit
+  if (m.rtt_us.size() != static_cast<std::size_t>(m.n()) * static_cast<std::size_t>(m.n()))
+    throw domain_error("cost matrix storage is not n*n");
+  return c->get(m, gpu_options().num_devices);
+}
+
+bool use_device_set() { return gpu_options().num_devices != 1; }
+
 rw_spec to_c(const CollectiveSpec& s) {
   rw_spec c{};
   c.algorithm = static_cast<int32_t>(s.algorithm);
@@ -380,8 +425,13 @@ std::vector<double> evaluate_batch(const CostMatrix& m, const std::vector<RankOr
   }
   std::vector<double> costs(orders.size());
   const rw_spec cs = to_c(spec);
-  check(rw_evaluate_batch(device_problem(m), &cs, flat.data(), static_cast<int64_t>(orders.size()), costs.data(),
-                          gpu_options().exact_batch ? static_cast<uint32_t>(RW_EVAL_EXACT) : 0u, nullptr));
+  const uint32_t flags = gpu_options().exact_batch ? static_cast<uint32_t>(RW_EVAL_EXACT) : 0u;
+  if (use_device_set())
+    check(rw_evaluate_batch_set(device_set(m).get(), &cs, flat.data(), RW_LAYOUT_INT32, 0,
+                                static_cast<int64_t>(orders.size()), costs.data(), flags));
+  else
+    check(rw_evaluate_batch(device_problem(m), &cs, flat.data(), static_cast<int64_t>(orders.size()), costs.data(),
+                            flags, nullptr));
   return costs;
 }
 
@@ -451,7 +501,10 @@ Solution brute_force(const CostMatrix& m, const CollectiveSpec& spec, int thresh
   sol.method = SolveMethod::BruteForce;
   sol.order.perm.resize(static_cast<std::size_t>(spec.n));
   uint64_t evals = 0;
-  check(rw_brute_force(device_problem(m), &cs, threshold, sol.order.perm.data(), &sol.cost, &evals));
+  if (use_device_set())
+    check(rw_brute_force_set(device_set(m).get(), &cs, threshold, sol.order.perm.data(), &sol.cost, &evals));
+  else
+    check(rw_brute_force(device_problem(m), &cs, threshold, sol.order.perm.data(), &sol.cost, &evals));
   sol.evaluations = evals;
   return sol;
 }
@@ -503,7 +556,10 @@ Solution anneal(const CostMatrix& m, const CollectiveSpec& spec, const SolverCon
   sol.method = SolveMethod::Anneal;
   sol.order.perm.resize(static_cast<std::size_t>(spec.n));
   uint64_t evals = 0;
-  check(rw_anneal(device_problem(m), &cs, &c, &g, sol.order.perm.data(), &sol.cost, &evals, nullptr));
+  if (use_device_set())
+    check(rw_anneal_set(device_set(m).get(), &cs, &c, &g, sol.order.perm.data(), &sol.cost, &evals, nullptr));
+  else
+    check(rw_anneal(device_problem(m), &cs, &c, &g, sol.order.perm.data(), &sol.cost, &evals, nullptr));
   sol.evaluations = evals;
   return sol;
 }

@@ -461,4 +461,15 @@ void brute_force_range(const Problem& p, const EvalPlan& plan, uint64_t first, u
   *index_out = h.index;
 }
 
+namespace {
+__global__ void k_select_key(SetReduce* r) {
+  r->min_key = r->cost == r->min_cost ? r->key : ~0ull;
+}
+}  // namespace
+
+void launch_select_key(SetReduce* d, cudaStream_t st) {
+  k_select_key<<<1, 1, 0, st>>>(d);
+  RW_CUDA(cudaGetLastError());
+}
+
 }  // namespace rwb

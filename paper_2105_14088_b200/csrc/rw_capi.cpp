@@ -25,6 +25,11 @@ struct rw_problem {
   rwb::Problem* impl;
 };
 
+struct rw_problem_set {
+  rwb::ProblemSet* impl;
+  std::vector<rw_problem> members;  // borrowed handles of the member problems
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -657,6 +662,133 @@ rw_status rw_two_stage_solve(const double* rtt_us, int32_t n, const rw_spec* spe
     *cost_out = sol.cost;
     if (method_out) *method_out = static_cast<int32_t>(sol.method);
     if (evals_out) *evals_out = sol.evaluations;
+  });
+}
+
+// ---- multi-GPU: one process, a device set, in-process NCCL -----------------
+
+rw_status rw_problem_set_create(const double* rtt_us, int32_t n, int32_t storage_hint, const int32_t* devices,
+                                int32_t ndevices, rw_problem_set** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    need(rtt_us, "rtt_us");
+    auto* h = new rw_problem_set{nullptr, {}};
+    try {
+      h->impl = rwb::problem_set_create(rtt_us, n, storage_hint, devices, ndevices);
+      for (int i = 0; i < rwb::problem_set_size(*h->impl); ++i)
+        h->members.push_back(rw_problem{&rwb::problem_set_member(*h->impl, i)});
+    } catch (...) {
+      if (h->impl) rwb::problem_set_destroy(h->impl);
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+rw_status rw_problem_set_destroy(rw_problem_set* s) {
+  return guarded([&] {
+    if (!s) return;
+    rwb::problem_set_destroy(s->impl);
+    delete s;
+  });
+}
+
+namespace {
+rwb::ProblemSet& get_set(const rw_problem_set* s) {
+  if (!s || !s->impl) rwb::fail_domain("null rw_problem_set");
+  return *s->impl;
+}
+}  // namespace
+
+rw_status rw_problem_set_devices(const rw_problem_set* s, int32_t* ndevices_out, int32_t* devices_out) {
+  return guarded([&] {
+    need(ndevices_out, "ndevices_out");
+    rwb::ProblemSet& q = get_set(s);
+    *ndevices_out = rwb::problem_set_size(q);
+    if (devices_out)
+      for (int i = 0; i < *ndevices_out; ++i) devices_out[i] = rwb::problem_set_device(q, i);
+  });
+}
+
+rw_status rw_problem_set_member(const rw_problem_set* s, int32_t index, rw_problem** out) {
+  return guarded([&] {
+    need(out, "out");
+    get_set(s);
+    if (index < 0 || index >= static_cast<int32_t>(s->members.size())) rwb::fail_domain("member index out of range");
+    *out = const_cast<rw_problem*>(&s->members[static_cast<size_t>(index)]);
+  });
+}
+
+rw_status rw_evaluate_batch_set(const rw_problem_set* s, const rw_spec* spec, const void* perms, int32_t layout,
+                                int32_t bits, int64_t batch, double* costs, uint32_t flags) {
+  return guarded([&] {
+    need(spec, "spec");
+    if (batch < 0) rwb::fail_domain("batch must be >= 0");
+    if (batch > 0) {
+      need(perms, "perms");
+      need(costs, "costs");
+    }
+    rwb::ProblemSet& q = get_set(s);
+    rwb::make_plan(rwb::problem_set_member(q, 0), *spec);  // validates spec and n
+    if (layout != RW_LAYOUT_INT32 && layout != RW_LAYOUT_U16 && layout != RW_LAYOUT_PACKED)
+      rwb::fail_domain("unknown order layout");
+    if (layout == RW_LAYOUT_PACKED && (bits < 1 || bits > 16 || (spec->n > 1 && (1ll << bits) < spec->n)))
+      rwb::fail_domain("packed orders need 1 <= bits <= 16 and 2^bits >= n");
+    rwb::evaluate_host_orders_set(q, *spec, perms, layout, bits, batch, costs, (flags & RW_EVAL_EXACT) != 0,
+                                  (flags & RW_EVAL_NO_VALIDATE) == 0);
+  });
+}
+
+rw_status rw_brute_force_set(const rw_problem_set* s, const rw_spec* spec, int32_t threshold, int32_t* perm_out,
+                             double* cost_out, uint64_t* evals_out) {
+  return guarded([&] {
+    need(spec, "spec");
+    need(perm_out, "perm_out");
+    need(cost_out, "cost_out");
+    rwb::validate_spec(*spec);
+    if (spec->n > threshold)
+      rwb::fail_domain("N=" + std::to_string(spec->n) + " exceeds the brute-force threshold " +
+                       std::to_string(threshold) + "; use anneal");
+    rwb::ProblemSet& q = get_set(s);
+    rwb::make_plan(rwb::problem_set_member(q, 0), *spec);
+    rwb::brute_force_set(q, *spec, perm_out, cost_out, evals_out);
+  });
+}
+
+rw_status rw_anneal_set(const rw_problem_set* s, const rw_spec* spec, const rw_solver_config* cfg,
+                        const rw_gpu_config* gpu, int32_t* perm_out, double* cost_out, uint64_t* evals_out,
+                        rw_search_report* report) {
+  return guarded([&] {
+    const auto t_start = std::chrono::steady_clock::now();
+    need(spec, "spec");
+    need(cfg, "cfg");
+    need(perm_out, "perm_out");
+    need(cost_out, "cost_out");
+    rwb::validate_spec(*spec);
+    if (!(cfg->budget_s > 0.0)) rwb::fail_domain("solver budget must be > 0");
+    if (!(cfg->cooling > 0.0 && cfg->cooling < 1.0)) rwb::fail_domain("cooling factor must be in (0, 1)");
+    if (cfg->restarts < 1) rwb::fail_domain("restarts must be >= 1");
+    if (cfg->brute_force_threshold < 2) rwb::fail_domain("brute-force threshold must be >= 2");
+    rwb::ProblemSet& q = get_set(s);
+    if (rwb::problem_set_member(q, 0).n != spec->n) rwb::fail_domain("matrix dimension does not match spec.n");
+    rwb::make_plan(rwb::problem_set_member(q, 0), *spec);
+    rw_gpu_config g{};
+    if (gpu) g = *gpu;
+    const rwb::AnnealResult r = rwb::anneal_set(q, *spec, *cfg, g);
+    std::copy(r.order.begin(), r.order.end(), perm_out);
+    *cost_out = r.cost;
+    if (evals_out) *evals_out = r.evaluations;
+    if (report) {
+      report->winner_chain = r.chain;
+      report->chains = r.chains;
+      report->proposals = static_cast<int64_t>(r.proposals);
+      report->levels = r.levels;
+      report->levels_run = r.levels_run;
+      report->initial_temperature = r.t0;
+      report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
   });
 }
 

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <limits>
 #include <type_traits>
+#include <vector>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
@@ -843,10 +844,17 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   // Ring transpose pays while a row block holds enough rows per order slice:
   // on B200 it wins at N=1024 (4.2e8 vs 2.8e8 evals/s) and loses from N=2048
   // (1.23e8 vs 1.35e8; N=4096 3.4e7 vs 6.7e7), so AUTO stops at 1536.
-  if (model == kRing && !smem_mat && (p.path == RW_PATH_TRANSPOSE || (p.path == RW_PATH_AUTO && n <= 1536)) &&
+  // Small batches (single evaluate() calls, short e2e chunks) skip the
+  // transpose paths: their fixed cost per launch (memset, three kernels, every
+  // score CTA staging a row block) exceeds one gather launch below a few
+  // thousand orders.
+  const bool few = batch < (model == kRing ? 4096 : 512);
+  if (model == kRing && !smem_mat &&
+      (p.path == RW_PATH_TRANSPOSE || (p.path == RW_PATH_AUTO && n <= 1536 && !few)) &&
       launch_ring_transpose(p, plan, d_perms, (int)sizeof(P), batch, d_costs, validate, err_slot, st, slot))
     return;
-  if (model == kHalvingDoubling && !smem_mat && (p.path == RW_PATH_AUTO || p.path == RW_PATH_TRANSPOSE) &&
+  if (model == kHalvingDoubling && !smem_mat &&
+      (p.path == RW_PATH_TRANSPOSE || (p.path == RW_PATH_AUTO && !few)) &&
       launch_rounds_transpose(p, plan, d_perms, (int)sizeof(P), batch, d_costs, validate, err_slot, st, slot))
     return;
   if constexpr (std::is_same<P, uint16_t>::value) {
@@ -1026,9 +1034,48 @@ int64_t packed_row_bytes(int n, int bits) { return 16 * (((int64_t)n * bits + 12
 // copy of chunk k+1 overlaps the scoring of chunk k on the other stream, and
 // costs come back per chunk.  fmt: 4 = int32, 2 = uint16, 0 = packed (`bits`
 // per element; unpacked on the device into uint16 before scoring).
+// First invalid order of a host batch (error path only: the device flagged
+// one; the device's index is relative to its launch, this one is global).
+static int64_t first_bad_host_order(const void* perms, int fmt, int bits, int64_t batch, int n) {
+  const int64_t row = fmt == 0 ? packed_row_bytes(n, bits) : (int64_t)n * fmt;
+  std::vector<unsigned char> seen((size_t)n);
+  for (int64_t b = 0; b < batch; ++b) {
+    const char* r = static_cast<const char*>(perms) + b * row;
+    std::fill(seen.begin(), seen.end(), 0);
+    bool ok = true;
+    for (int i = 0; i < n && ok; ++i) {
+      int64_t v;
+      if (fmt == 4) v = reinterpret_cast<const int32_t*>(r)[i];
+      else if (fmt == 2) v = reinterpret_cast<const uint16_t*>(r)[i];
+      else {
+        const auto* w = reinterpret_cast<const uint32_t*>(r);
+        const uint32_t bit = (uint32_t)i * (uint32_t)bits, q = bit >> 5, sh = bit & 31u;
+        uint32_t x = w[q] >> sh;
+        if (sh + (uint32_t)bits > 32u) x |= w[q + 1] << (32u - sh);
+        v = x & ((1u << bits) - 1u);
+      }
+      ok = v >= 0 && v < n && !seen[(size_t)v];
+      if (ok) seen[(size_t)v] = 1;
+    }
+    if (!ok) return b;
+  }
+  return -1;
+}
+
 void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perms, int fmt, int bits, int64_t batch,
-                              double* costs, bool exact, bool validate, rw_eval_report* report) {
+                              double* costs, bool exact, bool validate, rw_eval_report* report, int64_t index_base) {
   if (batch <= 0) return;
+  auto raise = [&](cudaStream_t st) {
+    ThreadCtx& cc = thread_ctx(p.device);
+    try {
+      raise_order_errors(cc.d_err, cc.h_err, st);
+    } catch (const Failure& f) {
+      if (f.status != RW_ERR_DOMAIN) throw;
+      const int64_t b = first_bad_host_order(perms, fmt, bits, batch, plan.n);
+      throw Failure(RW_ERR_DOMAIN, "rank order is not a permutation of [0, " + std::to_string(plan.n) +
+                                       ") (batch entry " + std::to_string(index_base + std::max<int64_t>(b, 0)) + ")");
+    }
+  };
   DeviceGuard g(p.device);
   ThreadCtx& c = thread_ctx(p.device);
   const int n = plan.n;
@@ -1053,17 +1100,22 @@ void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perm
   };
   const size_t u16_bytes = fmt == 0 ? align16((size_t)n * 2) : 0;  // per order, packed only
   if (batch * (int64_t)n <= (1 << 16)) {
-    // small batches (single evaluate() calls): one stream, one synchronisation
+    // small batches (single evaluate() calls): orders and costs go through a
+    // pinned staging buffer (a pageable copy is a synchronous staged copy in
+    // the driver), one stream, one synchronisation
     cudaStream_t st = c.stream[0];
     const size_t pb = align16((size_t)(batch * row));
     const size_t ub = align16(u16_bytes * batch);
     char* base = static_cast<char*>(c.scratch(0, pb + ub + (size_t)batch * 8 + 64));
     auto* d_cost = reinterpret_cast<double*>(base + pb + ub);
-    const void* d_eval = stage(st, hp, batch, base, reinterpret_cast<uint16_t*>(base + pb));
+    char* h = static_cast<char*>(c.pinned(pb + (size_t)batch * 8));
+    std::memcpy(h, hp, (size_t)(batch * row));
+    const void* d_eval = stage(st, h, batch, base, reinterpret_cast<uint16_t*>(base + pb));
     launch_evaluate(p, plan, d_eval, eval_bytes, batch, d_cost, exact, validate, c.d_err, st, 2);
-    RW_CUDA(cudaMemcpyAsync(costs, d_cost, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
-    if (validate) raise_order_errors(c.d_err, c.h_err, st);  // synchronises st
+    RW_CUDA(cudaMemcpyAsync(h + pb, d_cost, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+    if (validate) raise(st);  // synchronises st
     else RW_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(costs, h + pb, (size_t)batch * 8);
     finish();
     return;
   }
@@ -1096,7 +1148,7 @@ void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perm
   RW_CUDA(cudaEventRecord(c.ev[1], c.stream[1]));
   RW_CUDA(cudaStreamWaitEvent(c.stream[0], c.ev[1], 0));
   RW_CUDA(cudaStreamSynchronize(c.stream[0]));
-  if (validate) raise_order_errors(c.d_err, c.h_err, c.stream[0]);
+  if (validate) raise(c.stream[0]);
   finish();
 }
 

@@ -128,7 +128,10 @@ struct ThreadCtx {
   int* h_err = nullptr;  // pinned
   void* d_buf[8] = {};
   size_t d_cap[8] = {};
+  void* h_pin = nullptr;  // pinned host staging for small synchronous calls
+  size_t h_cap = 0;
   void* scratch(int slot, size_t bytes);
+  void* pinned(size_t bytes);
 };
 ThreadCtx& thread_ctx(int device);
 
@@ -203,10 +206,39 @@ void local_search_device(Problem& p, const EvalPlan& plan, int32_t* perms, int64
 // Random orders (Philox), device side.
 void sample_orders_device(int n, int64_t samples, uint64_t seed, uint16_t* d_out, cudaStream_t st);
 
+// ---------------------------------------------------- multi-GPU (rw_multi) --
+// Per-member reduction record of a sharded search (device memory): the
+// member's best (cost, tie key) and evaluation count, and the all-reduced
+// results.
+struct alignas(16) SetReduce {
+  double cost;
+  double min_cost;                // NCCL all-reduce MIN of cost
+  unsigned long long key;         // member's tie key (lex index / chain id)
+  unsigned long long min_key;     // MIN of the keys of members at min_cost
+  unsigned long long evals;
+  unsigned long long evals_sum;   // NCCL all-reduce SUM of evals
+};
+// min_key = (cost == min_cost) ? key : ~0, on the device (one thread).
+void launch_select_key(SetReduce* d, cudaStream_t st);
+
+struct ProblemSet;
+ProblemSet* problem_set_create(const double* rtt, int n, int hint, const int* devices, int ndev);
+void problem_set_destroy(ProblemSet* s);
+int problem_set_size(const ProblemSet& s);
+Problem& problem_set_member(ProblemSet& s, int i);
+int problem_set_device(const ProblemSet& s, int i);
+void evaluate_host_orders_set(ProblemSet& s, const rw_spec& spec, const void* perms, int fmt, int bits, int64_t batch,
+                              double* costs, bool exact, bool validate);
+void brute_force_set(ProblemSet& s, const rw_spec& spec, int32_t* perm_out, double* cost_out, uint64_t* evals_out);
+struct AnnealResult;
+AnnealResult anneal_set(ProblemSet& s, const rw_spec& spec, const rw_solver_config& cfg, const rw_gpu_config& gpu);
+
 // Host orders of any accepted layout (fmt 4: int32, 2: uint16, 0: packed with
 // `bits` per element) through the chunked H2D / score / D2H pipeline.
+// index_base: batch index of perms[0] in the caller's batch (error messages).
 void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perms, int fmt, int bits, int64_t batch,
-                              double* costs, bool exact, bool validate, rw_eval_report* report);
+                              double* costs, bool exact, bool validate, rw_eval_report* report,
+                              int64_t index_base = 0);
 int64_t packed_row_bytes(int n, int bits);
 
 // Scores host orders and returns reference-exact costs (used by search code).

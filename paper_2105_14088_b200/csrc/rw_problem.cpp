@@ -7,9 +7,11 @@
 //   check_inputs (cost_model.cpp:13-19)   -> make_plan (same wording)
 //   round_bytes (cost_model.cpp:47-51)    -> EvalPlan::round_bytes (same FP64 ops)
 //   expand_dbt (cost_model.cpp:194-222)   -> build_dbt_plan (critical-path tree)
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <memory>
 
 #include "rw_internal.h"
 
@@ -84,6 +86,21 @@ void* ThreadCtx::scratch(int slot, size_t bytes) {
     d_cap[slot] = cap;
   }
   return d_buf[slot];
+}
+
+void* ThreadCtx::pinned(size_t bytes) {
+  if (h_cap < bytes) {
+    if (h_pin) {
+      RW_CUDA(cudaStreamSynchronize(stream[0]));
+      RW_CUDA(cudaStreamSynchronize(stream[1]));
+      RW_CUDA(cudaFreeHost(h_pin));
+      h_pin = nullptr;
+    }
+    const size_t cap = std::max<size_t>(bytes + bytes / 2, 64 * 1024);
+    RW_CUDA(cudaMallocHost(&h_pin, cap));
+    h_cap = cap;
+  }
+  return h_pin;
 }
 
 ThreadCtx& thread_ctx(int device) {
@@ -527,6 +544,30 @@ static Problem* create_problem(const double* rtt, int n, int hint, int device) {
   return p.release();
 }
 
+// A replica of `src` on another device: the host-side analysis and metadata
+// are copied, the device matrix is allocated but NOT filled (the problem set
+// broadcasts it from the first member over NVLink, rw_multi.cpp).
+static Problem* replica_problem(const Problem& src, int device) {
+  auto p = std::make_unique<Problem>();
+  p->n = src.n;
+  p->device = device;
+  p->storage = src.storage;
+  p->frac_bits = src.frac_bits;
+  p->scale = src.scale;
+  p->symmetric = src.symmetric;
+  p->zero_diag = src.zero_diag;
+  p->max_value = src.max_value;
+  p->max_q = src.max_q;
+  p->mat_bytes = src.mat_bytes;
+  p->path = src.path;
+  DeviceGuard g(device);
+  RW_CUDA(cudaMalloc(&p->d_mat, p->mat_bytes));
+  RW_CUDA(cudaMalloc(&p->d_err, 2 * sizeof(unsigned long long)));
+  const unsigned long long init[2] = {0ull, ~0ull};
+  RW_CUDA(cudaMemcpy(p->d_err, init, sizeof(init), cudaMemcpyHostToDevice));
+  return p.release();
+}
+
 static void destroy_problem(Problem* p) {
   if (!p) return;
   {
@@ -546,4 +587,5 @@ static void destroy_problem(Problem* p) {
 namespace rwb {
 Problem* problem_create(const double* rtt, int n, int hint, int device) { return create_problem(rtt, n, hint, device); }
 void problem_destroy(Problem* p) { destroy_problem(p); }
+Problem* problem_replica(const Problem& src, int device) { return replica_problem(src, device); }
 }  // namespace rwb
