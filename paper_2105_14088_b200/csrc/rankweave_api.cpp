@@ -406,7 +406,10 @@ double bcube_cost(const CostMatrix& m, const RankOrder& o, const CollectiveSpec&
 }
 
 double evaluate(const CostMatrix& m, const RankOrder& order, const CollectiveSpec& spec) {
-  check_inputs(m, order, spec);
+  // rw_evaluate applies check_inputs (cost_model.cpp:13-19) itself, in the
+  // same order and wording (spec, matrix size, permutation); only the entry
+  // count is checked here, after the spec and size, as the reference does.
+  if (order.size() != spec.n) check_inputs(m, order, spec);
   return gpu_evaluate(m, order, spec);
 }
 

@@ -127,6 +127,17 @@ PYBIND11_MODULE(_rankweave_cpp, mod) {
       .def_readwrite("external_model_path", &rw::TwoStageOptions::external_model_path)
       .def_readwrite("log", &rw::TwoStageOptions::log);
 
+  py::class_<rw::GpuOptions>(mod, "GpuOptions")
+      .def(py::init<>())
+      .def_readwrite("device", &rw::GpuOptions::device)
+      .def_readwrite("chains", &rw::GpuOptions::chains)
+      .def_readwrite("exact_batch", &rw::GpuOptions::exact_batch)
+      .def_readwrite("immutable_matrices", &rw::GpuOptions::immutable_matrices)
+      .def_readwrite("num_devices", &rw::GpuOptions::num_devices);
+  mod.def("set_gpu_options", &rw::set_gpu_options);
+  mod.def("gpu_options", &rw::gpu_options);
+  mod.def("sample_orders", &rw::sample_orders);
+
   mod.def("validate", py::overload_cast<const rw::CostMatrix&>(&rw::validate));
   mod.def("validate", py::overload_cast<const rw::CollectiveSpec&>(&rw::validate));
   mod.def("evaluate", &rw::evaluate, py::arg("m"), py::arg("order"), py::arg("spec"),

@@ -1111,6 +1111,7 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   smem_attr(init, dyn);
   init<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
   RW_CUDA(cudaGetLastError());
+  const uint64_t setup_evals = evals;  // T0 / calibration samples, before the chains start
   evals += (uint64_t)chains;
 
   auto ring = smem_mat ? k_anneal_ring<T, true> : k_anneal_ring<T, false>;
@@ -1159,6 +1160,7 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   res.evaluations = evals;
   res.chain = wi;
   res.levels_run = level;
+  res.setup_evaluations = setup_evals;
   return res;
 }
 

@@ -1099,10 +1099,28 @@ void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perm
     }
   };
   const size_t u16_bytes = fmt == 0 ? align16((size_t)n * 2) : 0;  // per order, packed only
+  if (batch * row <= (64 << 10) && fmt != 0 && p.path == RW_PATH_AUTO) {
+    // tiny batches (single evaluate() calls): zero-copy.  The orders are
+    // copied into mapped pinned memory that the kernel reads over PCIe, and
+    // the kernel writes the costs back there: one launch, one synchronisation,
+    // no copy operations on the stream.
+    cudaStream_t st = c.stream[0];
+    const size_t pb = align16((size_t)(batch * row));
+    char* h = static_cast<char*>(c.pinned(pb + (size_t)batch * 8));
+    char* dh = static_cast<char*>(c.d_pin);
+    std::memcpy(h, hp, (size_t)(batch * row));
+    launch_evaluate(p, plan, dh, eval_bytes, batch, reinterpret_cast<double*>(dh + pb), exact, validate, c.d_err, st,
+                    2);
+    if (validate) raise(st);  // synchronises st
+    else RW_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(costs, h + pb, (size_t)batch * 8);
+    finish();
+    return;
+  }
   if (batch * (int64_t)n <= (1 << 16)) {
-    // small batches (single evaluate() calls): orders and costs go through a
-    // pinned staging buffer (a pageable copy is a synchronous staged copy in
-    // the driver), one stream, one synchronisation
+    // small batches: orders and costs go through the pinned staging buffer
+    // (a pageable copy is a synchronous staged copy in the driver), one
+    // stream, one synchronisation
     cudaStream_t st = c.stream[0];
     const size_t pb = align16((size_t)(batch * row));
     const size_t ub = align16(u16_bytes * batch);

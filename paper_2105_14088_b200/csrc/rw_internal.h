@@ -128,7 +128,8 @@ struct ThreadCtx {
   int* h_err = nullptr;  // pinned
   void* d_buf[8] = {};
   size_t d_cap[8] = {};
-  void* h_pin = nullptr;  // pinned host staging for small synchronous calls
+  void* h_pin = nullptr;  // pinned, mapped host staging for small synchronous calls
+  void* d_pin = nullptr;  // its device alias
   size_t h_cap = 0;
   void* scratch(int slot, size_t bytes);
   void* pinned(size_t bytes);
@@ -198,6 +199,7 @@ struct AnnealResult {
   int levels = 0;
   int levels_run = 0;    // temperature levels completed within the budget
   double t0 = 0.0;
+  uint64_t setup_evaluations = 0;  // T0 / calibration samples (identical on every shard)
 };
 AnnealResult anneal_device(Problem& p, const EvalPlan& plan, const rw_solver_config& cfg, const rw_gpu_config& gpu);
 void local_search_device(Problem& p, const EvalPlan& plan, int32_t* perms, int64_t batch, int max_rounds,

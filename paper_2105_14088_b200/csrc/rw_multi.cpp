@@ -426,7 +426,16 @@ AnnealResult anneal_set(ProblemSet& s, const rw_spec& spec, const rw_solver_conf
     sync_all(s);
     out.cost = r.min_cost;
     out.chain = static_cast<int64_t>(r.min_key);
-    out.evaluations = r.evals_sum;
+    // every shard draws the same T0 / calibration samples (seeded by the
+    // solver seed alone); count them once, as one device does
+    uint64_t dup = 0;
+    int active = 0;
+    for (const auto& x : res)
+      if (!x.order.empty()) {
+        dup = x.setup_evaluations;
+        ++active;
+      }
+    out.evaluations = r.evals_sum - (active > 1 ? dup * static_cast<uint64_t>(active - 1) : 0);
   } else {
     out = res[0];
   }

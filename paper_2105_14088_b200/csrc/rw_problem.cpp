@@ -97,7 +97,10 @@ void* ThreadCtx::pinned(size_t bytes) {
       h_pin = nullptr;
     }
     const size_t cap = std::max<size_t>(bytes + bytes / 2, 64 * 1024);
-    RW_CUDA(cudaMallocHost(&h_pin, cap));
+    // mapped: small calls let the kernel read the orders and write the costs
+    // here directly (zero-copy), without separate copy operations
+    RW_CUDA(cudaHostAlloc(&h_pin, cap, cudaHostAllocMapped | cudaHostAllocPortable));
+    RW_CUDA(cudaHostGetDevicePointer(&d_pin, h_pin, 0));
     h_cap = cap;
   }
   return h_pin;

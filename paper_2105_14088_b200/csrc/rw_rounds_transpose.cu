@@ -83,6 +83,8 @@ struct RRouteArgs {
   int key_bytes;    // 4 or 8
   unsigned long long zero_key;
   int aligned;      // order rows are 16-byte aligned
+  int slots;        // partner slots per host: rounds, or ceil(rounds / 2) when paired
+  int paired;       // symmetric matrix, xor pairing: one slot per round pair (below)
 };
 
 // Stages one order into shared memory as uint16 (vectorised when the row is
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
   const int chunks8 = n >> 3;
   const int cshift = 31 - __clz(chunks8);
   const int rshift = 31 - __clz(a.R);
-  const int items = a.rounds << cshift;
+  const int items = a.slots << cshift;
   const bool aligned = a.aligned != 0;
   for (int64_t o = blockIdx.x; o < a.count; o += gridDim.x) {
     __syncthreads();  // the previous order's readers of p / pos are done
@@ -163,29 +165,53 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
       if (__syncthreads_or(bad) && threadIdx.x == 0) report_bad_order(a.err, n, a.base + o);
     }
     for (int w = threadIdx.x; w < items; w += blockDim.x) {
-      const int r = w >> cshift;
+      const int r = w >> cshift;  // round, or round pair when a.paired
       const int c = w & (chunks8 - 1);
       const int s = 1 << r;
       const uint4 q4 = pos4[c];
       const uint32_t js[4] = {q4.x, q4.y, q4.z, q4.w};
       uint32_t outw[4];
+      if (a.paired) {
+        // Round pair (2r, 2r+1), symmetric matrix: the four hosts at positions
+        // with bits (2r+1, 2r) = 00, 01, 10, 11 of an aligned group form two
+        // pairs per round; 00 and 11 own the round-2r pairs (00,01), (10,11),
+        // 01 and 10 own the round-(2r+1) pairs (01,11), (00,10).  Every pair
+        // is looked up exactly once (c(a,b) == c(b,a)) and every host holds
+        // exactly one lookup; bit 15 tags round 2r+1.  A lone last round
+        // (odd round count) keeps both directions (max is unchanged).
+        const int r0 = 2 * r;
+        const bool lone = r0 + 1 >= a.rounds;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t j0 = js[k] & 0xFFFFu, j1 = js[k] >> 16;
-        uint32_t v0, v1;
-        if (a.xor_pairing) {
-          v0 = p[j0 ^ s];
-          v1 = p[j1 ^ s];
-        } else {
-          v0 = (int)j0 < half ? (uint32_t)p[j0 + s] : 0xFFFFu;
-          v1 = (int)j1 < half ? (uint32_t)p[j1 + s] : 0xFFFFu;
+        for (int k = 0; k < 4; ++k) {
+          uint32_t v[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t j = e ? (js[k] >> 16) : (js[k] & 0xFFFFu);
+            const uint32_t b0 = (j >> r0) & 1u, b1 = (j >> (r0 + 1)) & 1u;
+            const bool second = !lone && b0 != b1;
+            v[e] = second ? ((uint32_t)p[j ^ (2u << r0)] | 0x8000u) : (uint32_t)p[j ^ (1u << r0)];
+          }
+          outw[k] = v[0] | (v[1] << 16);
         }
-        outw[k] = v0 | (v1 << 16);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t j0 = js[k] & 0xFFFFu, j1 = js[k] >> 16;
+          uint32_t v0, v1;
+          if (a.xor_pairing) {
+            v0 = p[j0 ^ s];
+            v1 = p[j1 ^ s];
+          } else {
+            v0 = (int)j0 < half ? (uint32_t)p[j0 + s] : 0xFFFFu;
+            v1 = (int)j1 < half ? (uint32_t)p[j1 + s] : 0xFFFFu;
+          }
+          outw[k] = v0 | (v1 << 16);
+        }
       }
       const int h0 = c << 3;
       const int b = h0 >> rshift;
       const int s0 = h0 & (a.R - 1);
-      *reinterpret_cast<uint4*>(out + (((size_t)b * a.rounds + r) * a.count + o) * a.R + s0) =
+      *reinterpret_cast<uint4*>(out + (((size_t)b * a.slots + r) * a.count + o) * a.R + s0) =
           make_uint4(outw[0], outw[1], outw[2], outw[3]);
     }
   }
@@ -198,7 +224,8 @@ constexpr int kRThreads = 1024;  // 31 consumer warps + 1 producer warp
 struct RScoreArgs {
   int64_t count;
   int n;
-  int rounds;
+  int rounds;    // partner slots per host (round pairs when kPaired)
+  int nrounds;   // reduction rounds (keys rows)
   int nblocks;
   int stages;   // ring depth
   int stage_orders;  // orders per stage (a multiple of 32)
@@ -208,7 +235,7 @@ struct RScoreArgs {
 // kAll: every host is a source (xor pairing), so the route wrote no
 // sentinels and every partner is < n (stage_order_vec masks entries into
 // range): the per-lookup range test is dropped.
-template <typename T, int R, bool kAll>
+template <typename T, int R, bool kAll, bool kPaired>
 __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, const uint16_t* __restrict__ buf,
                                                                const T* __restrict__ gmat) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -284,7 +311,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
             k -= cnt;
           }
           const uint4* q4 = reinterpret_cast<const uint4*>(sp + ((size_t)r * kRStageOrders + k) * R);
-          K key = KeyOf<T>::enc(T(0));
+          const K zero = KeyOf<T>::enc(T(0));
+          K key = zero, key1 = zero;
 #pragma unroll
           for (int c = 0; c < R / 8; ++c) {
             const uint4 q = q4[c];
@@ -292,13 +320,20 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
               const uint32_t col = (h & 1) ? (w[h >> 1] >> 16) : (w[h >> 1] & 0xFFFFu);
-              if (kAll || col < (uint32_t)n) {
+              if constexpr (kPaired) {
+                // bit 15 tags the second round of the pair (partners < 2^15)
+                const K v = KeyOf<T>::enc(blk[(c * 8 + h) * n + (col & 0x7FFFu)]);
+                if (col & 0x8000u) key1 = v > key1 ? v : key1;
+                else key = v > key ? v : key;
+              } else if (kAll || col < (uint32_t)n) {
                 const K v = KeyOf<T>::enc(blk[(c * 8 + h) * n + col]);
                 key = v > key ? v : key;
               }
             }
           }
-          if (key != KeyOf<T>::enc(T(0))) atomicMax(keys + (size_t)r * a.count + o0 + k, key);
+          const int r0 = kPaired ? 2 * r : r;
+          if (key != zero) atomicMax(keys + (size_t)r0 * a.count + o0 + k, key);
+          if (kPaired && key1 != zero) atomicMax(keys + (size_t)(r0 + 1) * a.count + o0 + k, key1);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
@@ -334,18 +369,19 @@ __global__ void k_rounds_finalize(RFinalArgs a, const void* __restrict__ keys_v,
 
 template <typename T, int R>
 void launch_score(const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat, cudaStream_t st,
-                  bool all) {
-  auto k = all ? k_rounds_score<T, R, true> : k_rounds_score<T, R, false>;
+                  bool all, bool paired) {
+  auto k = paired ? k_rounds_score<T, R, true, true>
+                  : (all ? k_rounds_score<T, R, true, false> : k_rounds_score<T, R, false, false>);
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, kRThreads, smem, st>>>(sa, buf, static_cast<const T*>(mat));
 }
 
 template <typename T>
 void launch_score_r(int R, const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat,
-                    cudaStream_t st, bool all) {
-  if (R == 32) launch_score<T, 32>(sa, grid, smem, buf, mat, st, all);
-  else if (R == 16) launch_score<T, 16>(sa, grid, smem, buf, mat, st, all);
-  else launch_score<T, 8>(sa, grid, smem, buf, mat, st, all);
+                    cudaStream_t st, bool all, bool paired) {
+  if (R == 32) launch_score<T, 32>(sa, grid, smem, buf, mat, st, all, paired);
+  else if (R == 16) launch_score<T, 16>(sa, grid, smem, buf, mat, st, all, paired);
+  else launch_score<T, 8>(sa, grid, smem, buf, mat, st, all, paired);
 }
 
 }  // namespace
@@ -356,6 +392,10 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   if (plan.model != kHalvingDoubling || n < 512 || n > 16384 || (n & (n - 1)) != 0 || batch <= 0) return false;
   const int rounds = plan.rounds;
   if (rounds < 1 || rounds > 14) return false;
+  // Symmetric matrix + xor pairing: one partner slot per host per round pair
+  // (half the lookups and half the exchange buffer, see k_rounds_route).
+  const bool paired = plan.pairing == RW_PAIRING_XOR && p.symmetric && rounds >= 2;
+  const int slots = paired ? (rounds + 1) / 2 : rounds;
   int sms = 148, optin = 227 * 1024;
   RW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
   RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
@@ -367,7 +407,7 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   int R = 0, stages = 2, kRStageOrders = 0;
   for (int cand : {32, 16, 8}) {
     const size_t mat = al16((size_t)cand * n * esz);
-    const size_t per_order = (size_t)rounds * cand * 2;
+    const size_t per_order = (size_t)slots * cand * 2;
     if (mat + 2 * 64 * per_order <= budget) {
       R = cand;
       kRStageOrders = (int)std::min<size_t>(256, (budget - mat) / (2 * per_order)) & ~31;
@@ -376,10 +416,10 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   }
   if (!R) return false;
   const int nblocks = n / R;
-  const size_t score_smem = al16((size_t)R * n * esz) + (size_t)stages * kRStageOrders * rounds * R * 2;
+  const size_t score_smem = al16((size_t)R * n * esz) + (size_t)stages * kRStageOrders * slots * R * 2;
   const size_t route_smem = 2 * al16((size_t)n * 2);
 
-  const int64_t per_order_bytes = (int64_t)2 * rounds * n;
+  const int64_t per_order_bytes = (int64_t)2 * slots * n;
   // Partner-buffer size: every score CTA restages ~2.5 row blocks per chunk,
   // so chunks of >= 4096 orders keep that below a quarter of the partner
   // traffic (measured on B200: 48 MB -> 7.8e6, 384 MB -> 1.14e7 evals/s at
@@ -411,19 +451,20 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   for (int64_t off = 0; off < batch; off += kmax) {
     const int64_t cnt_o = std::min(kmax, batch - off);
     RRouteArgs ra{cnt_o, off, n, rounds, plan.pairing == RW_PAIRING_XOR ? 1 : 0, R,
-                  reinterpret_cast<unsigned long long*>(err_slot), keys, key_bytes, zero_key, 0};
+                  reinterpret_cast<unsigned long long*>(err_slot), keys, key_bytes, zero_key, 0, slots,
+                  paired ? 1 : 0};
     const int rgrid = (int)std::min<int64_t>(cnt_o, (int64_t)sms * 8);
     const char* perms = static_cast<const char*>(d_perms) + (size_t)off * n * perm_bytes;
     ra.aligned = (reinterpret_cast<uintptr_t>(perms) & 15) == 0 ? 1 : 0;
     void* args[] = {&ra, (void*)&perms, (void*)&buf};
     RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), args, route_smem, st));
-    RScoreArgs sa{cnt_o, n, rounds, nblocks, stages, kRStageOrders, keys};
+    RScoreArgs sa{cnt_o, n, slots, rounds, nblocks, stages, kRStageOrders, keys};
     const bool xor_all = plan.pairing == RW_PAIRING_XOR;
     const int sgrid = (int)std::min<int64_t>(sms, nblocks * ((cnt_o + kRStageOrders - 1) / kRStageOrders));
     switch (p.storage) {
-      case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all); break;
-      case RW_STORAGE_F32: launch_score_r<float>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all); break;
-      default: launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all); break;
+      case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired); break;
+      case RW_STORAGE_F32: launch_score_r<float>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired); break;
+      default: launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired); break;
     }
     RW_CUDA(cudaGetLastError());
     fa.count = cnt_o;

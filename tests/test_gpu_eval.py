@@ -658,3 +658,33 @@ def test_host_wire_layouts_agree(port, n):
         prob.evaluate_batch_packed(spec, rw.api.pack_orders(bad, bits), bits, 5)
     with pytest.raises(rw.DomainError):
         prob.evaluate_batch(spec, bad.astype(np.uint16))
+
+
+@pytest.mark.parametrize("n,kind", [(512, "u16"), (2048, "u16"), (1024, "f32"), (4096, "f64")])
+def test_hd_xor_round_pairs_on_symmetric_matrices(port, n, kind):
+    """Symmetric matrix + xor pairing: the transpose path looks every pair up
+    once, one slot per host per round pair (rw_rounds_transpose.cu); odd round
+    counts (n = 512, 2048) keep a lone last round.  Bit-equal to the L2-gather
+    path and the oracle."""
+    rng = np.random.default_rng(n + 7)
+    if kind == "u16":
+        a = rng.integers(0, 4000, size=(n, n)).astype(np.float64) / 16.0
+    elif kind == "f32":
+        a = rng.random((n, n)).astype(np.float32).astype(np.float64) * 64.0
+    else:
+        a = rng.random((n, n)) * 100.0
+    m = np.triu(a, 1) + np.triu(a, 1).T
+    probs = {}
+    for pth in ("l2", "transpose"):
+        probs[pth] = rw.Problem(m)
+        probs[pth].set_path(pth)
+    assert probs["transpose"].info["symmetric"] == 1
+    perms = np.array([rng.permutation(n) for _ in range(200)], dtype=np.int32)
+    for mode in (1, 0):
+        spec = rw.CollectiveSpec(rw.Algorithm.HalvingDoubling, n, 2.0 ** 20, 2, rw.CostMode(mode),
+                                 rw.HdPairing.XorPairing)
+        want = port.evaluate_batch(m, perms[:30], make_spec(1, n, 2.0 ** 20, 2, mode, 1))
+        got_t = probs["transpose"].evaluate_batch(spec, perms)
+        got_l = probs["l2"].evaluate_batch(spec, perms)
+        assert np.array_equal(got_t[:30], want), mode
+        assert np.array_equal(got_t, got_l), mode
