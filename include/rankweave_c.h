@@ -90,7 +90,7 @@ typedef struct rw_solver_config {
 
 /* GPU extension of the search configuration (not in the reference). */
 typedef struct rw_gpu_config {
-  int32_t chains;       /* SA chains on this call; <= 0: one per restart */
+  int32_t chains;       /* SA chains on this call; <= 0: max(restarts, 4 x SMs) */
   int32_t chain_begin;  /* global id of the first chain (multi-GPU sharding) */
   int32_t chain_total;  /* total chains across all ranks (<= 0: chains) */
   int32_t schedule;     /* temperatures when initial_temperature <= 0:
@@ -98,7 +98,7 @@ typedef struct rw_gpu_config {
                                costs, floor T0 * 1e-6; solver.cpp:152-167);
                            1 = calibrated (ring): T0 = 0.1 x mean uphill 2-opt
                                delta of random orders, floor = 5th-percentile
-                               uphill delta / 7; the calibration samples are
+                               uphill delta / 20; the calibration samples are
                                counted as evaluations */
   int64_t max_proposals;/* total evaluation budget of the call (T0/calibration
                            samples + chain starts + proposals); the steps per

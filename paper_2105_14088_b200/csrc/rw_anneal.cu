@@ -1244,6 +1244,7 @@ void sample_orders_device(int n, int64_t samples, uint64_t seed, uint16_t* d_out
 }
 
 AnnealResult anneal_device(Problem& p, const EvalPlan& plan, const rw_solver_config& cfg, const rw_gpu_config& gpu) {
+  NvtxRange nvtx("K4 anneal");
   switch (p.storage) {
     case RW_STORAGE_U16: return anneal_typed<uint16_t>(p, plan, cfg, gpu);
     case RW_STORAGE_F32: return anneal_typed<float>(p, plan, cfg, gpu);
@@ -1254,6 +1255,7 @@ AnnealResult anneal_device(Problem& p, const EvalPlan& plan, const rw_solver_con
 void local_search_device(Problem& p, const EvalPlan& plan, int32_t* perms, int64_t batch, int max_rounds,
                          double* costs, uint64_t* evals) {
   if (batch <= 0) return;
+  NvtxRange nvtx("K3 local search");
   switch (p.storage) {
     case RW_STORAGE_U16: local_search_typed<uint16_t>(p, plan, perms, batch, max_rounds, costs, evals); break;
     case RW_STORAGE_F32: local_search_typed<float>(p, plan, perms, batch, max_rounds, costs, evals); break;

@@ -375,6 +375,7 @@ void unrank(const rw_spec& s, uint64_t index, int32_t* perm) {
 
 void brute_force_range(const Problem& p, const EvalPlan& plan, uint64_t first, uint64_t count, double* cost_out,
                        uint64_t* index_out) {
+  NvtxRange nvtx("K2 exhaustive range");
   DeviceGuard g(p.device);
   ThreadCtx& c = thread_ctx(p.device);
   cudaStream_t st = c.stream[0];

@@ -105,6 +105,7 @@ rw_status rw_validate_spec(const rw_spec* spec) {
 
 rw_status rw_problem_create(const double* rtt_us, int32_t n, int32_t storage_hint, int32_t device, rw_problem** out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_problem_create");
     need(out, "out");
     *out = nullptr;
     need(rtt_us, "rtt_us");
@@ -153,6 +154,7 @@ rw_status rw_problem_set_path(rw_problem* p, int32_t path) {
 
 rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* perm, double* cost) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_evaluate");
     need(spec, "spec");
     need(perm, "perm");
     need(cost, "cost");
@@ -166,6 +168,7 @@ rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* p
 rw_status rw_evaluate_batch(const rw_problem* p, const rw_spec* spec, const int32_t* perms, int64_t batch,
                             double* costs, uint32_t flags, rw_eval_report* report) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_evaluate_batch");
     need(spec, "spec");
     if (batch < 0) rwb::fail_domain("batch must be >= 0");
     if (batch > 0) {
@@ -182,6 +185,7 @@ rw_status rw_evaluate_batch(const rw_problem* p, const rw_spec* spec, const int3
 rw_status rw_evaluate_batch_u16(const rw_problem* p, const rw_spec* spec, const uint16_t* perms, int64_t batch,
                                 double* costs, uint32_t flags, rw_eval_report* report) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_evaluate_batch_u16");
     need(spec, "spec");
     if (batch < 0) rwb::fail_domain("batch must be >= 0");
     if (batch > 0) {
@@ -230,6 +234,7 @@ rw_status rw_pack_orders(const int32_t* perms, int32_t n, int64_t batch, int32_t
 rw_status rw_evaluate_batch_packed(const rw_problem* p, const rw_spec* spec, const void* packed, int32_t bits,
                                    int64_t batch, double* costs, uint32_t flags, rw_eval_report* report) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_evaluate_batch_packed");
     need(spec, "spec");
     if (batch < 0) rwb::fail_domain("batch must be >= 0");
     if (batch > 0) {
@@ -248,6 +253,7 @@ rw_status rw_evaluate_batch_packed(const rw_problem* p, const rw_spec* spec, con
 rw_status rw_evaluate_batch_device(const rw_problem* p, const rw_spec* spec, const void* d_perms, int32_t perm_bytes,
                                    int64_t batch, double* d_costs, void* stream, uint32_t flags) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_evaluate_batch_device");
     need(spec, "spec");
     if (batch < 0) rwb::fail_domain("batch must be >= 0");
     if (batch > 0) {
@@ -305,6 +311,7 @@ rw_status rw_brute_force_space(const rw_spec* spec, uint64_t* count_out) {
 rw_status rw_brute_force(const rw_problem* p, const rw_spec* spec, int32_t threshold, int32_t* perm_out,
                          double* cost_out, uint64_t* evals_out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_brute_force");
     need(spec, "spec");
     need(perm_out, "perm_out");
     need(cost_out, "cost_out");
@@ -328,6 +335,7 @@ rw_status rw_brute_force(const rw_problem* p, const rw_spec* spec, int32_t thres
 rw_status rw_brute_force_range(const rw_problem* p, const rw_spec* spec, uint64_t first, uint64_t count,
                                double* cost_out, uint64_t* index_out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_brute_force_range");
     need(spec, "spec");
     need(cost_out, "cost_out");
     need(index_out, "index_out");
@@ -353,6 +361,7 @@ rw_status rw_unrank(const rw_spec* spec, uint64_t index, int32_t* perm_out) {
 rw_status rw_anneal(const rw_problem* p, const rw_spec* spec, const rw_solver_config* cfg, const rw_gpu_config* gpu,
                     int32_t* perm_out, double* cost_out, uint64_t* evals_out, rw_search_report* report) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_anneal");
     const auto t_start = std::chrono::steady_clock::now();
     need(spec, "spec");
     need(cfg, "cfg");
@@ -388,6 +397,7 @@ rw_status rw_anneal(const rw_problem* p, const rw_spec* spec, const rw_solver_co
 rw_status rw_local_search(const rw_problem* p, const rw_spec* spec, int32_t* perms_inout, int64_t batch,
                           int32_t max_rounds, double* costs_out, uint64_t* evals_out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_local_search");
     need(spec, "spec");
     if (batch < 0) rwb::fail_domain("batch must be >= 0");
     if (batch > 0) {
@@ -424,6 +434,7 @@ rw_status rw_sample_orders(int32_t n, int32_t samples, uint64_t seed, int32_t* p
 // in one batch with the reference-identical (sorted, serial) ring summation.
 rw_status rw_sample_costs(const rw_problem* p, const rw_spec* spec, int32_t samples, uint64_t seed, double* costs_out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_sample_costs");
     need(spec, "spec");
     if (samples < 1) rwb::fail_domain("sample_orders: need at least 1 sample");
     need(costs_out, "costs_out");
@@ -515,6 +526,7 @@ rw_status rw_simulate_batch(const rw_problem* p, int32_t nlevels, const int32_t*
                             const double* oversub, const rw_spec* spec, const int32_t* perms, int64_t batch,
                             double* out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_simulate_batch");
     need(fanout, "fanout");
     need(bandwidth, "bandwidth");
     need(oversub, "oversub");
@@ -670,6 +682,7 @@ rw_status rw_two_stage_solve(const double* rtt_us, int32_t n, const rw_spec* spe
 rw_status rw_problem_set_create(const double* rtt_us, int32_t n, int32_t storage_hint, const int32_t* devices,
                                 int32_t ndevices, rw_problem_set** out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_problem_set_create");
     need(out, "out");
     *out = nullptr;
     need(rtt_us, "rtt_us");
@@ -724,6 +737,7 @@ rw_status rw_problem_set_member(const rw_problem_set* s, int32_t index, rw_probl
 rw_status rw_evaluate_batch_set(const rw_problem_set* s, const rw_spec* spec, const void* perms, int32_t layout,
                                 int32_t bits, int64_t batch, double* costs, uint32_t flags) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_evaluate_batch_set");
     need(spec, "spec");
     if (batch < 0) rwb::fail_domain("batch must be >= 0");
     if (batch > 0) {
@@ -744,6 +758,7 @@ rw_status rw_evaluate_batch_set(const rw_problem_set* s, const rw_spec* spec, co
 rw_status rw_brute_force_set(const rw_problem_set* s, const rw_spec* spec, int32_t threshold, int32_t* perm_out,
                              double* cost_out, uint64_t* evals_out) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_brute_force_set");
     need(spec, "spec");
     need(perm_out, "perm_out");
     need(cost_out, "cost_out");
@@ -761,6 +776,7 @@ rw_status rw_anneal_set(const rw_problem_set* s, const rw_spec* spec, const rw_s
                         const rw_gpu_config* gpu, int32_t* perm_out, double* cost_out, uint64_t* evals_out,
                         rw_search_report* report) {
   return guarded([&] {
+    rwb::NvtxRange nvtx_("rw_anneal_set");
     const auto t_start = std::chrono::steady_clock::now();
     need(spec, "spec");
     need(cfg, "cfg");

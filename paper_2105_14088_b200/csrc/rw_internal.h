@@ -12,9 +12,22 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "rankweave_c.h"
 
 namespace rwb {
+
+// NVTX range around a host-side phase (K1 scoring launches, K2 exhaustive
+// search, K3 local search, K4 annealing, and every C ABI entry point), so an
+// nsys / ncu --nvtx timeline shows which call issued which kernels.  Header-
+// only NVTX v3: a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- errors ----
 struct Failure : std::runtime_error {

@@ -46,6 +46,10 @@ def main():
     A = rw.Algorithm
     if which in ("ring", "all"):
         score(torch, rw, "C4", "fixed", lambda n, s: rw.CollectiveSpec(A.Ring, n, s), 1 << 18)
+    if which in ("ring_f32", "all"):
+        score(torch, rw, "C4", "f32", lambda n, s: rw.CollectiveSpec(A.Ring, n, s), 1 << 18)
+    if which in ("ring_f64", "all"):
+        score(torch, rw, "C4", "f64", lambda n, s: rw.CollectiveSpec(A.Ring, n, s), 1 << 18)
     if which in ("hdxor", "all"):
         score(torch, rw, "C5", "fixed",
               lambda n, s: rw.CollectiveSpec(A.HalvingDoubling, n, s, 2, rw.CostMode.LatencyTimesSize,
