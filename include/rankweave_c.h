@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define RW_ABI_VERSION 1
+#define RW_ABI_VERSION 2  /* 2: uint16 / packed host orders, device sets (NCCL), host logic, Philox samplers */
 
 typedef enum rw_status {
   RW_OK = 0,

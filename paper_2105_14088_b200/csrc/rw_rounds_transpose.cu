@@ -140,8 +140,11 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
   const int n = a.n;
   uint16_t* p = reinterpret_cast<uint16_t*>(smem);
   uint16_t* pos = reinterpret_cast<uint16_t*>(smem + al16((size_t)n * 2));
-  const uint4* pos4 = reinterpret_cast<const uint4*>(pos);
-  for (int k = threadIdx.x; k < n; k += blockDim.x) pos[k] = 0;
+  uint4* pos4 = reinterpret_cast<uint4*>(pos);
+  // pos starts (and is reset to) the 0xFFFF sentinel: a host no position
+  // names keeps it, which is how a repeated host (the bijection check) shows.
+  const uint4 none = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  for (int k = threadIdx.x; k < (n >> 3); k += blockDim.x) pos4[k] = none;
   const int half = n >> 1;
   const int chunks8 = n >> 3;
   const int cshift = 31 - __clz(chunks8);
@@ -160,15 +163,16 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) pos[p[i]] = (uint16_t)i;
     __syncthreads();
-    if (kValidate) {
-      for (int h = threadIdx.x; h < n; h += blockDim.x) bad |= p[pos[h]] != h;
-      if (__syncthreads_or(bad) && threadIdx.x == 0) report_bad_order(a.err, n, a.base + o);
-    }
+    const uint32_t jmask = (uint32_t)(n - 1) * 0x10001u;  // keeps sentinel positions in range
     for (int w = threadIdx.x; w < items; w += blockDim.x) {
       const int r = w >> cshift;  // round, or round pair when a.paired
       const int c = w & (chunks8 - 1);
       const int s = 1 << r;
-      const uint4 q4 = pos4[c];
+      uint4 q4 = pos4[c];
+      // valid positions are < n (a power of two): any bit outside n-1 is the
+      // sentinel of a host no position names, i.e. a repeated host elsewhere
+      if (r == 0 && ((q4.x | q4.y | q4.z | q4.w) & ~jmask) != 0) bad = true;
+      q4 = make_uint4(q4.x & jmask, q4.y & jmask, q4.z & jmask, q4.w & jmask);
       const uint32_t js[4] = {q4.x, q4.y, q4.z, q4.w};
       uint32_t outw[4];
       if (a.paired) {
@@ -188,8 +192,8 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
           for (int e = 0; e < 2; ++e) {
             const uint32_t j = e ? (js[k] >> 16) : (js[k] & 0xFFFFu);
             const uint32_t b0 = (j >> r0) & 1u, b1 = (j >> (r0 + 1)) & 1u;
-            const bool second = !lone && b0 != b1;
-            v[e] = second ? ((uint32_t)p[j ^ (2u << r0)] | 0x8000u) : (uint32_t)p[j ^ (1u << r0)];
+            const uint32_t second = lone ? 0u : (b0 ^ b1);
+            v[e] = (uint32_t)p[j ^ ((1u + second) << r0)] | (second << 15);  // one gather
           }
           outw[k] = v[0] | (v[1] << 16);
         }
@@ -214,6 +218,9 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
       *reinterpret_cast<uint4*>(out + (((size_t)b * a.slots + r) * a.count + o) * a.R + s0) =
           make_uint4(outw[0], outw[1], outw[2], outw[3]);
     }
+    __syncthreads();  // every reader of pos is done: reset it to the sentinel
+    for (int k = threadIdx.x; k < (n >> 3); k += blockDim.x) pos4[k] = none;
+    if (kValidate && __syncthreads_or(bad) && threadIdx.x == 0) report_bad_order(a.err, n, a.base + o);
   }
 }
 
