@@ -83,6 +83,12 @@ struct Problem {
   int nb_k = 0;
   std::mutex mu;
   std::unique_ptr<DbtPlan> dbt;
+  // Max-based models on FP64 storage: the order-preserving rank of every
+  // entry among the matrix's distinct values (u32, half the bytes of FP64)
+  // and the rank -> value table; built lazily on the device (rw_rounds_transpose.cu).
+  uint32_t* d_rank = nullptr;
+  double* d_rank_vals = nullptr;
+  uint32_t zero_rank = 0;
   size_t elem_bytes() const { return storage == RW_STORAGE_U16 ? 2 : storage == RW_STORAGE_F32 ? 4 : 8; }
 };
 

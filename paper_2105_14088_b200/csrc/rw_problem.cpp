@@ -580,6 +580,8 @@ static void destroy_problem(Problem* p) {
     if (p->d_err) cudaFree(p->d_err);
     if (p->dbt && p->dbt->d_all) cudaFree(p->dbt->d_all);
     if (p->d_nb) cudaFree(p->d_nb);
+    if (p->d_rank) cudaFree(p->d_rank);
+    if (p->d_rank_vals) cudaFree(p->d_rank_vals);
   }
   delete p;
 }

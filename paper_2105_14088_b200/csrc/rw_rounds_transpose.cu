@@ -24,10 +24,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
 #include "rw_tma.cuh"
+
+#include <cub/cub.cuh>
 
 namespace rwb {
 
@@ -46,6 +50,12 @@ struct KeyOf<uint16_t> {
   using type = unsigned int;
   __device__ static unsigned int enc(uint16_t v) { return v; }
   __device__ static uint16_t dec(unsigned int k) { return (uint16_t)k; }
+};
+template <>
+struct KeyOf<uint32_t> {  // ranks of FP64 values (order-preserving as integers)
+  using type = unsigned int;
+  __device__ static unsigned int enc(uint32_t v) { return v; }
+  __device__ static uint32_t dec(unsigned int k) { return k; }
 };
 template <>
 struct KeyOf<float> {
@@ -374,6 +384,91 @@ __global__ void k_rounds_finalize(RFinalArgs a, const void* __restrict__ keys_v,
   costs[o] = total;
 }
 
+// Rank finalize: the round's maximum rank decodes to its FP64 value through
+// the sorted distinct values, then the reference's fl(max * bytes_r) sum.
+__global__ void k_rounds_finalize_ranks(RFinalArgs a, const unsigned int* __restrict__ keys,
+                                        const double* __restrict__ vals, double* __restrict__ costs) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= a.count) return;
+  double total = 0.0;
+  for (int r = 0; r < a.rounds; ++r) {
+    double v = vals[keys[(size_t)r * a.count + o]];
+    if (a.mode == RW_LATENCY_TIMES_SIZE) v = __dmul_rn(v, a.bytes[r]);
+    total = __dadd_rn(total, v);
+  }
+  costs[o] = total;
+}
+
+// ---------------------------------------------------------- rank transform --
+// v -> the value whose rank represents it: NaN never wins the reference's
+// running max (std::max from 0, cost_model.cpp:83) and -0.0 == 0.0, so both
+// map to +0.0, which is always in the table.
+__device__ __forceinline__ double rank_value(double v) { return (v != v || v == 0.0) ? 0.0 : v; }
+
+__global__ void k_rank_prepare(const double* __restrict__ m, int64_t nn, double* __restrict__ out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nn; k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = k < nn ? rank_value(m[k]) : 0.0;
+}
+
+__global__ void k_rank_assign(const double* __restrict__ m, int64_t nn, const double* __restrict__ uniq,
+                              const int* __restrict__ count, uint32_t* __restrict__ rank) {
+  const int cnt = *count;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += (int64_t)gridDim.x * blockDim.x) {
+    const double v = rank_value(m[k]);
+    int lo = 0, hi = cnt - 1;  // v is in the table: exact lower_bound
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (uniq[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    rank[k] = (uint32_t)lo;
+  }
+}
+
+// Builds Problem::d_rank / d_rank_vals (FP64 storage): sort + unique of the
+// sanitised entries (cub), then one binary search per entry.  Exact: a
+// round's maximum rank is the rank of its maximum value.
+void ensure_ranks(Problem& p, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(p.mu);
+  if (p.d_rank) return;
+  const int64_t nn = (int64_t)p.n * p.n;
+  double *d_in = nullptr, *d_sorted = nullptr, *d_uniq = nullptr;
+  int* d_cnt = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp_sort = 0, tmp_uniq = 0;
+  RW_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_sort, d_in, d_sorted, (int)(nn + 1)));
+  RW_CUDA(cub::DeviceSelect::Unique(nullptr, tmp_uniq, d_sorted, d_uniq, d_cnt, (int)(nn + 1)));
+  RW_CUDA(cudaMalloc(&d_in, (size_t)(nn + 1) * 8));
+  RW_CUDA(cudaMalloc(&d_sorted, (size_t)(nn + 1) * 8));
+  RW_CUDA(cudaMalloc(&d_uniq, (size_t)(nn + 1) * 8));
+  RW_CUDA(cudaMalloc(&d_cnt, sizeof(int)));
+  RW_CUDA(cudaMalloc(&d_tmp, std::max(tmp_sort, tmp_uniq)));
+  uint32_t* d_rank = nullptr;
+  RW_CUDA(cudaMalloc(&d_rank, (size_t)nn * 4));
+  const double* m = static_cast<const double*>(p.d_mat);
+  k_rank_prepare<<<148 * 8, 256, 0, st>>>(m, nn, d_in);
+  RW_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, tmp_sort, d_in, d_sorted, (int)(nn + 1), 0, 64, st));
+  RW_CUDA(cub::DeviceSelect::Unique(d_tmp, tmp_uniq, d_sorted, d_uniq, d_cnt, (int)(nn + 1), st));
+  k_rank_assign<<<148 * 8, 256, 0, st>>>(m, nn, d_uniq, d_cnt, d_rank);
+  RW_CUDA(cudaGetLastError());
+  int cnt = 0;
+  RW_CUDA(cudaMemcpyAsync(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RW_CUDA(cudaStreamSynchronize(st));
+  std::vector<double> uniq((size_t)cnt);
+  RW_CUDA(cudaMemcpy(uniq.data(), d_uniq, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
+  double* d_vals = nullptr;
+  RW_CUDA(cudaMalloc(&d_vals, (size_t)cnt * 8));
+  RW_CUDA(cudaMemcpy(d_vals, uniq.data(), (size_t)cnt * 8, cudaMemcpyHostToDevice));
+  p.zero_rank = (uint32_t)(std::lower_bound(uniq.begin(), uniq.end(), 0.0) - uniq.begin());
+  cudaFree(d_in);
+  cudaFree(d_sorted);
+  cudaFree(d_uniq);
+  cudaFree(d_cnt);
+  cudaFree(d_tmp);
+  p.d_rank_vals = d_vals;
+  p.d_rank = d_rank;
+}
+
 template <typename T, int R>
 void launch_score(const RScoreArgs& sa, int grid, size_t smem, const uint16_t* buf, const void* mat, cudaStream_t st,
                   bool all, bool paired) {
@@ -407,7 +502,12 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   RW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
   RW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device));
   const size_t budget = (size_t)std::min(optin, 227 * 1024) - 1024;
-  const size_t esz = p.elem_bytes();
+  // FP64 rows do not fit a row block of 8 at N=4096 (256 KB): max-based
+  // scoring runs on the u32 ranks of the entries instead (exact, see
+  // ensure_ranks), which halves the bytes per lookup.
+  const bool ranks = p.storage == RW_STORAGE_F64 && n >= 2048;
+  if (ranks) ensure_ranks(const_cast<Problem&>(p), st);
+  const size_t esz = ranks ? 4 : p.elem_bytes();
   // Largest row block that leaves room for two stages of >= 64 orders; the
   // rest of shared memory becomes two stages of up to 256 orders (larger bulk
   // copies and fewer hand-offs, as measured for the ring score).
@@ -445,7 +545,7 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   void* keys = c.scratch(slot + 1, (size_t)rounds * kmax * key_bytes);
   unsigned long long zero_key = 0;
   if (p.storage == RW_STORAGE_F32) zero_key = 0x80000000ull;
-  if (p.storage == RW_STORAGE_F64) zero_key = 0x8000000000000000ull;
+  if (p.storage == RW_STORAGE_F64) zero_key = ranks ? p.zero_rank : 0x8000000000000000ull;
 
   auto route = validate ? (perm_bytes == 2 ? (void*)k_rounds_route<uint16_t, true> : (void*)k_rounds_route<int32_t, true>)
                         : (perm_bytes == 2 ? (void*)k_rounds_route<uint16_t, false> : (void*)k_rounds_route<int32_t, false>);
@@ -471,7 +571,10 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
     switch (p.storage) {
       case RW_STORAGE_U16: launch_score_r<uint16_t>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired); break;
       case RW_STORAGE_F32: launch_score_r<float>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired); break;
-      default: launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired); break;
+      default:
+        if (ranks) launch_score_r<uint32_t>(R, sa, sgrid, score_smem, buf, p.d_rank, st, xor_all, paired);
+        else launch_score_r<double>(R, sa, sgrid, score_smem, buf, p.d_mat, st, xor_all, paired);
+        break;
     }
     RW_CUDA(cudaGetLastError());
     fa.count = cnt_o;
@@ -479,7 +582,12 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
     switch (p.storage) {
       case RW_STORAGE_U16: k_rounds_finalize<uint16_t><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
       case RW_STORAGE_F32: k_rounds_finalize<float><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
-      default: k_rounds_finalize<double><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
+      default:
+        if (ranks)
+          k_rounds_finalize_ranks<<<fgrid, 128, 0, st>>>(fa, static_cast<const unsigned int*>(keys), p.d_rank_vals,
+                                                         d_costs + off);
+        else k_rounds_finalize<double><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off);
+        break;
     }
     RW_CUDA(cudaGetLastError());
   }

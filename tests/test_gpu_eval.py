@@ -688,3 +688,36 @@ def test_hd_xor_round_pairs_on_symmetric_matrices(port, n, kind):
         got_l = probs["l2"].evaluate_batch(spec, perms)
         assert np.array_equal(got_t[:30], want), mode
         assert np.array_equal(got_t, got_l), mode
+
+
+@pytest.mark.parametrize("sym", [False, True])
+def test_hd_f64_rank_transform_beyond_shared_memory(port, sym):
+    """FP64 matrices at N >= 2048 score halving-doubling on the u32 ranks of
+    their entries (rw_rounds_transpose.cu ensure_ranks): exact, including the
+    reference's running std::max from +0.0 (cost_model.cpp:83) -- NaN never
+    wins, negatives and -0.0 never beat 0, +inf does.  Both pairings, both
+    cost modes, against the L2-gather path and the oracle."""
+    n = 2048
+    rng = np.random.default_rng(2048 + sym)
+    a = rng.random((n, n)) * 50.0
+    a[rng.random((n, n)) < 0.01] = np.nan
+    a[rng.random((n, n)) < 0.05] *= -1.0
+    a[rng.random((n, n)) < 0.01] = -0.0
+    a[5, 9] = np.inf
+    m = (np.triu(a, 1) + np.triu(a, 1).T) if sym else a
+    if sym:
+        m[np.isnan(m)] = 0.25  # triu + triu.T spreads NaN; keep the matrix symmetric and NaN-free
+    probs = {}
+    for pth in ("l2", "transpose"):
+        probs[pth] = rw.Problem(m)
+        probs[pth].set_path(pth)
+    assert probs["transpose"].info["storage"] == 3
+    perms = np.array([rng.permutation(n) for _ in range(40)], dtype=np.int32)
+    for pair in (0, 1):
+        for mode in (1, 0):
+            spec = rw.CollectiveSpec(rw.Algorithm.HalvingDoubling, n, 1e6, 2, rw.CostMode(mode), rw.HdPairing(pair))
+            want = port.evaluate_batch(m, perms[:12], make_spec(1, n, 1e6, 2, mode, pair))
+            got_t = probs["transpose"].evaluate_batch(spec, perms)
+            got_l = probs["l2"].evaluate_batch(spec, perms)
+            np.testing.assert_array_equal(got_t[:12], want)
+            np.testing.assert_array_equal(got_t, got_l)
