@@ -30,6 +30,7 @@
 // sum over hosts h of rtt[h][pred(h)] is the same multiset of hops.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "rw_device.cuh"
 #include "rw_internal.h"
@@ -487,7 +488,11 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
   // L2-resident; measured in bench.py on B200 at N=1024 (evals/s):
   // 48 MB 4.85e8, 96 MB 5.07e8, 128 MB 5.30e8, 256 MB 5.45e8, 512 MB 5.55e8,
   // 1 GB 5.59e8.  Scratch only grows to min(batch, chunk) orders.
-  const int64_t chunk = std::max<int64_t>(4096, ((int64_t)512 << 20) / ((int64_t)n * 2));
+  static const int64_t chunk_bytes = [] {
+    const char* e = std::getenv("RW_RING_CHUNK_MB");  // A/B measurements only
+    return e ? std::max(8L, std::atol(e)) << 20 : (int64_t)512 << 20;
+  }();
+  const int64_t chunk = std::max<int64_t>(4096, chunk_bytes / ((int64_t)n * 2));
   ThreadCtx& c = thread_ctx(p.device);
   const int64_t kmax = std::min(batch, chunk);
   uint16_t* predbuf = static_cast<uint16_t*>(c.scratch(slot, (size_t)nblocks * kmax * R * 2));
