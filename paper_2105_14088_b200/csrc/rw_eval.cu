@@ -358,6 +358,89 @@ __global__ void __launch_bounds__(1024) k_rounds(KArgs a, RoundsArgs r, const P*
   }
 }
 
+// ---------------------------------- K1: double tree, one CTA per order ----
+// Matrices beyond shared memory (N >= 1024): a CTA scores one order at a time
+// with its edge values in shared memory (32 KB at N=4096 in the exact
+// integer form), so the depth-by-depth recursion (cost_model.cpp:94-116)
+// reads children from shared memory and 8 warps share each depth's matrix
+// gathers; the per-warp form keeps a single warp on the whole order and
+// spills the edge values to L2.  The operation sequence per edge and the
+// final max over the top edges are those of warp_dbt_cost, so the result is
+// bit-identical.
+template <typename T, typename P, bool kValidate>
+__global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __restrict__ perms,
+                                                 const T* __restrict__ mat, double* __restrict__ costs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n, E = d.edges;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem);
+  uint8_t* flags = smem + align16((size_t)n * 2);
+  unsigned char* vbase = flags + align16((size_t)n);
+  const bool im = d.int_mode != 0;
+  uint32_t* iv = reinterpret_cast<uint32_t*>(vbase);
+  double* dv = reinterpret_cast<double*>(vbase);
+  __shared__ int s_bad;
+  const uint32_t nmask = (uint32_t)(n - 1);  // n is a power of two for the tree model
+  for (int k = threadIdx.x; k < n; k += blockDim.x) flags[k] = 0;
+  uint8_t marker = 0;
+  for (int64_t o = blockIdx.x; o < a.batch; o += gridDim.x) {
+    marker = marker == 255 ? 1 : marker + 1;
+    if (marker == 1) {  // wrapped: clear stale markers
+      __syncthreads();
+      for (int k = threadIdx.x; k < n; k += blockDim.x) flags[k] = 0;
+    }
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    bool bad = false;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t v = (uint32_t)ld_order<P>(perms + o * n, i);
+      bad |= v > nmask;
+      p[i] = (uint16_t)(v & nmask);
+      if (kValidate) flags[v & nmask] = marker;
+    }
+    __syncthreads();
+    if (kValidate)
+      for (int h = threadIdx.x; h < n; h += blockDim.x) bad |= flags[h] != marker;
+    if (bad) s_bad = 1;
+    for (int depth = d.depths - 1; depth >= 0; --depth) {
+      const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
+#pragma unroll 2
+      for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        const int src = __ldg(d.src + e), dst = __ldg(d.dst + e), ch = __ldg(d.c0 + e);
+        const T raw = ld_matrix<T>(mat, (size_t)p[src] * n + p[dst]);
+        if (im) {
+          uint32_t sub = 0;
+          if (ch >= 0) {
+            const uint32_t x = iv[ch], y = iv[__ldg(d.c1 + e)];
+            sub = x > y ? x : y;
+          }
+          iv[e] = (uint32_t)raw + sub;
+        } else {
+          double c = to_double(raw, a.scale);
+          if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+          const double sub = ch >= 0 ? ref_max(dv[ch], dv[__ldg(d.c1 + e)]) : 0.0;
+          dv[e] = __dadd_rn(c, sub);
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const int top = __ldg(d.depth_off + 1);
+      double best;
+      if (im) {
+        uint32_t b = iv[0];
+        for (int e = 1; e < top; ++e) b = iv[e] > b ? iv[e] : b;
+        best = __dmul_rn((double)b, d.w);
+      } else {
+        best = dv[0];
+        for (int e = 1; e < top; ++e) best = ref_max(best, dv[e]);
+      }
+      costs[o] = best;
+      if (kValidate && s_bad) report_bad_order(a.err, n, o);
+    }
+    (void)E;
+  }
+}
+
 // -------------------------------------------------- K1: double tree -------
 template <typename T, typename P, bool kSmem, bool kValidate>
 __global__ void __launch_bounds__(1024) k_dbt(KArgs a, DbtArgs d, const P* __restrict__ perms,
@@ -887,6 +970,20 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
     d.half = plan.half;
     d.int_mode = plan.dbt_int ? 1 : 0;
     d.w = plan.dbt_w;
+    // Beyond shared memory: one CTA per order with the edge values in shared
+    // memory (k_dbt_cta), when a batch has enough orders to fill the SMs.
+    const size_t cta_smem = align16((size_t)n * 2) + align16((size_t)n) +
+                            (size_t)edges * (plan.dbt_int && std::is_same<T, uint16_t>::value ? 4 : 8);
+    if (!smem_mat && n >= 1024 && batch >= 2 * (int64_t)dp.sms && 2 * cta_smem <= budget) {
+      auto kc = validate ? k_dbt_cta<T, P, true> : k_dbt_cta<T, P, false>;
+      set_smem(kc, cta_smem);
+      int per_sm = 0;
+      RW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, 256, cta_smem));
+      const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)dp.sms * std::max(1, per_sm)));
+      kc<<<cgrid, 256, cta_smem, st>>>(a, d, d_perms, gmat, d_costs);
+      RW_CUDA(cudaGetLastError());
+      return;
+    }
     if (a.val_stride == 0 && n > 1) {
       ThreadCtx& c = thread_ctx(p.device);
       d.gvals = static_cast<double*>(c.scratch(slot, (size_t)grid * warps_per_block * edges * 8));

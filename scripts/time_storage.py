@@ -29,12 +29,17 @@ def main():
         "ring": (0, 0),
         "hd-xor": (1, 1),
         "hd-paper": (1, 0),
+        "dbt": (2, 0),
+        "bcube8": (3, 0),
     }
     cases = []
     for kind in ("fixed", "f32", "f64"):
         cases.append(("C4", "ring", kind, 1 << 20))
         cases.append(("C5", "hd-xor", kind, 1 << 15))
         cases.append(("C5", "hd-paper", kind, 1 << 15))
+        cases.append(("C4", "dbt", kind, 1 << 17))
+        cases.append(("C5", "dbt", kind, 1 << 15))
+        cases.append(("C5", "bcube8", kind, 1 << 15))
     only = sys.argv[1:]
     names = {1: "u16", 2: "f32", 3: "f64"}
     for cfg, model, kind, count in cases:
@@ -45,7 +50,8 @@ def main():
         n = m.shape[0]
         size = rw.fixtures.size_for(kind)
         alg, pair = models[model]
-        spec = rw.CollectiveSpec(A(alg), n, size, 2, rw.CostMode.LatencyTimesSize, P(pair))
+        b = 8 if model == "bcube8" else 2
+        spec = rw.CollectiveSpec(A(alg), n, size, b, rw.CostMode.LatencyTimesSize, P(pair))
         prob = rw.Problem(m)
         g = torch.Generator(device="cuda")
         g.manual_seed(5)
@@ -57,7 +63,7 @@ def main():
         torch.cuda.synchronize()
         prob.sync_errors()
         rows = o[:4].cpu().numpy().view(np.uint16).astype(np.int32)
-        want = port.evaluate_batch(m, rows, make_spec(alg, n, size, 2, 1, pair))
+        want = port.evaluate_batch(m, rows, make_spec(alg, n, size, b, 1, pair))
         got = c[:4].cpu().numpy()
         rel = float(np.max(np.abs(got - want) / np.abs(want)))
         reps = 5

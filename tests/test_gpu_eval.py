@@ -721,3 +721,28 @@ def test_hd_f64_rank_transform_beyond_shared_memory(port, sym):
             got_l = probs["l2"].evaluate_batch(spec, perms)
             np.testing.assert_array_equal(got_t[:12], want)
             np.testing.assert_array_equal(got_t, got_l)
+
+
+@pytest.mark.parametrize("cfg,kind", [("C4", "fixed"), ("C4", "f64"), ("C5", "fixed"), ("C5", "f32")])
+def test_dbt_cta_kernel_large_batches(port, cfg, kind):
+    """The double binary tree beyond shared memory: batches that fill the SMs
+    take one CTA per order with the edge values in shared memory (k_dbt_cta);
+    small batches the per-warp kernel.  Both must give the oracle's bits, in
+    the exact integer form (u16) and the FP64 sequence (f32 / f64)."""
+    m = fixtures.config_matrix(cfg, kind)
+    n = m.shape[0]
+    prob = rw.Problem(m)
+    size = fixtures.size_for(kind)
+    rng = np.random.default_rng(n + len(kind))
+    perms = np.array([rng.permutation(n) for _ in range(400)], dtype=np.int32)
+    for mode in (1, 0):
+        spec = rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, n, size, 2, rw.CostMode(mode))
+        big = prob.evaluate_batch(spec, perms)                       # k_dbt_cta
+        small = np.concatenate([prob.evaluate_batch(spec, perms[k:k + 50]) for k in range(0, 400, 50)])  # per warp
+        assert np.array_equal(big, small), mode
+        want = port.evaluate_batch(m, perms[:10], make_spec(2, n, size, 2, mode, 0))
+        assert np.array_equal(big[:10], want), mode
+    bad = perms.copy()
+    bad[333, 3] = bad[333, 4]
+    with pytest.raises(rw.DomainError, match="batch entry 333"):
+        prob.evaluate_batch(rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, n, size), bad)
