@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(1024) k_rounds(KArgs a, RoundsArgs r, const P*
 }
 
 // ---------------------------------- K1: double tree, one CTA per order ----
-// Matrices beyond shared memory (N >= 1024): a CTA scores one order at a time
+// Matrices beyond shared memory (N >= 2048): a CTA scores one order at a time
 // with its edge values in shared memory (32 KB at N=4096 in the exact
 // integer form), so the depth-by-depth recursion (cost_model.cpp:94-116)
 // reads children from shared memory and 8 warps share each depth's matrix
@@ -974,7 +974,7 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
     // memory (k_dbt_cta), when a batch has enough orders to fill the SMs.
     const size_t cta_smem = align16((size_t)n * 2) + align16((size_t)n) +
                             (size_t)edges * (plan.dbt_int && std::is_same<T, uint16_t>::value ? 4 : 8);
-    if (!smem_mat && n >= 1024 && batch >= 2 * (int64_t)dp.sms && 2 * cta_smem <= budget) {
+    if (!smem_mat && n >= 2048 && batch >= 2 * (int64_t)dp.sms && 2 * cta_smem <= budget) {
       auto kc = validate ? k_dbt_cta<T, P, true> : k_dbt_cta<T, P, false>;
       set_smem(kc, cta_smem);
       int per_sm = 0;

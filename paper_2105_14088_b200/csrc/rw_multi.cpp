@@ -278,8 +278,9 @@ ProblemSet* problem_set_create(const double* rtt, int n, int hint, const int* de
     for (int i = 0; i < k; ++i) s->workers.push_back(std::make_unique<MemberWorker>(devs[static_cast<size_t>(i)]));
     if (k > 1) {
       const NcclApi& api = nccl();
-      s->comms.resize(static_cast<size_t>(k));
-      nccl_check(api.commInitAll(s->comms.data(), k, devs.data()), "comm init");
+      std::vector<ncclComm_t> comms(static_cast<size_t>(k));
+      nccl_check(api.commInitAll(comms.data(), k, devs.data()), "comm init");
+      s->comms = std::move(comms);  // only initialised communicators are ever destroyed
       // replicate the device matrix from member 0 over NVLink
       nccl_check(api.groupStart(), "group start");
       for (int i = 0; i < k; ++i) {
@@ -292,7 +293,7 @@ ProblemSet* problem_set_create(const double* rtt, int n, int hint, const int* de
       sync_all(*s);
     }
   } catch (...) {
-    for (Problem* m : s->members) problem_destroy(m);
+    problem_set_destroy(s.release());  // workers, communicators, streams, buffers, members
     throw;
   }
   return s.release();

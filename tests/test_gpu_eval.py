@@ -723,13 +723,15 @@ def test_hd_f64_rank_transform_beyond_shared_memory(port, sym):
             np.testing.assert_array_equal(got_t, got_l)
 
 
-@pytest.mark.parametrize("cfg,kind", [("C4", "fixed"), ("C4", "f64"), ("C5", "fixed"), ("C5", "f32")])
+@pytest.mark.parametrize("cfg,kind", [("C5h", "fixed"), ("C5h", "f64"), ("C5", "fixed"), ("C5", "f32")])
 def test_dbt_cta_kernel_large_batches(port, cfg, kind):
     """The double binary tree beyond shared memory: batches that fill the SMs
     take one CTA per order with the edge values in shared memory (k_dbt_cta);
     small batches the per-warp kernel.  Both must give the oracle's bits, in
     the exact integer form (u16) and the FP64 sequence (f32 / f64)."""
-    m = fixtures.config_matrix(cfg, kind)
+    m = fixtures.config_matrix(cfg[:2], kind)
+    if cfg == "C5h":  # C5 truncated to 2048 hosts
+        m = np.ascontiguousarray(m[:2048, :2048])
     n = m.shape[0]
     prob = rw.Problem(m)
     size = fixtures.size_for(kind)
