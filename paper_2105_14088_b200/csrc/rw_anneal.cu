@@ -948,10 +948,7 @@ int fill_model_args(AnnealArgs& a, const EvalPlan& plan) {
   }
   if (plan.model == kDoubleBinaryTree && plan.dbt) {
     dbt_edges = plan.dbt->edges;
-    a.dbt.src = plan.dbt->d_src();
-    a.dbt.dst = plan.dbt->d_dst();
-    a.dbt.c0 = plan.dbt->d_c0();
-    a.dbt.c1 = plan.dbt->d_c1();
+    a.dbt.rec = plan.dbt->d_rec();
     a.dbt.depth_off = plan.dbt->d_depth_off();
     a.dbt.depths = plan.dbt->depths;
     a.dbt.edges = dbt_edges;

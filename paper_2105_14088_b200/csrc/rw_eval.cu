@@ -405,19 +405,19 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
       const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
 #pragma unroll 2
       for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-        const int src = __ldg(d.src + e), dst = __ldg(d.dst + e), ch = __ldg(d.c0 + e);
-        const T raw = ld_matrix<T>(mat, (size_t)p[src] * n + p[dst]);
+        const int4 r = __ldg(d.rec + e);  // {src, dst, c0, c1}
+        const T raw = ld_matrix<T>(mat, (size_t)p[r.x] * n + p[r.y]);
         if (im) {
           uint32_t sub = 0;
-          if (ch >= 0) {
-            const uint32_t x = iv[ch], y = iv[__ldg(d.c1 + e)];
+          if (r.z >= 0) {
+            const uint32_t x = iv[r.z], y = iv[r.w];
             sub = x > y ? x : y;
           }
           iv[e] = (uint32_t)raw + sub;
         } else {
           double c = to_double(raw, a.scale);
           if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-          const double sub = ch >= 0 ? ref_max(dv[ch], dv[__ldg(d.c1 + e)]) : 0.0;
+          const double sub = r.z >= 0 ? ref_max(dv[r.z], dv[r.w]) : 0.0;
           dv[e] = __dadd_rn(c, sub);
         }
       }
@@ -959,10 +959,7 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
     kern<<<grid, threads, dyn, st>>>(a, d_perms, gmat, plan.ring_mul, d_costs);
   } else if (model == kDoubleBinaryTree) {
     DbtArgs d{};
-    d.src = plan.dbt->d_src();
-    d.dst = plan.dbt->d_dst();
-    d.c0 = plan.dbt->d_c0();
-    d.c1 = plan.dbt->d_c1();
+    d.rec = plan.dbt->d_rec();
     d.depth_off = plan.dbt->d_depth_off();
     d.depths = plan.dbt->depths;
     d.edges = edges;

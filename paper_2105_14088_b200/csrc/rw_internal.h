@@ -57,11 +57,9 @@ struct DbtPlan {
   int edges = 0;
   int depths = 0;
   std::vector<int32_t> h_src, h_dst, h_c0, h_c1, h_depth_off;
-  int32_t* d_all = nullptr;  // [src | dst | c0 | c1 | depth_off]
-  const int32_t* d_src() const { return d_all; }
-  const int32_t* d_dst() const { return d_all + edges; }
-  const int32_t* d_c0() const { return d_all + 2 * edges; }
-  const int32_t* d_c1() const { return d_all + 3 * edges; }
+  // [edge records {src, dst, c0, c1} (one 16-byte load per edge) | depth_off]
+  int32_t* d_all = nullptr;
+  const int4* d_rec() const { return reinterpret_cast<const int4*>(d_all); }
   const int32_t* d_depth_off() const { return d_all + 4 * edges; }
 };
 

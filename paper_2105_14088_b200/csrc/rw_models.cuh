@@ -25,10 +25,7 @@ struct RoundsArgs {
 };
 
 struct DbtArgs {
-  const int32_t* src;
-  const int32_t* dst;
-  const int32_t* c0;
-  const int32_t* c1;
+  const int4* rec;  // per edge {src, dst, c0, c1}: positions and child edges (-1: none)
   const int32_t* depth_off;
   int depths;
   int edges;
@@ -41,28 +38,21 @@ struct DbtArgs {
   double w;        // int_mode: value = sum * w
 };
 
-// Plan arrays (src | dst | c0 | c1 | depth_off, int32) in shared memory:
-// 16 B per edge.  All threads of the CTA call it before any early exit.
+// Plan (edge records {src, dst, c0, c1} | depth_off, int32) in shared memory:
+// 16 B per edge, one LDS.128 per edge.  All threads of the CTA call it before any early exit.
 __host__ __device__ inline size_t dbt_plan_bytes(int edges, int depths) {
   return ((size_t)4 * edges + depths + 1) * 4 + 16;
 }
 __device__ __forceinline__ void stage_dbt_plan(DbtArgs& d, unsigned char* smem) {
   if (!d.stage_plan) return;
-  int32_t* s = reinterpret_cast<int32_t*>(smem + d.plan_off);
+  int4* r = reinterpret_cast<int4*>(smem + d.plan_off);
   const int E = d.edges;
-  for (int k = threadIdx.x; k < E; k += blockDim.x) {
-    s[k] = d.src[k];
-    s[E + k] = d.dst[k];
-    s[2 * E + k] = d.c0[k];
-    s[3 * E + k] = d.c1[k];
-  }
-  for (int k = threadIdx.x; k <= d.depths; k += blockDim.x) s[4 * E + k] = d.depth_off[k];
+  for (int k = threadIdx.x; k < E; k += blockDim.x) r[k] = d.rec[k];
+  int32_t* off = reinterpret_cast<int32_t*>(r + E);
+  for (int k = threadIdx.x; k <= d.depths; k += blockDim.x) off[k] = d.depth_off[k];
   __syncthreads();
-  d.src = s;
-  d.dst = s + E;
-  d.c0 = s + 2 * E;
-  d.c1 = s + 3 * E;
-  d.depth_off = s + 4 * E;
+  d.rec = r;
+  d.depth_off = off;
 }
 
 // Sum over rounds of the round maximum (cost_model.cpp:71-92, 118-138).
@@ -114,11 +104,11 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
         const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 4
         for (int e = lo + lane; e < hi; e += 32) {
-          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[d.src[e]], s_perm[d.dst[e]]);
-          const int ch = d.c0[e];
+          const int4 r = d.rec[e];
+          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
           uint32_t sub = 0;
-          if (ch >= 0) {
-            const uint32_t x = iv[ch], y = iv[d.c1[e]];
+          if (r.z >= 0) {
+            const uint32_t x = iv[r.z], y = iv[r.w];
             sub = x > y ? x : y;
           }
           iv[e] = c + sub;
@@ -136,11 +126,11 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
     const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 4
     for (int e = lo + lane; e < hi; e += 32) {
-      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[d.src[e]], s_perm[d.dst[e]]), scale);
+      const int4 r = d.rec[e];
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
       if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-      const int ch = d.c0[e];
       // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
-      const double sub = ch >= 0 ? ref_max(vals[ch], vals[d.c1[e]]) : 0.0;
+      const double sub = r.z >= 0 ? ref_max(vals[r.z], vals[r.w]) : 0.0;
       vals[e] = __dadd_rn(c, sub);
     }
     __syncwarp();

@@ -253,7 +253,8 @@ static void build_dbt_plan(DbtPlan& plan, int n) {
   }
   std::vector<int32_t> all;
   all.reserve(4 * plan.edges + plan.depths + 1);
-  for (auto* v : {&plan.h_src, &plan.h_dst, &plan.h_c0, &plan.h_c1}) all.insert(all.end(), v->begin(), v->end());
+  for (int e = 0; e < plan.edges; ++e)
+    for (const auto* v : {&plan.h_src, &plan.h_dst, &plan.h_c0, &plan.h_c1}) all.push_back((*v)[static_cast<size_t>(e)]);
   all.insert(all.end(), plan.h_depth_off.begin(), plan.h_depth_off.end());
   RW_CUDA(cudaMalloc(&plan.d_all, all.size() * sizeof(int32_t)));
   RW_CUDA(cudaMemcpy(plan.d_all, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
