@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define RW_ABI_VERSION 2  /* 2: uint16 / packed host orders, device sets (NCCL), host logic, Philox samplers */
+#define RW_ABI_VERSION 2  /* 2: uint16 / packed host orders, device sets (NCCL), host logic, GPU options, Philox samplers */
 
 typedef enum rw_status {
   RW_OK = 0,
@@ -290,6 +290,19 @@ rw_status rw_brute_force_set(const rw_problem_set* s, const rw_spec* spec, int32
 rw_status rw_anneal_set(const rw_problem_set* s, const rw_spec* spec, const rw_solver_config* cfg,
                         const rw_gpu_config* gpu, int32_t* perm_out, double* cost_out, uint64_t* evals_out,
                         rw_search_report* report);
+
+/* rankweave::GpuOptions of the C++ drop-in (rankweave.hpp), process-wide:
+ * what evaluate / brute_force / anneal / two_stage_solve use when called
+ * through the reference's C++ API or rw_two_stage_solve. */
+typedef struct rw_gpu_options {
+  int32_t device;              /* -1: current CUDA device */
+  int32_t chains;              /* SA chains; <= 0: max(restarts, 4 x SMs) per device */
+  int32_t exact_batch;         /* evaluate_batch with the reference's summation order */
+  int32_t immutable_matrices;  /* cache device matrices by address, not content */
+  int32_t num_devices;         /* > 1 (0: all visible): device sets with in-process NCCL */
+} rw_gpu_options;
+rw_status rw_set_gpu_options(const rw_gpu_options* opts);
+rw_status rw_get_gpu_options(rw_gpu_options* out);
 
 /* ---- host logic (one implementation, shared with the C++ drop-in) ------ */
 /* distribution_stats (stats.cpp:64-81): out4 = {min, max, mean, stddev}. */

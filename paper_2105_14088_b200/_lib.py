@@ -52,6 +52,11 @@ class rw_search_report(C.Structure):
                 ("seconds", C.c_double)]
 
 
+class rw_gpu_options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("chains", C.c_int32), ("exact_batch", C.c_int32),
+                ("immutable_matrices", C.c_int32), ("num_devices", C.c_int32)]
+
+
 class rw_eval_report(C.Structure):
     _fields_ = [("bit_exact", C.c_int32), ("kernel", C.c_int32), ("kernel_ms", C.c_float),
                 ("lookups", C.c_int64)]
@@ -104,6 +109,8 @@ SIGNATURES = {
     "rw_brute_force_set": (C.c_int, [_vp, P(rw_spec), C.c_int32, _i32p, _dp, _u64p]),
     "rw_anneal_set": (C.c_int, [_vp, P(rw_spec), P(rw_solver_config), P(rw_gpu_config), _i32p, _dp, _u64p,
                                 P(rw_search_report)]),
+    "rw_set_gpu_options": (C.c_int, [P(rw_gpu_options)]),
+    "rw_get_gpu_options": (C.c_int, [P(rw_gpu_options)]),
     "rw_distribution_stats": (C.c_int, [_dp, C.c_int64, _dp]),
     "rw_spearman": (C.c_int, [_dp, _dp, C.c_int64, C.c_int64, _dp]),
     "rw_parse_model_file": (C.c_int, [C.c_char_p, C.c_int32, _i32p]),

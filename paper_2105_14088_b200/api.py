@@ -673,6 +673,24 @@ def spearman(xs, ys) -> float:
     return out.value
 
 
+def gpu_options() -> dict:
+    """The C++ drop-in's process-wide GpuOptions (rankweave.hpp), which
+    two_stage_solve uses: device, chains, exact_batch, immutable_matrices,
+    num_devices (> 1 or 0 = all: device sets with in-process NCCL)."""
+    o = _lib.rw_gpu_options()
+    check(lib.rw_get_gpu_options(C.byref(o)))
+    return {f: getattr(o, f) for f, _ in o._fields_}
+
+
+def set_gpu_options(**kw) -> None:
+    cur = gpu_options()
+    unknown = set(kw) - set(cur)
+    if unknown:
+        raise TypeError(f"unknown GPU options {sorted(unknown)}")
+    cur.update({k: int(v) for k, v in kw.items()})
+    check(lib.rw_set_gpu_options(C.byref(_lib.rw_gpu_options(**cur))))
+
+
 def packed_row_bytes(n: int, bits: int) -> int:
     r = int(lib.rw_packed_row_bytes(n, bits))
     if r < 0:

@@ -115,7 +115,10 @@ def cmd_solve(a) -> int:
                               api.CostMode.LatencyOnly if a.latency_only else api.CostMode.LatencyTimesSize)
     cfg = api.SolverConfig(budget=a.budget, seed=a.seed, brute_force_threshold=a.threshold)
     log = (lambda s: print(s, file=sys.stderr))
-    sol = api.two_stage_solve(m, spec, cfg, external_model_path=a.external_model or "", log=log)
+    if a.devices != 1:
+        api.set_gpu_options(num_devices=a.devices)
+    sol = api.two_stage_solve(m, spec, cfg, external_model_path=a.external_model or "", log=log,
+                              emit_smt_path=a.emit_smt or "")
     ident = api.evaluate(m, api.RankOrder.identity(m.n()), spec)
     ratio = ident / sol.cost if sol.cost > 0 else 1.0
     print(f"identity cost {ident:.6g}  solved cost {sol.cost:.6g}  improvement x{ratio:.4f}  "
@@ -210,6 +213,9 @@ def main(argv=None) -> int:
     s.add_argument("--threshold", type=int, default=10)
     s.add_argument("--latency-only", action="store_true")
     s.add_argument("--external-model", default="")
+    s.add_argument("--emit-smt", default="", help="write the stage-2 SMT-LIB encoding (bound: the stage-1 cost)")
+    s.add_argument("--devices", type=int, default=1,
+                   help="GPUs of this process for the search (0: all visible; in-process NCCL)")
     s.add_argument("--out", default="")
     r = sub.add_parser("reorder")
     r.add_argument("--hosts", required=True)

@@ -648,6 +648,32 @@ rw_status rw_emit_smtlib(const double* rtt_us, int32_t n, const rw_spec* spec, i
   });
 }
 
+rw_status rw_set_gpu_options(const rw_gpu_options* opts) {
+  return guarded([&] {
+    need(opts, "opts");
+    if (opts->num_devices < 0) rwb::fail_domain("num_devices must be >= 0");
+    rankweave::GpuOptions o;
+    o.device = opts->device;
+    o.chains = opts->chains;
+    o.exact_batch = opts->exact_batch != 0;
+    o.immutable_matrices = opts->immutable_matrices != 0;
+    o.num_devices = opts->num_devices;
+    rankweave::set_gpu_options(o);
+  });
+}
+
+rw_status rw_get_gpu_options(rw_gpu_options* out) {
+  return guarded([&] {
+    need(out, "out");
+    const rankweave::GpuOptions o = rankweave::gpu_options();
+    out->device = o.device;
+    out->chains = o.chains;
+    out->exact_batch = o.exact_batch ? 1 : 0;
+    out->immutable_matrices = o.immutable_matrices ? 1 : 0;
+    out->num_devices = o.num_devices;
+  });
+}
+
 rw_status rw_two_stage_solve(const double* rtt_us, int32_t n, const rw_spec* spec, const rw_solver_config* cfg,
                              const char* emit_smt_path, const char* external_model_path, rw_log_fn log, void* user,
                              int32_t* perm_out, double* cost_out, int32_t* method_out, uint64_t* evals_out) {

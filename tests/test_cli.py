@@ -68,3 +68,25 @@ def test_solve_end_to_end(tmp_path):
     sol = json.loads(out.read_text())
     assert sol["cost"] == 247.0 and sol["method"] == "BruteForce" and sol["evaluations"] == 40320
     assert cli.main(["solve", "--matrix", str(p), "--algo", "hd", "--size", "1"]) == 3  # N=9 not a power of 2
+
+
+@pytest.mark.gpu
+def test_solve_emits_smt_and_runs_on_a_device_set(tmp_path):
+    """cmd_solve with --emit-smt writes the reference's stage-2 file (bound = the
+    stage-1 cost) and --devices 0 runs the search over every visible GPU of the
+    process (in-process NCCL) with the same result."""
+    from paper_2105_14088_b200 import api
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "brute.json")))
+    m = np.array(g["matrix16_int"])[:9, :9]
+    p = tmp_path / "m.json"
+    p.write_text(json.dumps({"hosts": [f"h{i}" for i in range(9)], "rtt_us": m.tolist()}))
+    out, smt = tmp_path / "o.json", tmp_path / "s.smt2"
+    try:
+        assert cli.main(["solve", "--matrix", str(p), "--algo", "ring", "--size", "1", "--out", str(out),
+                         "--emit-smt", str(smt), "--devices", "0"]) == 0
+    finally:
+        api.set_gpu_options(num_devices=1)
+    sol = json.loads(out.read_text())
+    assert sol["cost"] == 247.0 and sol["method"] == "BruteForce"
+    text = smt.read_text()
+    assert api.balanced_sexpr(text) and "(assert (< cost 247.0))" in text
