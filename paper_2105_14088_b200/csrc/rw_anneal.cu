@@ -306,6 +306,18 @@ __device__ __forceinline__ void apply_move(uint16_t* p, int n, const Move& m, in
   __syncwarp();
 }
 
+// q = p within a warp's shared-memory order buffers (16-byte aligned): one
+// 16-byte move per lane and chunk instead of one 2-byte move per element.
+__device__ __forceinline__ void copy_order(uint16_t* q, const uint16_t* p, int n, int lane) {
+  if ((n & 7) == 0) {
+    uint4* q4 = reinterpret_cast<uint4*>(q);
+    const uint4* p4 = reinterpret_cast<const uint4*>(p);
+    for (int c = lane; c < (n >> 3); c += 32) q4[c] = p4[c];
+  } else {
+    for (int i = lane; i < n; i += 32) q[i] = p[i];
+  }
+}
+
 __device__ __forceinline__ void store_order(uint16_t* g, const uint16_t* s, int n, int lane) {
   if ((n & 7) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (reinterpret_cast<uintptr_t>(s) & 15) == 0) {
     for (int i = lane; i < (n >> 3); i += 32) reinterpret_cast<uint4*>(g)[i] = reinterpret_cast<const uint4*>(s)[i];
@@ -546,7 +558,7 @@ __global__ void __launch_bounds__(256) k_anneal_full(AnnealArgs a, const T* __re
       const uint4 r = rng.block();
       ++ctr;
       const Move m = draw_move_mix(r, n, a.mix_swap, a.mix_rev);
-      for (int i = lane; i < n; i += 32) q[i] = p[i];
+      copy_order(q, p, n, lane);
       __syncwarp();
       apply_move(q, n, m, lane);
       double c;
@@ -815,7 +827,7 @@ __global__ void __launch_bounds__(256) k_local_search_full(AnnealArgs a, const T
     for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = g[i];
     __syncthreads();
     if (wib == 0) {
-      for (int i = lane; i < n; i += 32) q[i] = p[i];
+      copy_order(q, p, n, lane);
       __syncwarp();
       const double c = full_cost<T, kSmem>(q, n, mat, a, vals, lane);
       if (lane == 0) s_cur = c;
@@ -833,7 +845,7 @@ __global__ void __launch_bounds__(256) k_local_search_full(AnnealArgs a, const T
         long long t = start + scanned + k;
         if (t >= total) t -= total;
         const Move m = unrank_pair_move(t, pairs, n);
-        for (int i = lane; i < n; i += 32) q[i] = p[i];
+        copy_order(q, p, n, lane);
         __syncwarp();
         apply_move(q, n, m, lane);
         const double c = full_cost<T, kSmem>(q, n, mat, a, vals, lane);
@@ -862,7 +874,7 @@ __global__ void __launch_bounds__(256) k_local_search_full(AnnealArgs a, const T
         const Move m = unrank_pair_move(bt, pairs, n);
         if (wib == 0) {
           apply_move(p, n, m, lane);
-          for (int i = lane; i < n; i += 32) q[i] = p[i];
+          copy_order(q, p, n, lane);
           __syncwarp();
           const double c = full_cost<T, kSmem>(q, n, mat, a, vals, lane);  // exact, no drift
           if (lane == 0) s_cur = c;
