@@ -401,32 +401,24 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
     if (kValidate)
       for (int h = threadIdx.x; h < n; h += blockDim.x) bad |= flags[h] != marker;
     if (bad) s_bad = 1;
-    // (1) every edge's own cost: all gathers independent; (2) the recursion
-    // per depth from shared memory (the two phases of warp_dbt_cost)
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      const int4 r = __ldg(d.rec + e);  // {src, dst, c0, c1}
-      const T raw = ld_matrix<T>(mat, (size_t)p[r.x] * n + p[r.y]);
-      if (im) {
-        iv[e] = (uint32_t)raw;
-      } else {
-        double c = to_double(raw, a.scale);
-        if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-        dv[e] = c;
-      }
-    }
-    __syncthreads();
     for (int depth = d.depths - 1; depth >= 0; --depth) {
       const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
+#pragma unroll 2
       for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-        const int4 r = __ldg(d.rec + e);
+        const int4 r = __ldg(d.rec + e);  // {src, dst, c0, c1}
+        const T raw = ld_matrix<T>(mat, (size_t)p[r.x] * n + p[r.y]);
         if (im) {
+          uint32_t sub = 0;
           if (r.z >= 0) {
             const uint32_t x = iv[r.z], y = iv[r.w];
-            iv[e] += x > y ? x : y;
+            sub = x > y ? x : y;
           }
+          iv[e] = (uint32_t)raw + sub;
         } else {
-          // leaves add T(empty) = +0.0 too (turns a -0.0 edge cost into +0.0, as the reference)
-          dv[e] = __dadd_rn(dv[e], r.z >= 0 ? ref_max(dv[r.z], dv[r.w]) : 0.0);
+          double c = to_double(raw, a.scale);
+          if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+          const double sub = r.z >= 0 ? ref_max(dv[r.z], dv[r.w]) : 0.0;
+          dv[e] = __dadd_rn(c, sub);
         }
       }
       __syncthreads();
@@ -445,6 +437,7 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
       costs[o] = best;
       if (kValidate && s_bad) report_bad_order(a.err, n, o);
     }
+    (void)E;
   }
 }
 

@@ -96,32 +96,22 @@ template <typename T, bool kSmem>
 __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d, double scale,
                                 double* vals, int lane) {
   if (n <= 1) return 0.0;
-  // Two phases.  (1) Every edge's own cost, for all edges at once: the
-  // lookups do not depend on the recursion, so they are all independent
-  // (full memory-level parallelism instead of one batch per depth).
-  // (2) The depth-by-depth recursion value = cost + max(children), leaves
-  // first, in place: one dependent shared-memory round per depth.  Per edge
-  // the operations are those of T(i, j) in cost_model.cpp:94-116, so the
-  // result is bit-identical to a single-pass evaluation.
-  const int E = d.edges;
   if constexpr (std::is_same<T, uint16_t>::value) {
     if (d.int_mode) {
       // exact integer form (EvalPlan::dbt_int): path sums of raw codes
       uint32_t* iv = reinterpret_cast<uint32_t*>(vals);
-#pragma unroll 4
-      for (int e = lane; e < E; e += 32) {
-        const int4 r = d.rec[e];
-        iv[e] = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
-      }
-      __syncwarp();
       for (int depth = d.depths - 1; depth >= 0; --depth) {
         const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 4
         for (int e = lo + lane; e < hi; e += 32) {
           const int4 r = d.rec[e];
+          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
+          uint32_t sub = 0;
           if (r.z >= 0) {
             const uint32_t x = iv[r.z], y = iv[r.w];
-            iv[e] += x > y ? x : y;
+            sub = x > y ? x : y;
           }
+          iv[e] = c + sub;
         }
         __syncwarp();
       }
@@ -132,21 +122,16 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
       return __dmul_rn((double)best, d.w);
     }
   }
-#pragma unroll 4
-  for (int e = lane; e < E; e += 32) {
-    const int4 r = d.rec[e];
-    double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
-    if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-    vals[e] = c;
-  }
-  __syncwarp();
   for (int depth = d.depths - 1; depth >= 0; --depth) {
     const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 4
     for (int e = lo + lane; e < hi; e += 32) {
       const int4 r = d.rec[e];
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
+      if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
       // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
       const double sub = r.z >= 0 ? ref_max(vals[r.z], vals[r.w]) : 0.0;
-      vals[e] = __dadd_rn(vals[e], sub);
+      vals[e] = __dadd_rn(c, sub);
     }
     __syncwarp();
   }
