@@ -593,6 +593,219 @@ __global__ void __launch_bounds__(256) k_anneal_full(AnnealArgs a, const T* __re
   }
 }
 
+// ------------------------------ full-evaluation anneal, CTA per chain -----
+// Few chains (an equal-budget run, a short solve): a chain is latency-bound
+// on one warp (ncu, profiles/r02_anneal_dbt_c3.txt: issue 15%, "wait" and
+// short-scoreboard stalls; ~890 instructions and ~5,900 cycles per
+// proposal), so kCta threads share each proposal's copy, move and full
+// evaluation.  The Philox stream, the move, the exact cost arithmetic and the
+// acceptance are those of k_anneal_full, so the trajectory -- and the result
+// -- is identical; only the time per proposal changes.
+constexpr int kCta = 128;
+
+__device__ __forceinline__ void cta_copy_order(uint16_t* q, const uint16_t* p, int n) {
+  if ((n & 7) == 0) {
+    uint4* q4 = reinterpret_cast<uint4*>(q);
+    const uint4* p4 = reinterpret_cast<const uint4*>(p);
+    for (int c = threadIdx.x; c < (n >> 3); c += kCta) q4[c] = p4[c];
+  } else {
+    for (int i = threadIdx.x; i < n; i += kCta) q[i] = p[i];
+  }
+}
+
+// apply_move for kCta threads (same permutation as the warp version).
+__device__ __forceinline__ void cta_apply_move(uint16_t* p, int n, const Move& m) {
+  const int t = threadIdx.x;
+  if (m.type < 0) return;
+  if (m.type == 0) {
+    if (t == 0) {
+      const uint16_t x = p[m.i];
+      p[m.i] = p[m.j];
+      p[m.j] = x;
+    }
+  } else if (m.type == 1) {  // absolute positions (non-ring models): reverse [i..j]
+    const int len = m.j - m.i + 1, half = len >> 1;
+    for (int q = t; q < half; q += kCta) {
+      const int a = m.i + q, b = m.i + len - 1 - q;
+      const uint16_t x = p[a], y = p[b];
+      p[a] = y;
+      p[b] = x;
+    }
+  } else {
+    const int s = m.i, len = m.j, k = m.k;  // len <= kOrWindow + 3 < kCta
+    uint16_t v = 0;
+    if (t < len) {
+      int src = t + k;
+      if (src >= len) src -= len;
+      v = p[s + src];
+    }
+    __syncthreads();
+    if (t < len) p[s + t] = v;
+  }
+  __syncthreads();
+}
+
+template <typename T, bool kSmem>
+__device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d,
+                                               double scale, double* vals) {
+  if (n <= 1) return 0.0;
+  if constexpr (std::is_same<T, uint16_t>::value) {
+    if (d.int_mode) {
+      uint32_t* iv = reinterpret_cast<uint32_t*>(vals);
+      for (int depth = d.depths - 1; depth >= 0; --depth) {
+        const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 2
+        for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
+          const int4 r = d.rec[e];
+          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
+          uint32_t sub = 0;
+          if (r.z >= 0) {
+            const uint32_t x = iv[r.z], y = iv[r.w];
+            sub = x > y ? x : y;
+          }
+          iv[e] = c + sub;
+        }
+        __syncthreads();
+      }
+      const int top = d.depth_off[1];
+      uint32_t best = iv[0];
+      for (int e = 1; e < top; ++e) best = iv[e] > best ? iv[e] : best;
+      return __dmul_rn((double)best, d.w);
+    }
+  }
+  for (int depth = d.depths - 1; depth >= 0; --depth) {
+    const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 2
+    for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
+      const int4 r = d.rec[e];
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
+      if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+      const double sub = r.z >= 0 ? ref_max(vals[r.z], vals[r.w]) : 0.0;
+      vals[e] = __dadd_rn(c, sub);
+    }
+    __syncthreads();
+  }
+  const int top = d.depth_off[1];
+  double best = vals[0];
+  for (int e = 1; e < top; ++e) best = ref_max(best, vals[e]);
+  return best;
+}
+
+// Sum over rounds of the round maximum; the per-round maximum of raw codes is
+// exact under any grouping (no NaN survives the running max from 0), and the
+// rounds are summed in order, so the value equals warp_rounds_cost's.
+template <typename T, bool kSmem>
+__device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n, const T* mat, const RoundsArgs& r,
+                                                  double scale, typename MaxAcc<T>::type* red) {
+  using Acc = typename MaxAcc<T>::type;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  double total = 0.0;
+  long long stride = 1;
+  for (int rd = 0; rd < r.rounds; ++rd) {
+    Acc mx = Acc(0);
+    if (r.kind == 0) {
+      const int s = 1 << rd;
+      for (int j = t; j < (n >> 1); j += kCta)
+        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
+    } else if (r.kind == 1) {
+      const int s = 1 << rd;
+      for (int j = t; j < n; j += kCta) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+    } else {
+      const int bm1 = r.b - 1;
+      const int pairs = (n / r.b) * bm1;
+      for (int q = t; q < pairs; q += kCta) {
+        const int j = q / bm1;
+        const int k = 1 + (q - j * bm1);
+        const int dst = (int)(((long long)j + (long long)k * stride) % n);
+        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[dst]));
+      }
+      stride *= r.b;
+    }
+    mx = warp_max(mx);
+    if (lane == 0) red[(rd & 1) * (kCta / 32) + w] = mx;  // double-buffered by round parity
+    __syncthreads();
+    Acc m = red[(rd & 1) * (kCta / 32)];
+#pragma unroll
+    for (int k = 1; k < kCta / 32; ++k) m = ref_max<Acc>(m, red[(rd & 1) * (kCta / 32) + k]);
+    double rm = to_double((T)m, scale);
+    if (r.mode == RW_LATENCY_TIMES_SIZE) rm = __dmul_rn(rm, r.bytes[rd]);
+    total = __dadd_rn(total, rm);
+  }
+  return total;
+}
+
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(kCta) k_anneal_full_cta(AnnealArgs a, const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using Acc = typename MaxAcc<T>::type;
+  __shared__ Acc red[2 * (kCta / 32)];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  stage_dbt_plan(a.dbt, smem);
+  const int chain = blockIdx.x;
+  if (chain >= a.chains) return;
+  const int n = a.n;
+  unsigned char* base = smem + al16(a.mat_smem);
+  uint16_t* p = reinterpret_cast<uint16_t*>(base);
+  uint16_t* q = reinterpret_cast<uint16_t*>(base + al16((size_t)n * 2));
+  double* vals = reinterpret_cast<double*>(base + 2 * al16((size_t)n * 2));
+  if (a.dbt.gvals) vals = a.dbt.gvals + (size_t)chain * a.dbt.edges;
+  const uint16_t* gcur = a.cur + (size_t)chain * n;
+  for (int i = threadIdx.x; i < n; i += kCta) p[i] = gcur[i];
+  __syncthreads();
+  double cur = a.cur_cost[chain];
+  double best = a.best_cost[chain];
+  unsigned long long ctr = a.ctr[chain];
+  unsigned long long props = a.proposals[chain];
+  const int64_t gid = a.gid0 + chain;
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint64_t stream = ((uint64_t)gid << 5) | 31u;
+  for (int level = a.level_begin; level < a.level_end; ++level) {
+    const double t = a.temps[level];
+    for (int s = 0; s < a.steps; ++s) {
+      Philox rng;
+      rng.key = key;
+      rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+      const uint4 r = rng.block();
+      ++ctr;
+      const Move m = draw_move_mix(r, n, a.mix_swap, a.mix_rev);
+      cta_copy_order(q, p, n);
+      __syncthreads();
+      cta_apply_move(q, n, m);
+      double c;
+      if (a.model == kDoubleBinaryTree) c = cta_dbt_cost<T, kSmem>(q, n, mat, a.dbt, a.scale, vals);
+      else c = cta_rounds_cost<T, kSmem>(q, n, mat, a.rounds, a.scale, red);
+      const double delta = c - cur;
+      bool acc = delta <= 0.0;
+      if (!acc) {
+        const float u = (float)(r.w >> 8) * 0x1.0p-24f;
+        acc = u < __expf(-(float)(delta / t));
+      }
+      ++props;
+      if (acc) {
+        uint16_t* tmp = p;
+        p = q;
+        q = tmp;
+        cur = c;
+        if (cur < best) {
+          best = cur;
+          uint16_t* g = a.best + (size_t)chain * n;
+          for (int i = threadIdx.x; i < n; i += kCta) g[i] = p[i];
+        }
+      }
+      __syncthreads();  // every thread is done with q (and vals) before the next copy
+    }
+  }
+  uint16_t* g = a.cur + (size_t)chain * n;
+  for (int i = threadIdx.x; i < n; i += kCta) g[i] = p[i];
+  if (threadIdx.x == 0) {
+    a.cur_cost[chain] = cur;
+    a.best_cost[chain] = best;
+    a.ctr[chain] = ctr;
+    a.proposals[chain] = props;
+  }
+}
+
 // Temperature calibration (schedule 1): each warp draws a random order and
 // prices `per_lane` random 2-opt (symmetric) or swap moves per lane against
 // it; the deltas (kernel units) go to `out` for the host to summarise.
@@ -1127,6 +1340,31 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   auto full = smem_mat ? k_anneal_full<T, true> : k_anneal_full<T, false>;
   smem_attr(ring, dyn_ring);
   smem_attr(full, dyn);
+  // Few chains of a full-evaluation model: one CTA of kCta threads per chain
+  // (k_anneal_full_cta, identical trajectory) instead of one warp.
+  AnnealArgs ac = a;
+  size_t cta_dyn = 0;
+  bool use_cta = plan.model != kRing && n > 1 && chains <= 2 * di.sms;
+  bool cta_smem_mat = false;
+  if (use_cta) {
+    const size_t chain_bytes = 2 * al16((size_t)n * 2) + al16((size_t)dbt_edges * vb);
+    cta_smem_mat = al16(mat_bytes) + chain_bytes <= (size_t)di.smem;
+    ac.mat_smem = cta_smem_mat ? mat_bytes : 0;
+    ac.dbt.stage_plan = 0;
+    ac.dbt.gvals = nullptr;
+    cta_dyn = al16(ac.mat_smem) + chain_bytes;
+    if (cta_dyn > (size_t)di.smem) use_cta = false;
+    if (use_cta && plan.model == kDoubleBinaryTree && dbt_edges > 0) {
+      const size_t pb = dbt_plan_bytes(dbt_edges, a.dbt.depths);
+      if (al16(cta_dyn) + pb <= (size_t)di.smem) {
+        ac.dbt.stage_plan = 1;
+        ac.dbt.plan_off = (int)al16(cta_dyn);
+        cta_dyn = al16(cta_dyn) + pb;
+      }
+    }
+  }
+  auto fullc = cta_smem_mat ? k_anneal_full_cta<T, true> : k_anneal_full_cta<T, false>;
+  if (use_cta) smem_attr(fullc, cta_dyn);
   const auto deadline = start + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(cfg.budget_s));
   const int per_launch = std::max(1, (int)std::min<long long>(levels, (1LL << 16) / std::max(1, steps_eff)));
   int level = 0;
@@ -1135,8 +1373,15 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
     if (Clock::now() >= deadline) break;
     a.level_begin = level;
     a.level_end = std::min(levels, level + per_launch);
-    if (plan.model == kRing) ring<<<grid, threads, dyn_ring, st>>>(a, static_cast<const T*>(p.d_mat));
-    else full<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
+    if (plan.model == kRing) {
+      ring<<<grid, threads, dyn_ring, st>>>(a, static_cast<const T*>(p.d_mat));
+    } else if (use_cta) {
+      ac.level_begin = a.level_begin;
+      ac.level_end = a.level_end;
+      fullc<<<chains, kCta, cta_dyn, st>>>(ac, static_cast<const T*>(p.d_mat));
+    } else {
+      full<<<grid, threads, dyn, st>>>(a, static_cast<const T*>(p.d_mat));
+    }
     RW_CUDA(cudaGetLastError());
     level = a.level_end;
   }

@@ -361,3 +361,22 @@ def test_sample_philox_extension_is_deterministic():
     orders = rw.sample_orders_philox(64, 256, 3)
     assert all(sorted(o) == list(range(64)) for o in orders)
     assert np.array_equal(a, Port().evaluate_batch(m, orders, make_spec(0, 64, fixtures.SIZE_FIXED)))
+
+
+@pytest.mark.parametrize("alg,pair", [(2, 0), (1, 1), (3, 0)])
+def test_anneal_cta_chains_follow_the_warp_chains_exactly(alg, pair):
+    """Full-evaluation models: few chains run one CTA per chain
+    (k_anneal_full_cta), many chains one warp per chain (k_anneal_full).
+    Philox streams are keyed by global chain id, so 400 chains in one call
+    (warp kernel) and the same chains as two shards of 200 (CTA kernel) must
+    end at the same winner, cost and order."""
+    m = fixtures.config_matrix("C1", "fixed")
+    prob = rw.Problem(m)
+    spec = rw.CollectiveSpec(rw.Algorithm(alg), 64, fixtures.SIZE_FIXED, 2, rw.CostMode.LatencyTimesSize,
+                             rw.HdPairing(pair))
+    cfg = rw.SolverConfig(seed=9, budget=1e6, steps_per_temperature=24)
+    o_all, c_all, _, rep_all = prob.anneal(spec, cfg, chains=400)
+    a = prob.anneal(spec, cfg, chains=200, chain_begin=0, chain_total=400)
+    b = prob.anneal(spec, cfg, chains=200, chain_begin=200, chain_total=400)
+    best = min([(a[1], a[3]["winner_chain"], a[0].tolist()), (b[1], b[3]["winner_chain"], b[0].tolist())])
+    assert best[0] == c_all and best[1] == rep_all["winner_chain"] and best[2] == o_all.tolist()
