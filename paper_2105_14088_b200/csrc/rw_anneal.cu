@@ -711,13 +711,10 @@ __device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n,
       const int s = 1 << rd;
       for (int j = t; j < n; j += kCta) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
     } else {
-      const int bm1 = r.b - 1;
-      const int pairs = (n / r.b) * bm1;
-      for (int q = t; q < pairs; q += kCta) {
-        const int j = q / bm1;
-        const int k = 1 + (q - j * bm1);
-        const int dst = (int)(((long long)j + (long long)k * stride) % n);
-        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[dst]));
+      const int st = (int)stride;  // j + (B-1)*B^i <= N-1: no modulo (warp_rounds_cost)
+      for (int j = t; j < n / r.b; j += kCta) {
+        const int a = s_perm[j];
+        for (int k = 1; k < r.b; ++k) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, a, s_perm[j + k * st]));
       }
       stride *= r.b;
     }

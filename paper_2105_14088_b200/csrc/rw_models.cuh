@@ -72,13 +72,14 @@ __device__ double warp_rounds_cost(const uint16_t* s_perm, int n, const T* mat, 
       const int s = 1 << rd;
       for (int j = lane; j < n; j += 32) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
     } else {
-      const int bm1 = r.b - 1;
-      const int pairs = (n / r.b) * bm1;
-      for (int t = lane; t < pairs; t += 32) {
-        const int j = t / bm1;
-        const int k = 1 + (t - j * bm1);
-        const int dst = (int)(((long long)j + (long long)k * stride) % n);
-        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[dst]));
+      // BCube: sources j < N/B, partners j + k*B^i for k = 1..B-1.  The
+      // reference's "% n" never fires (j + (B-1)*B^i <= N-1), so the pairs are
+      // walked source by source with no division or modulo; the round maximum
+      // is the same under any order.
+      const int st = (int)stride;
+      for (int j = lane; j < n / r.b; j += 32) {
+        const int a = s_perm[j];
+        for (int k = 1; k < r.b; ++k) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, a, s_perm[j + k * st]));
       }
       stride *= r.b;
     }
