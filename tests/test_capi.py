@@ -112,3 +112,56 @@ def test_null_and_shape_arguments_are_domain_errors():
         _lib.check(_lib.lib.rw_evaluate(None, None, None, None))
     with pytest.raises(rw.DomainError):
         rw.Problem(np.zeros((3, 4)))
+
+
+def test_packed_layout_helpers_on_the_host():
+    """rw_packed_row_bytes / rw_pack_orders (host side of the packed wire
+    layout): 10 bits per host at N=1024 is 1280 bytes per order; the packing
+    round-trips; out-of-width values and bad widths are domain errors."""
+    from paper_2105_14088_b200 import api
+    assert api.packed_row_bytes(1024, 10) == 1280
+    assert api.packed_row_bytes(13, 4) == 16 and api.packed_bits(13) == 4 and api.packed_bits(1024) == 10
+    assert int(_lib.lib.rw_packed_row_bytes(0, 10)) == -1 and int(_lib.lib.rw_packed_row_bytes(8, 17)) == -1
+    rng = np.random.default_rng(1)
+    for n, bits in ((13, 4), (64, 6), (1000, 10), (4096, 12), (300, 16)):
+        o = np.array([rng.permutation(n) for _ in range(5)], dtype=np.int32)
+        buf = api.pack_orders(o, bits)
+        assert buf.size == 5 * api.packed_row_bytes(n, bits)
+        w = np.concatenate([buf.view(np.uint32), np.zeros(1, np.uint32)]).astype(np.uint64)
+        row = api.packed_row_bytes(n, bits) // 4
+        for b in range(5):
+            i = np.arange(n, dtype=np.uint64) * np.uint64(bits)
+            q = (i >> np.uint64(5)) + np.uint64(b * row)
+            sh = i & np.uint64(31)
+            v = ((w[q] | (w[q + np.uint64(1)] << np.uint64(32))) >> sh) & np.uint64((1 << bits) - 1)
+            assert np.array_equal(v.astype(np.int64), o[b])
+    with pytest.raises(rw.DomainError):
+        api.pack_orders(np.array([[0, 1, 2, 3, 4, 5, 6, 7, 8]]), 3)  # 2^3 < 9
+    with pytest.raises(rw.DomainError):
+        api.pack_orders(np.array([[0, 1, 99]]), 2)
+
+
+def test_gpu_options_round_trip_through_the_c_abi():
+    from paper_2105_14088_b200 import api
+    before = api.gpu_options()
+    try:
+        api.set_gpu_options(chains=77, immutable_matrices=1, num_devices=0)
+        o = api.gpu_options()
+        assert (o["chains"], o["immutable_matrices"], o["num_devices"]) == (77, 1, 0)
+        with pytest.raises(rw.DomainError):
+            api.set_gpu_options(num_devices=-1)
+        with pytest.raises(TypeError):
+            api.set_gpu_options(bogus=1)
+    finally:
+        api.set_gpu_options(**before)
+    assert api.gpu_options() == before
+
+
+def test_problem_set_argument_checks_without_gpu_work():
+    from paper_2105_14088_b200 import api
+    if rw.device_count() == 0:
+        with pytest.raises((rw.DomainError, rw.RankweaveError)):
+            api.ProblemSet(np.zeros((4, 4)))
+    else:
+        with pytest.raises(rw.DomainError):
+            api.ProblemSet(np.zeros((4, 4)), devices=[0, 0])
