@@ -403,37 +403,22 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
     if (bad) s_bad = 1;
     for (int depth = d.depths - 1; depth >= 0; --depth) {
       const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
-      // Batches of kB edges per thread: the records, then the kB matrix
-      // gathers are all issued before any edge value is stored (the stores
-      // to shared memory would otherwise order the next gathers behind them).
-      constexpr int kB = 4;
-      for (int e0 = lo + threadIdx.x; e0 < hi; e0 += kB * blockDim.x) {
-        int4 r[kB];
-        T raw[kB];
-#pragma unroll
-        for (int k = 0; k < kB; ++k) {
-          const int e = e0 + k * blockDim.x;
-          r[k] = e < hi ? __ldg(d.rec + e) : make_int4(0, 0, -1, -1);  // {src, dst, c0, c1}
-        }
-#pragma unroll
-        for (int k = 0; k < kB; ++k) raw[k] = ld_matrix<T>(mat, (size_t)p[r[k].x] * n + p[r[k].y]);
-#pragma unroll
-        for (int k = 0; k < kB; ++k) {
-          const int e = e0 + k * blockDim.x;
-          if (e >= hi) break;
-          if (im) {
-            uint32_t sub = 0;
-            if (r[k].z >= 0) {
-              const uint32_t x = iv[r[k].z], y = iv[r[k].w];
-              sub = x > y ? x : y;
-            }
-            iv[e] = (uint32_t)raw[k] + sub;
-          } else {
-            double c = to_double(raw[k], a.scale);
-            if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-            const double sub = r[k].z >= 0 ? ref_max(dv[r[k].z], dv[r[k].w]) : 0.0;
-            dv[e] = __dadd_rn(c, sub);
+#pragma unroll 2
+      for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        const int4 r = __ldg(d.rec + e);  // {src, dst, c0, c1}
+        const T raw = ld_matrix<T>(mat, (size_t)p[r.x] * n + p[r.y]);
+        if (im) {
+          uint32_t sub = 0;
+          if (r.z >= 0) {
+            const uint32_t x = iv[r.z], y = iv[r.w];
+            sub = x > y ? x : y;
           }
+          iv[e] = (uint32_t)raw + sub;
+        } else {
+          double c = to_double(raw, a.scale);
+          if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+          const double sub = r.z >= 0 ? ref_max(dv[r.z], dv[r.w]) : 0.0;
+          dv[e] = __dadd_rn(c, sub);
         }
       }
       __syncthreads();

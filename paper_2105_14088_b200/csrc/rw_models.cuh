@@ -103,25 +103,16 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
       uint32_t* iv = reinterpret_cast<uint32_t*>(vals);
       for (int depth = d.depths - 1; depth >= 0; --depth) {
         const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
-        // batches of 4 edges per lane: records and lookups issued before the
-        // stores (which would otherwise order the next lookups behind them)
-        for (int e0 = lo + lane; e0 < hi; e0 += 128) {
-          int4 r[4];
-          uint32_t c[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) r[k] = e0 + 32 * k < hi ? d.rec[e0 + 32 * k] : make_int4(0, 0, -1, -1);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) c[k] = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r[k].x], s_perm[r[k].y]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (e0 + 32 * k >= hi) break;
-            uint32_t sub = 0;
-            if (r[k].z >= 0) {
-              const uint32_t x = iv[r[k].z], y = iv[r[k].w];
-              sub = x > y ? x : y;
-            }
-            iv[e0 + 32 * k] = c[k] + sub;
+#pragma unroll 4
+        for (int e = lo + lane; e < hi; e += 32) {
+          const int4 r = d.rec[e];
+          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
+          uint32_t sub = 0;
+          if (r.z >= 0) {
+            const uint32_t x = iv[r.z], y = iv[r.w];
+            sub = x > y ? x : y;
           }
+          iv[e] = c + sub;
         }
         __syncwarp();
       }
@@ -134,22 +125,14 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
   }
   for (int depth = d.depths - 1; depth >= 0; --depth) {
     const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
-    for (int e0 = lo + lane; e0 < hi; e0 += 128) {
-      int4 r[4];
-      T raw[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) r[k] = e0 + 32 * k < hi ? d.rec[e0 + 32 * k] : make_int4(0, 0, -1, -1);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) raw[k] = mat_at<T, kSmem>(mat, n, s_perm[r[k].x], s_perm[r[k].y]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (e0 + 32 * k >= hi) break;
-        double c = to_double(raw[k], scale);
-        if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
-        // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
-        const double sub = r[k].z >= 0 ? ref_max(vals[r[k].z], vals[r[k].w]) : 0.0;
-        vals[e0 + 32 * k] = __dadd_rn(c, sub);
-      }
+#pragma unroll 4
+    for (int e = lo + lane; e < hi; e += 32) {
+      const int4 r = d.rec[e];
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
+      if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+      // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
+      const double sub = r.z >= 0 ? ref_max(vals[r.z], vals[r.w]) : 0.0;
+      vals[e] = __dadd_rn(c, sub);
     }
     __syncwarp();
   }
