@@ -152,6 +152,9 @@ struct ThreadCtx {
   void* pinned(size_t bytes);
 };
 ThreadCtx& thread_ctx(int device);
+// Frees the calling thread's contexts (streams, scratch, pinned staging);
+// for threads the library owns (rw_multi.cpp member workers) before they exit.
+void thread_ctx_release();
 
 // Scope of one asynchronous *_device call on a caller's stream: every scratch
 // buffer the launch code asks for (ThreadCtx::scratch) comes from the

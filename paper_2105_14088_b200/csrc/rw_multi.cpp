@@ -127,7 +127,11 @@ class MemberWorker {
       {
         std::unique_lock<std::mutex> l(mu_);
         cv_.wait(l, [this] { return stop_ || task_; });
-        if (stop_) return;
+        if (stop_) {
+          l.unlock();
+          thread_ctx_release();  // this thread's streams and scratch die with the set
+          return;
+        }
         f = std::move(task_);
         task_ = nullptr;
       }

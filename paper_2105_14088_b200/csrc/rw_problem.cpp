@@ -106,10 +106,34 @@ void* ThreadCtx::pinned(size_t bytes) {
   return h_pin;
 }
 
+namespace {
+// One context per (thread, device).  Not torn down by thread-exit handlers
+// (CUDA objects must not be destroyed during process shutdown); threads the
+// library owns release theirs explicitly (thread_ctx_release).
+thread_local std::map<int, ThreadCtx*> t_ctxs;
+}  // namespace
+
+void thread_ctx_release() {
+  for (auto& kv : t_ctxs) {
+    ThreadCtx* c = kv.second;
+    if (cudaSetDevice(c->device) == cudaSuccess) {
+      for (auto& s : c->stream) cudaStreamSynchronize(s);
+      for (void* b : c->d_buf)
+        if (b) cudaFree(b);
+      if (c->d_err) cudaFree(c->d_err);
+      if (c->h_err) cudaFreeHost(c->h_err);
+      if (c->h_pin) cudaFreeHost(c->h_pin);
+      for (auto& e : c->ev) cudaEventDestroy(e);
+      for (auto& s : c->stream) cudaStreamDestroy(s);
+    }
+    cudaGetLastError();
+    delete c;
+  }
+  t_ctxs.clear();
+}
+
 ThreadCtx& thread_ctx(int device) {
-  // One context per (thread, device); intentionally never torn down (CUDA
-  // objects must not be destroyed from thread-exit handlers during shutdown).
-  thread_local std::map<int, ThreadCtx*> ctxs;
+  auto& ctxs = t_ctxs;
   auto it = ctxs.find(device);
   if (it != ctxs.end()) return *it->second;
   auto* c = new ThreadCtx();

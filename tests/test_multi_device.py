@@ -97,3 +97,27 @@ def test_cpp_drop_in_over_device_sets_is_device_count_invariant():
     assert first.count("\n") == 6 and "brute ring cost=" in first
     for k, out in outs.items():
         assert out == first, k
+
+
+def test_set_lifecycle_releases_its_threads_resources():
+    """A device set owns one host thread per member; destroying the set frees
+    those threads' streams and scratch (repeated sets do not leak device memory)."""
+    import torch
+    m = fixtures.config_matrix("C4", "fixed")
+    spec = fixtures.ring_spec(1024, fixtures.SIZE_FIXED)
+    o = np.array([np.random.default_rng(k).permutation(1024) for k in range(20000)], dtype=np.int32)
+    k = device_counts()[-1]
+
+    def one():
+        s = rw.api.ProblemSet(m, devices=list(range(k)))
+        s.evaluate_batch(spec, o)
+        s.close()
+
+    one()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(0)[0]
+    for _ in range(4):
+        one()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info(0)[0]
+    assert free0 - free1 < (64 << 20), (free0, free1)
