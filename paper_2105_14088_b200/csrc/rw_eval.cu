@@ -371,7 +371,7 @@ template <typename T, typename P, bool kValidate>
 __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __restrict__ perms,
                                                  const T* __restrict__ mat, double* __restrict__ costs) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int n = a.n, E = d.edges;
+  const int n = a.n;
   uint16_t* p = reinterpret_cast<uint16_t*>(smem);
   uint8_t* flags = smem + align16((size_t)n * 2);
   unsigned char* vbase = flags + align16((size_t)n);
@@ -437,7 +437,6 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
       costs[o] = best;
       if (kValidate && s_bad) report_bad_order(a.err, n, o);
     }
-    (void)E;
   }
 }
 
