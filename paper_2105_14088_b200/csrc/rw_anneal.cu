@@ -709,7 +709,14 @@ __device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n,
         mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
     } else if (r.kind == 1) {
       const int s = 1 << rd;
-      for (int j = t; j < n; j += kCta) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+      if (r.sym) {  // each unordered pair once (warp_rounds_cost)
+        for (int k = t; k < (n >> 1); k += kCta) {
+          const int j = ((k >> rd) << (rd + 1)) | (k & (s - 1));
+          mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
+        }
+      } else {
+        for (int j = t; j < n; j += kCta) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+      }
     } else {
       const int st = (int)stride;  // j + (B-1)*B^i <= N-1: no modulo (warp_rounds_cost)
       for (int j = t; j < n / r.b; j += kCta) {
@@ -1163,6 +1170,7 @@ int fill_model_args(AnnealArgs& a, const EvalPlan& plan) {
   int dbt_edges = 0;
   if (plan.model == kHalvingDoubling || plan.model == kBCube) {
     a.rounds.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
+    a.rounds.sym = a.symmetric;
     a.rounds.rounds = plan.rounds;
     a.rounds.b = plan.bcube_b;
     a.rounds.mode = plan.mode;
@@ -1448,6 +1456,7 @@ void local_search_typed(Problem& p, const EvalPlan& plan, int32_t* perms, int64_
     a.n = n;
     a.model = plan.model;
     a.scale = p.scale;
+    a.symmetric = p.symmetric ? 1 : 0;
     const int dbt_edges = fill_model_args(a, plan);
     const size_t mat_bytes = (size_t)n * n * sizeof(T);
     const size_t vb = (std::is_same<T, uint16_t>::value && plan.dbt_int) ? 4 : 8;  // edge value bytes

@@ -998,6 +998,7 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
   } else {
     RoundsArgs r{};
     r.kind = plan.model == kBCube ? 2 : (plan.pairing == RW_PAIRING_PAPER ? 0 : 1);
+    r.sym = p.symmetric ? 1 : 0;
     r.rounds = plan.rounds;
     r.b = plan.bcube_b;
     r.mode = plan.mode;

@@ -18,6 +18,7 @@ __device__ __forceinline__ T mat_at(const T* m, int n, int a, int b) {
 
 struct RoundsArgs {
   int kind;  // 0 hd paper, 1 hd xor, 2 bcube
+  int sym;   // symmetric matrix: xor pairs are looked up once (c(a,b) == c(b,a))
   int rounds;
   int b;
   int mode;
@@ -70,7 +71,17 @@ __device__ double warp_rounds_cost(const uint16_t* s_perm, int n, const T* mat, 
         mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
     } else if (r.kind == 1) {
       const int s = 1 << rd;
-      for (int j = lane; j < n; j += 32) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+      if (r.sym) {
+        // each unordered pair {j, j^s} once: j with bit s clear.  On a
+        // symmetric matrix both directions hold the same value, so the round
+        // maximum is unchanged (NaN is never symmetric-equal; -0.0 never wins).
+        for (int k = lane; k < (n >> 1); k += 32) {
+          const int j = ((k >> rd) << (rd + 1)) | (k & (s - 1));
+          mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
+        }
+      } else {
+        for (int j = lane; j < n; j += 32) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+      }
     } else {
       // BCube: sources j < N/B, partners j + k*B^i for k = 1..B-1.  The
       // reference's "% n" never fires (j + (B-1)*B^i <= N-1), so the pairs are
