@@ -709,7 +709,7 @@ __device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n,
         mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
     } else if (r.kind == 1) {
       const int s = 1 << rd;
-      if (r.sym) {  // each unordered pair once (warp_rounds_cost)
+      if (r.sym && n >= 2 * kCta) {  // each unordered pair once (warp_rounds_cost); small n: all lanes busy anyway
         for (int k = t; k < (n >> 1); k += kCta) {
           const int j = ((k >> rd) << (rd + 1)) | (k & (s - 1));
           mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
