@@ -1214,10 +1214,31 @@ void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perm
       char* base = static_cast<char*>(c.scratch(0, pb + ub + 64));
       d_eval = stage(st, h, batch, base, reinterpret_cast<uint16_t*>(base + pb));
     }
+    // A single unvalidated order (evaluate()): the host polls the mapped cost
+    // slot instead of waiting in cudaStreamSynchronize -- the kernel's cost
+    // store is its last access to these buffers.  A NaN pattern no cost
+    // computation produces marks the slot pending; the stream is queried now
+    // and then, which also surfaces a failed launch.
+    constexpr uint64_t kPending = 0x7FF4DEAD5EED0001ull;
+    volatile uint64_t* slot = reinterpret_cast<volatile uint64_t*>(h + pb);
+    const bool poll = batch == 1 && !validate;
+    if (poll) *slot = kPending;
     launch_evaluate(p, plan, d_eval, eval_bytes, batch, reinterpret_cast<double*>(dh + pb), exact, validate, c.d_err,
                     st, 2);
-    if (validate) raise(st);  // synchronises st
-    else RW_CUDA(cudaStreamSynchronize(st));
+    if (validate) {
+      raise(st);  // synchronises st
+    } else if (poll) {
+      for (unsigned spin = 1;; ++spin) {
+        if (*slot != kPending) break;
+        if ((spin & 1023u) == 0) {
+          const cudaError_t e = cudaStreamQuery(st);
+          if (e == cudaSuccess) break;  // done: the slot holds the cost (even if it equals the pattern)
+          if (e != cudaErrorNotReady) RW_CUDA(e);
+        }
+      }
+    } else {
+      RW_CUDA(cudaStreamSynchronize(st));
+    }
     std::memcpy(costs, h + pb, (size_t)batch * 8);
     finish();
     return;
