@@ -810,6 +810,250 @@ __global__ void __launch_bounds__(kCta) k_anneal_full_cta(AnnealArgs a, const T*
   }
 }
 
+// ------------------------- tree-model anneal with delta-evaluated swaps -----
+// One chain per CTA (as k_anneal_full_cta) keeping the chain's edge values
+// (path value and own cost of every edge of the critical-path forest) in
+// shared memory.  A swap of positions i, j changes the own cost of at most 16
+// edges (those with i or j as an endpoint) and the path values of those edges
+// and their ancestors only: warp 0 recomputes just those, depth by depth, from
+// the leaves up, into an overlay (marked with a per-proposal generation), and
+// reads the new cost off the top edges.  Other moves take the full
+// evaluation into the second value buffers.  Every recomputed value uses the
+// operation sequence of warp_dbt_cost, so costs -- and the trajectory -- are
+// bit-identical to k_anneal_full.
+template <typename T, typename V, bool kSmem>
+struct DbtDelta {
+  // own cost of an edge between hosts a and b (kernel units: raw code in the
+  // integer form, otherwise fl(fl(value) * half) as warp_dbt_cost)
+  __device__ static V own(const T* mat, int n, const DbtArgs& d, double scale, int a, int b) {
+    if constexpr (std::is_same<V, uint32_t>::value) {
+      return (uint32_t)mat_at<T, kSmem>(mat, n, a, b);
+    } else {
+      double c = to_double(mat_at<T, kSmem>(mat, n, a, b), scale);
+      if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+      return c;
+    }
+  }
+  __device__ static V path(V own, bool leaf, V x, V y) {
+    if constexpr (std::is_same<V, uint32_t>::value) {
+      return leaf ? own : own + (x > y ? x : y);
+    } else {
+      return __dadd_rn(own, leaf ? 0.0 : ref_max(x, y));  // T(empty) = 0.0
+    }
+  }
+  __device__ static double finish(V best, const DbtArgs& d) {
+    if constexpr (std::is_same<V, uint32_t>::value) return __dmul_rn((double)best, d.w);
+    else return best;
+  }
+  __device__ static V top_max(V a, V b) {
+    if constexpr (std::is_same<V, uint32_t>::value) return b > a ? b : a;
+    else return ref_max(a, b);
+  }
+};
+
+template <typename T, typename V, bool kSmem>
+__device__ __forceinline__ double cta_dbt_full(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d,
+                                               const int4* rec, const int32_t* doff, double scale, V* val, V* own) {
+  using D = DbtDelta<T, V, kSmem>;
+  for (int depth = d.depths - 1; depth >= 0; --depth) {
+    const int lo = doff[depth], hi = doff[depth + 1];
+#pragma unroll 2
+    for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
+      const int4 r = rec[e];
+      const V c = D::own(mat, n, d, scale, s_perm[r.x], s_perm[r.y]);
+      own[e] = c;
+      val[e] = r.z >= 0 ? D::path(c, false, val[r.z], val[r.w]) : D::path(c, true, c, c);
+    }
+    __syncthreads();
+  }
+  V best = val[0];
+  for (int e = 1; e < doff[1]; ++e) best = D::top_max(best, val[e]);
+  return D::finish(best, d);
+}
+
+template <typename T, typename V, bool kSmem>
+__global__ void __launch_bounds__(kCta) k_anneal_dbt_delta(AnnealArgs a, const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using D = DbtDelta<T, V, kSmem>;
+  __shared__ double s_cost;
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const DbtArgs& d = a.dbt;
+  const int n = a.n, E = d.edges, t = threadIdx.x, lane = t & 31;
+  // layout after the matrix: rec | depth_off | pd | posedges | p | q | val x2 | own x2 | nval | nown | marks x2
+  unsigned char* b = smem + al16(a.mat_smem);
+  int4* rec = reinterpret_cast<int4*>(b);
+  b += al16((size_t)E * 16);
+  int32_t* doff = reinterpret_cast<int32_t*>(b);
+  b += al16((size_t)(d.depths + 1) * 4);
+  int32_t* pd = reinterpret_cast<int32_t*>(b);
+  b += al16((size_t)E * 4);
+  int32_t* pe = reinterpret_cast<int32_t*>(b);
+  b += al16((size_t)n * 32);
+  uint16_t* p = reinterpret_cast<uint16_t*>(b);
+  b += al16((size_t)n * 2);
+  uint16_t* q = reinterpret_cast<uint16_t*>(b);
+  b += al16((size_t)n * 2);
+  V* val = reinterpret_cast<V*>(b);
+  b += al16((size_t)E * sizeof(V));
+  V* val2 = reinterpret_cast<V*>(b);
+  b += al16((size_t)E * sizeof(V));
+  V* own = reinterpret_cast<V*>(b);
+  b += al16((size_t)E * sizeof(V));
+  V* own2 = reinterpret_cast<V*>(b);
+  b += al16((size_t)E * sizeof(V));
+  V* nval = reinterpret_cast<V*>(b);
+  b += al16((size_t)E * sizeof(V));
+  V* nown = reinterpret_cast<V*>(b);
+  b += al16((size_t)E * sizeof(V));
+  uint32_t* vmark = reinterpret_cast<uint32_t*>(b);
+  b += al16((size_t)E * 4);
+  uint32_t* omark = reinterpret_cast<uint32_t*>(b);
+  for (int e = t; e < E; e += kCta) {
+    rec[e] = d.rec[e];
+    pd[e] = d.pd[e];
+    vmark[e] = 0u;
+    omark[e] = 0u;
+  }
+  for (int k = t; k <= d.depths; k += kCta) doff[k] = d.depth_off[k];
+  for (int k = t; k < 8 * n; k += kCta) pe[k] = d.posedges[k];
+  const int chain = blockIdx.x;
+  const uint16_t* gcur = a.cur + (size_t)chain * n;
+  for (int i = t; i < n; i += kCta) p[i] = gcur[i];
+  __syncthreads();
+  cta_dbt_full<T, V, kSmem>(p, n, mat, d, rec, doff, a.scale, val, own);  // ends with a barrier
+  double cur = a.cur_cost[chain];
+  double best = a.best_cost[chain];
+  unsigned long long ctr = a.ctr[chain];
+  unsigned long long props = a.proposals[chain];
+  const int64_t gid = a.gid0 + chain;
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint64_t stream = ((uint64_t)gid << 5) | 31u;
+  uint32_t gen = 0;
+  const int top = doff[1];
+  for (int level = a.level_begin; level < a.level_end; ++level) {
+    const double temp = a.temps[level];
+    for (int s = 0; s < a.steps; ++s) {
+      Philox rng;
+      rng.key = key;
+      rng.ctr = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+      const uint4 r = rng.block();
+      ++ctr;
+      const Move m = draw_move_mix(r, n, a.mix_swap, a.mix_rev);
+      const bool swap = m.type == 0;
+      ++gen;
+      int node = -1;  // warp 0, lanes 0..15: an edge at position m.i / m.j, then its ancestors
+      double c;
+      if (swap) {
+        if (t < 32) {
+          const int hi = p[m.j], hj = p[m.i];  // hosts after the swap at positions i and j
+          if (lane < 16) node = pe[(lane < 8 ? m.i : m.j) * 8 + (lane & 7)];
+          if (node >= 0) {
+            const int4 rr = rec[node];
+            const int ha = rr.x == m.i ? hi : rr.x == m.j ? hj : p[rr.x];
+            const int hb = rr.y == m.i ? hi : rr.y == m.j ? hj : p[rr.y];
+            nown[node] = D::own(mat, n, d, a.scale, ha, hb);
+            omark[node] = gen;
+          }
+          __syncwarp();
+          int nd = node >= 0 ? (pd[node] & 0xFF) : -1;
+          for (int depth = d.depths - 1; depth >= 0; --depth) {
+            if (node >= 0 && nd == depth) {
+              const int4 rr = rec[node];
+              const V o = omark[node] == gen ? nown[node] : own[node];
+              V x = o, y = o;
+              if (rr.z >= 0) {
+                x = vmark[rr.z] == gen ? nval[rr.z] : val[rr.z];
+                y = vmark[rr.w] == gen ? nval[rr.w] : val[rr.w];
+              }
+              nval[node] = D::path(o, rr.z < 0, x, y);
+              vmark[node] = gen;
+              const int par = pd[node] >> 8;
+              node = par == 0xFFFFFF ? -1 : par;
+              nd = depth - 1;
+            }
+            __syncwarp();
+          }
+          V bv = vmark[0] == gen ? nval[0] : val[0];
+          for (int e = 1; e < top; ++e) bv = D::top_max(bv, vmark[e] == gen ? nval[e] : val[e]);
+          if (t == 0) s_cost = D::finish(bv, d);
+        }
+        __syncthreads();
+        c = s_cost;
+      } else {
+        cta_copy_order(q, p, n);
+        __syncthreads();
+        cta_apply_move(q, n, m);
+        c = cta_dbt_full<T, V, kSmem>(q, n, mat, d, rec, doff, a.scale, val2, own2);
+      }
+      const double delta = c - cur;
+      bool acc = delta <= 0.0;
+      if (!acc) {
+        const float u = (float)(r.w >> 8) * 0x1.0p-24f;
+        acc = u < __expf(-(float)(delta / temp));
+      }
+      ++props;
+      if (acc) {
+        if (swap) {
+          if (t < 32) {
+            // commit the overlay: walk the same chains again
+            int nd2 = -1, nn = -1;
+            if (lane < 16) nn = pe[(lane < 8 ? m.i : m.j) * 8 + (lane & 7)];
+            if (nn >= 0) {
+              own[nn] = nown[nn];
+              nd2 = pd[nn] & 0xFF;
+            }
+            for (int depth = d.depths - 1; depth >= 0; --depth) {
+              if (nn >= 0 && nd2 == depth) {
+                val[nn] = nval[nn];
+                const int par = pd[nn] >> 8;
+                nn = par == 0xFFFFFF ? -1 : par;
+                nd2 = depth - 1;
+              }
+            }
+            if (t == 0) {
+              const uint16_t x = p[m.i];
+              p[m.i] = p[m.j];
+              p[m.j] = x;
+            }
+          }
+        } else {
+          uint16_t* tp = p;
+          p = q;
+          q = tp;
+          V* tv = val;
+          val = val2;
+          val2 = tv;
+          V* to = own;
+          own = own2;
+          own2 = to;
+        }
+        cur = c;
+        __syncthreads();
+        if (cur < best) {
+          best = cur;
+          uint16_t* g = a.best + (size_t)chain * n;
+          for (int i = t; i < n; i += kCta) g[i] = p[i];
+        }
+      }
+      __syncthreads();  // every thread is done with this proposal's buffers
+    }
+  }
+  uint16_t* g = a.cur + (size_t)chain * n;
+  for (int i = t; i < n; i += kCta) g[i] = p[i];
+  if (t == 0) {
+    a.cur_cost[chain] = cur;
+    a.best_cost[chain] = best;
+    a.ctr[chain] = ctr;
+    a.proposals[chain] = props;
+  }
+}
+
+__host__ __device__ inline size_t dbt_delta_smem(size_t mat_smem, int n, int edges, int depths, size_t vb) {
+  return al16(mat_smem) + al16((size_t)edges * 16) + al16((size_t)(depths + 1) * 4) + al16((size_t)edges * 4) +
+         al16((size_t)n * 32) + 2 * al16((size_t)n * 2) + 6 * al16((size_t)edges * vb) + 2 * al16((size_t)edges * 4);
+}
+
 // Temperature calibration (schedule 1): each warp draws a random order and
 // prices `per_lane` random 2-opt (symmetric) or swap moves per lane against
 // it; the deltas (kernel units) go to `out` for the host to summarise.
@@ -1186,6 +1430,8 @@ int fill_model_args(AnnealArgs& a, const EvalPlan& plan) {
     a.dbt.half = plan.half;
     a.dbt.int_mode = plan.dbt_int ? 1 : 0;
     a.dbt.w = plan.dbt_w;
+    a.dbt.pd = plan.dbt->d_pd();
+    a.dbt.posedges = plan.dbt->d_posedges();
   }
   return dbt_edges;
 }
@@ -1370,6 +1616,24 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   }
   auto fullc = cta_smem_mat ? k_anneal_full_cta<T, true> : k_anneal_full_cta<T, false>;
   if (use_cta) smem_attr(fullc, cta_dyn);
+  // The tree model with few chains: swaps by delta evaluation (k_anneal_dbt_delta),
+  // when its tables fit next to the matrix (or without it).
+  bool use_delta = false;
+  size_t delta_dyn = 0;
+  void (*deltak)(AnnealArgs, const T*) = nullptr;
+  if (use_cta && plan.model == kDoubleBinaryTree && dbt_edges > 0) {
+    const bool iv = std::is_same<T, uint16_t>::value && plan.dbt_int;
+    const size_t vbd = iv ? 4 : 8;
+    bool dm = dbt_delta_smem(mat_bytes, n, dbt_edges, a.dbt.depths, vbd) <= (size_t)di.smem;
+    delta_dyn = dbt_delta_smem(dm ? mat_bytes : 0, n, dbt_edges, a.dbt.depths, vbd);
+    if (delta_dyn <= (size_t)di.smem) {
+      use_delta = true;
+      ac.mat_smem = dm ? mat_bytes : 0;
+      if (iv) deltak = dm ? k_anneal_dbt_delta<T, uint32_t, true> : k_anneal_dbt_delta<T, uint32_t, false>;
+      else deltak = dm ? k_anneal_dbt_delta<T, double, true> : k_anneal_dbt_delta<T, double, false>;
+      smem_attr(deltak, delta_dyn);
+    }
+  }
   const auto deadline = start + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(cfg.budget_s));
   const int per_launch = std::max(1, (int)std::min<long long>(levels, (1LL << 16) / std::max(1, steps_eff)));
   int level = 0;
@@ -1380,6 +1644,10 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
     a.level_end = std::min(levels, level + per_launch);
     if (plan.model == kRing) {
       ring<<<grid, threads, dyn_ring, st>>>(a, static_cast<const T*>(p.d_mat));
+    } else if (use_delta) {
+      ac.level_begin = a.level_begin;
+      ac.level_end = a.level_end;
+      deltak<<<chains, kCta, delta_dyn, st>>>(ac, static_cast<const T*>(p.d_mat));
     } else if (use_cta) {
       ac.level_begin = a.level_begin;
       ac.level_end = a.level_end;

@@ -61,6 +61,10 @@ struct DbtPlan {
   int32_t* d_all = nullptr;
   const int4* d_rec() const { return reinterpret_cast<const int4*>(d_all); }
   const int32_t* d_depth_off() const { return d_all + 4 * edges; }
+  // [per edge (parent << 8) | depth | per position 8 incident edges, -1 padded]
+  int32_t* d_aux = nullptr;
+  const int32_t* d_pd() const { return d_aux; }
+  const int32_t* d_posedges() const { return d_aux + edges; }
 };
 
 struct Problem {

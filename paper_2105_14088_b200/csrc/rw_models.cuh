@@ -37,6 +37,8 @@ struct DbtArgs {
   int plan_off;    // byte offset in the kernel's dynamic shared memory
   int int_mode;    // u16 storage, EvalPlan::dbt_int: uint32 path sums, vals as uint32
   double w;        // int_mode: value = sum * w
+  const int32_t* pd;        // delta tables (anneal): per edge (parent << 8) | depth
+  const int32_t* posedges;  //   per position 8 incident edges, -1 padded
 };
 
 // Plan (edge records {src, dst, c0, c1} | depth_off, int32) in shared memory:

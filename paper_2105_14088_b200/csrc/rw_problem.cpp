@@ -282,6 +282,28 @@ static void build_dbt_plan(DbtPlan& plan, int n) {
   all.insert(all.end(), plan.h_depth_off.begin(), plan.h_depth_off.end());
   RW_CUDA(cudaMalloc(&plan.d_all, all.size() * sizeof(int32_t)));
   RW_CUDA(cudaMemcpy(plan.d_all, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // Delta-evaluation tables (swap moves in the tree-model anneal): per edge
+  // (parent << 8) | depth, parent 0xFFFFFF at the roots; per position the (at
+  // most 6) edges with that position as an endpoint, -1 padded to 8.
+  std::vector<int32_t> aux(static_cast<size_t>(plan.edges) + 8 * static_cast<size_t>(n), -1);
+  for (int d = 0; d < plan.depths; ++d)
+    for (int e = plan.h_depth_off[d]; e < plan.h_depth_off[d + 1]; ++e) aux[static_cast<size_t>(e)] = (0xFFFFFF << 8) | d;
+  for (int e = 0; e < plan.edges; ++e) {
+    const int d = aux[static_cast<size_t>(e)] & 0xFF;
+    for (int c : {plan.h_c0[static_cast<size_t>(e)], plan.h_c1[static_cast<size_t>(e)]})
+      if (c >= 0) aux[static_cast<size_t>(c)] = (e << 8) | (d + 1);
+  }
+  for (int e = 0; e < plan.edges; ++e) {
+    for (int x : {plan.h_src[static_cast<size_t>(e)], plan.h_dst[static_cast<size_t>(e)]}) {
+      int32_t* slot = aux.data() + plan.edges + 8 * static_cast<size_t>(x);
+      int k = 0;
+      while (k < 8 && slot[k] >= 0 && slot[k] != e) ++k;
+      if (k == 8) fail_internal("double binary tree: more than 8 edges at one position");
+      slot[k] = e;
+    }
+  }
+  RW_CUDA(cudaMalloc(&plan.d_aux, aux.size() * sizeof(int32_t)));
+  RW_CUDA(cudaMemcpy(plan.d_aux, aux.data(), aux.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
 }
 
 // ------------------------------------------------------------- planning ---
@@ -604,6 +626,7 @@ static void destroy_problem(Problem* p) {
     if (p->d_mat) cudaFree(p->d_mat);
     if (p->d_err) cudaFree(p->d_err);
     if (p->dbt && p->dbt->d_all) cudaFree(p->dbt->d_all);
+    if (p->dbt && p->dbt->d_aux) cudaFree(p->dbt->d_aux);
     if (p->d_nb) cudaFree(p->d_nb);
     if (p->d_rank) cudaFree(p->d_rank);
     if (p->d_rank_vals) cudaFree(p->d_rank_vals);
