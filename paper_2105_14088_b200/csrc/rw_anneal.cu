@@ -374,24 +374,15 @@ __global__ void __launch_bounds__(256) k_anneal_init(AnnealArgs a, const T* __re
 }
 
 // ------------------------------------------------------- ring anneal -----
-template <typename T, bool kSmem>
-__global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __restrict__ gmat) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const T* mat = gmat;
-  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
-  const uint16_t* nbl = a.nb;
-  if (a.nb_smem) {  // candidate lists next to the warp buffers: no global load in the move draw
-    uint16_t* s_nb =
-        reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)(blockDim.x >> 5) * a.warp_bytes);
-    for (int k = threadIdx.x; k < a.n * a.K; k += blockDim.x) s_nb[k] = a.nb[k];
-    __syncthreads();
-    nbl = s_nb;
-  }
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
-  if (chain >= a.chains) return;
+// The ring chain's proposal loop (one warp per chain): `lookup(a, b)` reads
+// matrix entry (a, b) -- from L2, from the CTA's shared memory, or from a
+// cluster peer's shared memory (k_anneal_ring_cluster); `resync(p)` is the
+// FP drift resync (exact re-sum of the order).
+template <typename T, typename Lookup, typename Resync>
+__device__ __forceinline__ void anneal_ring_chain(const AnnealArgs& a, int chain, uint16_t* p, const uint16_t* nbl,
+                                                  Lookup lookup, Resync resync) {
+  const int lane = threadIdx.x & 31;
   const int n = a.n;
-  uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes);
   uint16_t* pos = p + al16((size_t)n * 2) / 2;  // inverse order (host -> position)
   const uint16_t* gcur = a.cur + (size_t)chain * n;
   for (int i = lane; i < n; i += 32) {
@@ -450,7 +441,7 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
 #pragma unroll
         for (int sl = 0; sl < kSlots; ++sl)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[sl][q] = mat_at<T, kSmem>(mat, n, dt[sl].row[q], dt[sl].col[q]);
+          for (int q = 0; q < 8; ++q) v[sl][q] = lookup(dt[sl].row[q], dt[sl].col[q]);
         // the next iteration's random blocks while the gathers are in flight
 #pragma unroll
         for (int sl = 0; sl < kSlots; ++sl) rnext[sl] = philox_at(ctr, sl);
@@ -511,7 +502,7 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
         remaining -= active;
       }
     }
-    if constexpr (!std::is_same<T, uint16_t>::value) cur = warp_ring_raw<T, kSmem>(p, n, mat, lane);  // drift resync
+    if constexpr (!std::is_same<T, uint16_t>::value) cur = resync(p);  // drift resync
   }
   __syncwarp();
   store_order(a.cur + (size_t)chain * n, p, n, lane);
@@ -521,6 +512,85 @@ __global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __re
     a.ctr[chain] = ctr;
     a.proposals[chain] = props;
   }
+}
+
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(256) k_anneal_ring(AnnealArgs a, const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const T* mat = gmat;
+  if constexpr (kSmem) mat = stage_mat<T>(gmat, a.mat_smem, smem);
+  const uint16_t* nbl = a.nb;
+  if (a.nb_smem) {  // candidate lists next to the warp buffers: no global load in the move draw
+    uint16_t* s_nb =
+        reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)(blockDim.x >> 5) * a.warp_bytes);
+    for (int k = threadIdx.x; k < a.n * a.K; k += blockDim.x) s_nb[k] = a.nb[k];
+    __syncthreads();
+    nbl = s_nb;
+  }
+  const int wib = threadIdx.x >> 5;
+  const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (chain >= a.chains) return;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem + al16(a.mat_smem) + (size_t)wib * a.warp_bytes);
+  const int n = a.n, lane = threadIdx.x & 31;
+  anneal_ring_chain<T>(
+      a, chain, p, nbl, [&](int r, int c) { return mat_at<T, kSmem>(mat, n, r, c); },
+      [&](const uint16_t* q) { return warp_ring_raw<T, kSmem>(q, n, mat, lane); });
+}
+
+// Ring chains with the matrix spread over a thread-block cluster's shared
+// memory (C CTAs of kRingClusterRows rows each, DSMEM): a proposal's lookups
+// are distributed shared-memory loads instead of L2 gathers, shortening the
+// round trip each iteration waits on.  Same proposal loop, same trajectory.
+constexpr int kRingClusterRows = 64;
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint16_t ld_dsmem_u16(uint32_t laddr, uint32_t rank) {
+  uint32_t raddr, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(rank));
+  asm volatile("ld.shared::cluster.u16 %0, [%1];" : "=r"(v) : "r"(raddr));
+  return (uint16_t)v;
+}
+
+__global__ void __launch_bounds__(256) k_anneal_ring_cluster(AnnealArgs a, const uint16_t* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  const uint32_t rank = cluster_ctarank();
+  const size_t rows_bytes = (size_t)kRingClusterRows * n * 2;
+  {  // this CTA's rows [rank * R, rank * R + R)
+    const uint4* src = reinterpret_cast<const uint4*>(gmat + (size_t)rank * kRingClusterRows * n);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (size_t k = threadIdx.x; k < (rows_bytes >> 4); k += blockDim.x) dst[k] = __ldg(src + k);
+  }
+  const uint16_t* nbl = a.nb;
+  unsigned char* wbase = smem + al16(rows_bytes);
+  if (a.nb_smem) {
+    uint16_t* s_nb = reinterpret_cast<uint16_t*>(wbase + (size_t)(blockDim.x >> 5) * a.warp_bytes);
+    for (int k = threadIdx.x; k < n * a.K; k += blockDim.x) s_nb[k] = a.nb[k];
+    nbl = s_nb;
+  }
+  __syncthreads();
+  cluster_sync_all();  // every CTA's rows are staged
+  const int wib = threadIdx.x >> 5;
+  const int chain = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (chain < a.chains) {
+    uint16_t* p = reinterpret_cast<uint16_t*>(wbase + (size_t)wib * a.warp_bytes);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+    anneal_ring_chain<uint16_t>(
+        a, chain, p, nbl,
+        [&](int r, int c) {
+          return ld_dsmem_u16(base + (uint32_t)(((r & (kRingClusterRows - 1)) * n + c) * 2),
+                              (uint32_t)r / kRingClusterRows);
+        },
+        [&](const uint16_t*) { return 0.0; });
+  }
+  cluster_sync_all();  // peers may still read this CTA's rows
 }
 
 // --------------------------------------------- full-evaluation anneal -----
@@ -1616,6 +1686,52 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   }
   auto fullc = cta_smem_mat ? k_anneal_full_cta<T, true> : k_anneal_full_cta<T, false>;
   if (use_cta) smem_attr(fullc, cta_dyn);
+  // Ring chains on a u16 matrix beyond one CTA, few enough for one wave of
+  // clusters: the matrix spread over a cluster's shared memory (C CTAs of 64
+  // rows, DSMEM lookups) instead of L2 gathers (k_anneal_ring_cluster).
+  AnnealArgs arc = a;
+  cudaLaunchConfig_t rc_cfg = {};
+  cudaLaunchAttribute rc_attr[1];
+  bool use_ring_cluster = false;
+  if (std::is_same<T, uint16_t>::value && plan.model == kRing && !smem_mat && n > 1 && n % kRingClusterRows == 0 &&
+      n / kRingClusterRows >= 2 && n / kRingClusterRows <= 16 && (p.path == RW_PATH_AUTO || p.path == RW_PATH_CLUSTER)) {
+    const int C = n / kRingClusterRows;
+    const size_t ring_wb = 2 * al16((size_t)n * 2);  // p + pos
+    const size_t rows = al16((size_t)kRingClusterRows * n * 2);
+    const size_t nbb = a.nb ? al16((size_t)n * a.K * 2) : 0;
+    auto kc = k_anneal_ring_cluster;
+    cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    const size_t smax = rows + 8 * ring_wb + nbb;
+    int clusters = 0;
+    if (smax <= (size_t)di.smem &&
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax) == cudaSuccess) {
+      rc_cfg.gridDim = dim3(C);
+      rc_cfg.blockDim = dim3(256);
+      rc_cfg.dynamicSmemBytes = smax;
+      rc_attr[0].id = cudaLaunchAttributeClusterDimension;
+      rc_attr[0].val.clusterDim.x = C;
+      rc_attr[0].val.clusterDim.y = 1;
+      rc_attr[0].val.clusterDim.z = 1;
+      rc_cfg.attrs = rc_attr;
+      rc_cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&clusters, (void*)kc, &rc_cfg) != cudaSuccess) clusters = 0;
+    }
+    cudaGetLastError();
+    if (clusters > 0 && (int64_t)chains <= (int64_t)clusters * C * 8) {
+      int cwpb = (int)((chains + (int64_t)clusters * C - 1) / ((int64_t)clusters * C));
+      cwpb = std::max(1, std::min(8, cwpb));
+      const int64_t ctas = (chains + cwpb - 1) / cwpb;
+      const int64_t grid_c = (ctas + C - 1) / C * C;
+      arc.warp_bytes = (int)ring_wb;
+      arc.nb_smem = (int)nbb;
+      arc.mat_smem = 0;
+      rc_cfg.gridDim = dim3((unsigned)grid_c);
+      rc_cfg.blockDim = dim3(cwpb * 32);
+      rc_cfg.dynamicSmemBytes = rows + (size_t)cwpb * ring_wb + nbb;
+      rc_cfg.stream = st;
+      use_ring_cluster = true;
+    }
+  }
   // The tree model with few chains: swaps by delta evaluation (k_anneal_dbt_delta),
   // when its tables fit next to the matrix (or without it).
   bool use_delta = false;
@@ -1642,7 +1758,11 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
     if (Clock::now() >= deadline) break;
     a.level_begin = level;
     a.level_end = std::min(levels, level + per_launch);
-    if (plan.model == kRing) {
+    if (plan.model == kRing && use_ring_cluster) {
+      arc.level_begin = a.level_begin;
+      arc.level_end = a.level_end;
+      RW_CUDA(cudaLaunchKernelEx(&rc_cfg, k_anneal_ring_cluster, arc, static_cast<const uint16_t*>(p.d_mat)));
+    } else if (plan.model == kRing) {
       ring<<<grid, threads, dyn_ring, st>>>(a, static_cast<const T*>(p.d_mat));
     } else if (use_delta) {
       ac.level_begin = a.level_begin;

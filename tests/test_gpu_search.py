@@ -380,3 +380,20 @@ def test_anneal_cta_chains_follow_the_warp_chains_exactly(alg, pair):
     b = prob.anneal(spec, cfg, chains=200, chain_begin=200, chain_total=400)
     best = min([(a[1], a[3]["winner_chain"], a[0].tolist()), (b[1], b[3]["winner_chain"], b[0].tolist())])
     assert best[0] == c_all and best[1] == rep_all["winner_chain"] and best[2] == o_all.tolist()
+
+
+def test_ring_anneal_cluster_matrix_follows_the_l2_chains_exactly():
+    """Ring chains on a u16 matrix beyond one CTA (C4) run with the matrix
+    spread over a thread-block cluster's shared memory (DSMEM lookups,
+    k_anneal_ring_cluster) when few chains fit one wave; forcing the L2 path
+    must give the same winner, cost and order (same Philox streams, same
+    arithmetic)."""
+    m = fixtures.config_matrix("C4", "fixed")
+    spec = fixtures.ring_spec(1024, fixtures.SIZE_FIXED)
+    cfg = rw.SolverConfig(seed=5, budget=1e6, steps_per_temperature=16)
+    auto, l2 = rw.Problem(m), rw.Problem(m)
+    l2.set_path("l2")
+    oa, ca, ea, ra = auto.anneal(spec, cfg, chains=148, schedule="calibrated")
+    ob, cb, eb, rb = l2.anneal(spec, cfg, chains=148, schedule="calibrated")
+    assert ca == cb and ea == eb and ra["winner_chain"] == rb["winner_chain"] and oa.tolist() == ob.tolist()
+    assert ca == Port().evaluate(m, oa.astype(np.int32), make_spec(0, 1024, fixtures.SIZE_FIXED))
