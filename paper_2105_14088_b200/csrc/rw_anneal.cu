@@ -1686,15 +1686,19 @@ AnnealResult anneal_typed(Problem& p, const EvalPlan& plan, const rw_solver_conf
   }
   auto fullc = cta_smem_mat ? k_anneal_full_cta<T, true> : k_anneal_full_cta<T, false>;
   if (use_cta) smem_attr(fullc, cta_dyn);
-  // Ring chains on a u16 matrix beyond one CTA, few enough for one wave of
-  // clusters: the matrix spread over a cluster's shared memory (C CTAs of 64
-  // rows, DSMEM lookups) instead of L2 gathers (k_anneal_ring_cluster).
+  // Opt-in (rw_problem_set_path RW_PATH_CLUSTER): ring chains on a u16 matrix
+  // beyond one CTA, few enough for one wave of clusters, with the matrix
+  // spread over a cluster's shared memory (C CTAs of 64 rows, DSMEM lookups)
+  // instead of L2 gathers (k_anneal_ring_cluster).  Measured on B200 at C4,
+  // 592 chains: 1.16e9 proposals/s against 1.70e9 for the L2 kernel -- a
+  // DSMEM random load costs about an L2 hit, and the 16-CTA clusters fit on
+  // 112 of 148 SMs -- so AUTO keeps the L2 kernel.
   AnnealArgs arc = a;
   cudaLaunchConfig_t rc_cfg = {};
   cudaLaunchAttribute rc_attr[1];
   bool use_ring_cluster = false;
   if (std::is_same<T, uint16_t>::value && plan.model == kRing && !smem_mat && n > 1 && n % kRingClusterRows == 0 &&
-      n / kRingClusterRows >= 2 && n / kRingClusterRows <= 16 && (p.path == RW_PATH_AUTO || p.path == RW_PATH_CLUSTER)) {
+      n / kRingClusterRows >= 2 && n / kRingClusterRows <= 16 && p.path == RW_PATH_CLUSTER) {
     const int C = n / kRingClusterRows;
     const size_t ring_wb = 2 * al16((size_t)n * 2);  // p + pos
     const size_t rows = al16((size_t)kRingClusterRows * n * 2);

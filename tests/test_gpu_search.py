@@ -383,15 +383,15 @@ def test_anneal_cta_chains_follow_the_warp_chains_exactly(alg, pair):
 
 
 def test_ring_anneal_cluster_matrix_follows_the_l2_chains_exactly():
-    """Ring chains on a u16 matrix beyond one CTA (C4) run with the matrix
-    spread over a thread-block cluster's shared memory (DSMEM lookups,
-    k_anneal_ring_cluster) when few chains fit one wave; forcing the L2 path
-    must give the same winner, cost and order (same Philox streams, same
-    arithmetic)."""
+    """Opt-in cluster path: ring chains on a u16 matrix beyond one CTA (C4)
+    with the matrix spread over a thread-block cluster's shared memory (DSMEM
+    lookups, k_anneal_ring_cluster); the L2 path must give the same winner,
+    cost and order (same Philox streams, same arithmetic)."""
     m = fixtures.config_matrix("C4", "fixed")
     spec = fixtures.ring_spec(1024, fixtures.SIZE_FIXED)
     cfg = rw.SolverConfig(seed=5, budget=1e6, steps_per_temperature=16)
     auto, l2 = rw.Problem(m), rw.Problem(m)
+    auto.set_path("cluster")
     l2.set_path("l2")
     oa, ca, ea, ra = auto.anneal(spec, cfg, chains=148, schedule="calibrated")
     ob, cb, eb, rb = l2.anneal(spec, cfg, chains=148, schedule="calibrated")
