@@ -237,6 +237,18 @@ class ProblemSet:
                                         o.shape[0], ptr(out, C.c_double), flags))
         return out
 
+    def evaluate_batch_packed(self, spec: "CollectiveSpec", packed: np.ndarray, bits: int, batch: int,
+                              exact: bool = False, validate: bool = True) -> np.ndarray:
+        """Packed host orders (pack_orders), one slice per device."""
+        p = np.ascontiguousarray(packed)
+        if p.nbytes < packed_row_bytes(spec.n, bits) * batch:
+            raise DomainError("packed buffer too small")
+        out = np.empty(batch, dtype=np.float64)
+        flags = (_lib.RW_EVAL_EXACT if exact else 0) | (0 if validate else _lib.RW_EVAL_NO_VALIDATE)
+        check(lib.rw_evaluate_batch_set(self._h, C.byref(spec._c()), C.c_void_p(p.ctypes.data), 0, bits, batch,
+                                        ptr(out, C.c_double), flags))
+        return out
+
     def brute_force(self, spec: "CollectiveSpec", threshold: int = 10) -> "Solution":
         perm = np.empty(spec.n, dtype=np.int32)
         cost = C.c_double()

@@ -64,6 +64,7 @@ def test_set_batch_scoring_splits_one_host_batch():
         s = rw.api.ProblemSet(m, devices=list(range(k)))
         assert np.array_equal(s.evaluate_batch(spec, o), want)
         assert np.array_equal(s.evaluate_batch(spec, o.astype(np.uint16)), want)
+        assert np.array_equal(s.evaluate_batch_packed(spec, rw.api.pack_orders(o, 10), 10, len(o)), want)
         bad = o[:4000].copy()
         bad[3333, 5] = bad[3333, 6]
         with pytest.raises(rw.DomainError, match="batch entry 3333"):
