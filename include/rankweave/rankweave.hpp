@@ -221,6 +221,10 @@ struct GpuOptions {
   // in-process NCCL communicator; 0: every visible device.  Results do not
   // depend on the device count for a fixed `chains`.
   int num_devices = 1;
+  // > 0: evaluate() is served by a resident evaluator on the device (one CTA
+  // that polls a mapped mailbox; no kernel launch per call), which leaves
+  // after this many microseconds without a call.  See rw_problem_set_resident.
+  int resident_idle_us = 0;
 };
 void set_gpu_options(const GpuOptions& opts);
 GpuOptions gpu_options();

@@ -32,7 +32,8 @@
 extern "C" {
 #endif
 
-#define RW_ABI_VERSION 2  /* 2: uint16 / packed host orders, device sets (NCCL), host logic, GPU options, Philox samplers */
+#define RW_ABI_VERSION 3  /* 2: uint16 / packed host orders, device sets (NCCL), host logic, GPU options, Philox samplers;
+                             3: resident evaluator (rw_problem_set_resident, rw_gpu_options.resident_idle_us) */
 
 typedef enum rw_status {
   RW_OK = 0,
@@ -169,6 +170,16 @@ rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out);
 enum { RW_PATH_AUTO = 0, RW_PATH_L2_GATHER = 1, RW_PATH_CLUSTER = 2, RW_PATH_TRANSPOSE = 3 };
 rw_status rw_problem_set_path(rw_problem* p, int32_t path);
 
+/* Resident evaluator for single-order rw_evaluate calls (N <= 4096): one CTA
+ * stays resident on the problem's device and serves them through a mailbox in
+ * mapped pinned host memory, so a call costs no kernel launch (B200, N=64:
+ * ~6 us instead of ~13 us).  The CTA leaves after idle_us without a call (at
+ * most 100000; and after 5 ms of continuous use, relaunched transparently), so
+ * a device-wide synchronisation elsewhere waits at most that long.
+ * idle_us <= 0 stops it.  Results are bit-identical to the launched path; a
+ * call made while another thread holds the server takes the launched path. */
+rw_status rw_problem_set_resident(rw_problem* p, int32_t idle_us);
+
 /* ---- cost model (cost_model.hpp:28-36) --------------------------------- */
 /* evaluate(m, order, spec): reference-identical bits for every matrix. */
 rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* perm, double* cost);
@@ -300,6 +311,7 @@ typedef struct rw_gpu_options {
   int32_t exact_batch;         /* evaluate_batch with the reference's summation order */
   int32_t immutable_matrices;  /* cache device matrices by address, not content */
   int32_t num_devices;         /* > 1 (0: all visible): device sets with in-process NCCL */
+  int32_t resident_idle_us;    /* > 0: evaluate() through a resident evaluator (rw_problem_set_resident) */
 } rw_gpu_options;
 rw_status rw_set_gpu_options(const rw_gpu_options* opts);
 rw_status rw_get_gpu_options(rw_gpu_options* out);

@@ -32,8 +32,12 @@ static CostMatrix matrix_for(int n) {
 
 int main(int argc, char** argv) {
 #ifdef RW_B200
+  // modes: (none) content-keyed matrix cache; "immutable": address-keyed;
+  // "resident": address-keyed + resident evaluator (rw_problem_set_resident)
   GpuOptions o = gpu_options();
-  o.immutable_matrices = argc > 1 && std::string(argv[1]) == "immutable";
+  const std::string mode = argc > 1 ? argv[1] : "";
+  o.immutable_matrices = mode == "immutable" || mode == "resident";
+  o.resident_idle_us = mode == "resident" ? 2000 : 0;
   set_gpu_options(o);
 #else
   (void)argc;

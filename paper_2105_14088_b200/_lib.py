@@ -54,7 +54,8 @@ class rw_search_report(C.Structure):
 
 class rw_gpu_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("chains", C.c_int32), ("exact_batch", C.c_int32),
-                ("immutable_matrices", C.c_int32), ("num_devices", C.c_int32)]
+                ("immutable_matrices", C.c_int32), ("num_devices", C.c_int32),
+                ("resident_idle_us", C.c_int32)]
 
 
 class rw_eval_report(C.Structure):
@@ -110,6 +111,7 @@ SIGNATURES = {
     "rw_anneal_set": (C.c_int, [_vp, P(rw_spec), P(rw_solver_config), P(rw_gpu_config), _i32p, _dp, _u64p,
                                 P(rw_search_report)]),
     "rw_set_gpu_options": (C.c_int, [P(rw_gpu_options)]),
+    "rw_problem_set_resident": (C.c_int, [_vp, C.c_int32]),
     "rw_get_gpu_options": (C.c_int, [P(rw_gpu_options)]),
     "rw_distribution_stats": (C.c_int, [_dp, C.c_int64, _dp]),
     "rw_spearman": (C.c_int, [_dp, _dp, C.c_int64, C.c_int64, _dp]),

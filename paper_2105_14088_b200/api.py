@@ -100,6 +100,12 @@ class Problem:
         'auto' (default), 'l2' (random L2 gathers), 'cluster' (DSMEM routing), 'transpose'."""
         check(lib.rw_problem_set_path(self._h, {"auto": 0, "l2": 1, "cluster": 2, "transpose": 3}[path]))
 
+    def set_resident(self, idle_us: int) -> None:
+        """Serve single-order evaluate() calls from a resident CTA on the device
+        (no kernel launch per call) that leaves after idle_us without a call;
+        0 stops it (rw_problem_set_resident)."""
+        check(lib.rw_problem_set_resident(self._h, int(idle_us)))
+
     def close(self):
         if getattr(self, "_h", None):
             lib.rw_problem_destroy(self._h)
@@ -110,6 +116,14 @@ class Problem:
             self.close()
         except Exception:
             pass
+
+    def evaluate(self, spec: "CollectiveSpec", perm) -> float:
+        """One order through rw_evaluate (the reference's evaluate(); served by
+        the resident evaluator when set_resident is on)."""
+        p = np.ascontiguousarray(perm, dtype=np.int32)
+        out = C.c_double()
+        check(lib.rw_evaluate(self._h, C.byref(spec._c()), ptr(p, C.c_int32), C.byref(out)))
+        return out.value
 
     # batch scoring ---------------------------------------------------------
     def evaluate_batch(self, spec: "CollectiveSpec", orders: np.ndarray, exact: bool = False,

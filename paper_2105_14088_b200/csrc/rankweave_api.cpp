@@ -77,7 +77,7 @@ struct ProblemRef {
 // GpuOptions::immutable_matrices the key is the storage address and size.
 class ProblemCache {
  public:
-  ProblemRef get(const CostMatrix& m, int device, bool by_address) {
+  ProblemRef get(const CostMatrix& m, int device, bool by_address, int resident_us) {
     std::lock_guard<std::mutex> lock(mu_);
     const std::size_t bytes = m.rtt_us.size() * sizeof(double);
     const void* addr = m.rtt_us.data();
@@ -87,13 +87,19 @@ class ProblemCache {
                                   : (!it->shadow.empty() && same_bytes(it->shadow.data(), addr, bytes));
       if (hit) {
         entries_.splice(entries_.begin(), entries_, it);
-        return ProblemRef{entries_.front().problem};
+        Entry& e = entries_.front();
+        if (e.resident_us != resident_us) {
+          check(rw_problem_set_resident(e.problem.get(), resident_us));
+          e.resident_us = resident_us;
+        }
+        return ProblemRef{e.problem};
       }
     }
     rw_problem* raw = nullptr;
     check(rw_problem_create(m.rtt_us.data(), m.n(), RW_STORAGE_AUTO, device, &raw));
     std::shared_ptr<rw_problem> p(raw, [](rw_problem* q) { rw_problem_destroy(q); });
-    Entry e{m.n(), device, m.rtt_us.size(), addr, by_address, {}, p};
+    if (resident_us > 0) check(rw_problem_set_resident(raw, resident_us));
+    Entry e{m.n(), device, m.rtt_us.size(), addr, by_address, {}, p, resident_us};
     if (!by_address) e.shadow = m.rtt_us;
     entries_.push_front(std::move(e));
     total_ += bytes;
@@ -113,6 +119,7 @@ class ProblemCache {
     bool by_address;
     std::vector<double> shadow;
     std::shared_ptr<rw_problem> problem;
+    int resident_us = 0;
   };
   std::mutex mu_;
   std::list<Entry> entries_;
@@ -128,7 +135,7 @@ ProblemRef device_problem(const CostMatrix& m) {
   if (m.rtt_us.size() != static_cast<std::size_t>(m.n()) * static_cast<std::size_t>(m.n()))
     throw domain_error("cost matrix storage is not n*n");
   const GpuOptions o = gpu_options();
-  return cache().get(m, o.device, o.immutable_matrices);
+  return cache().get(m, o.device, o.immutable_matrices, m.n() <= 4096 ? o.resident_idle_us : 0);
 }
 
 // Device sets (GpuOptions::num_devices != 1), cached by exact content like

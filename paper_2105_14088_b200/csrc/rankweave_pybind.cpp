@@ -133,7 +133,8 @@ PYBIND11_MODULE(_rankweave_cpp, mod) {
       .def_readwrite("chains", &rw::GpuOptions::chains)
       .def_readwrite("exact_batch", &rw::GpuOptions::exact_batch)
       .def_readwrite("immutable_matrices", &rw::GpuOptions::immutable_matrices)
-      .def_readwrite("num_devices", &rw::GpuOptions::num_devices);
+      .def_readwrite("num_devices", &rw::GpuOptions::num_devices)
+      .def_readwrite("resident_idle_us", &rw::GpuOptions::resident_idle_us);
   mod.def("set_gpu_options", &rw::set_gpu_options);
   mod.def("gpu_options", &rw::gpu_options);
   mod.def("sample_orders", &rw::sample_orders);

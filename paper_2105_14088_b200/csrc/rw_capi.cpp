@@ -161,7 +161,15 @@ rw_status rw_evaluate(const rw_problem* p, const rw_spec* spec, const int32_t* p
     rwb::Problem& q = get(p);
     const rwb::EvalPlan plan = rwb::make_plan(q, *spec);
     validate_host_order(perm, spec->n, spec->n);  // host check done: no device error read-back
-    rwb::evaluate_host_orders(q, plan, perm, 1, cost, /*exact=*/true, /*validate=*/false, nullptr);
+    if (!rwb::resident_evaluate(q, plan, perm, cost))
+      rwb::evaluate_host_orders(q, plan, perm, 1, cost, /*exact=*/true, /*validate=*/false, nullptr);
+  });
+}
+
+rw_status rw_problem_set_resident(rw_problem* p, int32_t idle_us) {
+  return guarded([&] {
+    rwb::Problem& q = get(p);
+    rwb::resident_configure(q, idle_us);
   });
 }
 
@@ -658,6 +666,7 @@ rw_status rw_set_gpu_options(const rw_gpu_options* opts) {
     o.exact_batch = opts->exact_batch != 0;
     o.immutable_matrices = opts->immutable_matrices != 0;
     o.num_devices = opts->num_devices;
+    o.resident_idle_us = opts->resident_idle_us;
     rankweave::set_gpu_options(o);
   });
 }
@@ -671,6 +680,7 @@ rw_status rw_get_gpu_options(rw_gpu_options* out) {
     out->exact_batch = o.exact_batch ? 1 : 0;
     out->immutable_matrices = o.immutable_matrices ? 1 : 0;
     out->num_devices = o.num_devices;
+    out->resident_idle_us = o.resident_idle_us;
   });
 }
 

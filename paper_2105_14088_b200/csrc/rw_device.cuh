@@ -140,5 +140,25 @@ struct Philox {
   }
 };
 
+// Ascending bitonic sort of np2 (a power of two) doubles by the whole CTA
+// (the sorted_sum order of cost_model.cpp:38-43; +inf pads sort last).
+__device__ inline void bitonic_sort_block(double* v, int np2) {
+  for (int k = 2; k <= np2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double x = v[i], y = v[ixj];
+          const bool up = (i & k) == 0;
+          if (up ? (x > y) : (x < y)) {
+            v[i] = y;
+            v[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
 }  // namespace dev
 }  // namespace rwb

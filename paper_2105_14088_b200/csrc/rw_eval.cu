@@ -484,24 +484,6 @@ __global__ void __launch_bounds__(1024) k_dbt(KArgs a, DbtArgs d, const P* __res
 // One CTA per order: hops fl(rtt * S) into a power-of-two buffer padded with
 // +inf, bitonic sort ascending, then one thread sums serially -- the exact
 // operation sequence of sorted_sum (cost_model.cpp:38-43).
-__device__ void bitonic_sort_block(double* v, int np2) {
-  for (int k = 2; k <= np2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const double x = v[i], y = v[ixj];
-          const bool up = (i & k) == 0;
-          if (up ? (x > y) : (x < y)) {
-            v[i] = y;
-            v[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
 
 template <typename T, typename P, bool kValidate>
 __global__ void __launch_bounds__(256) k_ring_exact(KArgs a, const P* __restrict__ perms, const T* __restrict__ gmat,

@@ -67,6 +67,8 @@ struct DbtPlan {
   const int32_t* d_posedges() const { return d_aux + edges; }
 };
 
+struct ResidentServer;  // rw_resident.cu
+
 struct Problem {
   int n = 0;
   int device = 0;
@@ -91,6 +93,8 @@ struct Problem {
   uint32_t* d_rank = nullptr;
   double* d_rank_vals = nullptr;
   uint32_t zero_rank = 0;
+  // Resident evaluator for single-order calls (rw_problem_set_resident).
+  ResidentServer* resident = nullptr;
   size_t elem_bytes() const { return storage == RW_STORAGE_U16 ? 2 : storage == RW_STORAGE_F32 ? 4 : 8; }
 };
 
@@ -268,6 +272,13 @@ void evaluate_host_orders_fmt(Problem& p, const EvalPlan& plan, const void* perm
 int64_t packed_row_bytes(int n, int bits);
 
 // Scores host orders and returns reference-exact costs (used by search code).
+// Resident evaluator (rw_resident.cu): idle_us <= 0 stops and frees it.
+constexpr int kResidentMaxN = 4096;
+void resident_configure(Problem& p, int idle_us);
+void resident_release(Problem& p);
+// false: not configured, or busy with another thread (use the launched path)
+bool resident_evaluate(Problem& p, const EvalPlan& plan, const int32_t* perm, double* cost);
+
 void evaluate_host_orders(Problem& p, const EvalPlan& plan, const int32_t* perms, int64_t batch, double* costs,
                           bool exact, bool validate, rw_eval_report* report);
 

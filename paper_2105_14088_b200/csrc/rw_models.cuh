@@ -171,5 +171,103 @@ __device__ double warp_ring_raw(const uint16_t* s_perm, int n, const T* mat, int
   }
 }
 
+// Double binary tree critical path by a CTA of kCta threads: each depth's
+// edges are spread over the CTA, values in shared memory (vals: `edges`
+// doubles, or uint32 in the exact integer form).  Same per-edge operation
+// sequence and final max as warp_dbt_cost, so the value is bit-identical.
+template <int kCta, typename T, bool kSmem>
+__device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d,
+                                               double scale, double* vals) {
+  if (n <= 1) return 0.0;
+  if constexpr (std::is_same<T, uint16_t>::value) {
+    if (d.int_mode) {
+      uint32_t* iv = reinterpret_cast<uint32_t*>(vals);
+      for (int depth = d.depths - 1; depth >= 0; --depth) {
+        const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 2
+        for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
+          const int4 r = d.rec[e];
+          const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
+          uint32_t sub = 0;
+          if (r.z >= 0) {
+            const uint32_t x = iv[r.z], y = iv[r.w];
+            sub = x > y ? x : y;
+          }
+          iv[e] = c + sub;
+        }
+        __syncthreads();
+      }
+      const int top = d.depth_off[1];
+      uint32_t best = iv[0];
+      for (int e = 1; e < top; ++e) best = iv[e] > best ? iv[e] : best;
+      return __dmul_rn((double)best, d.w);
+    }
+  }
+  for (int depth = d.depths - 1; depth >= 0; --depth) {
+    const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
+#pragma unroll 2
+    for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
+      const int4 r = d.rec[e];
+      double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
+      if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
+      const double sub = r.z >= 0 ? ref_max(vals[r.z], vals[r.w]) : 0.0;
+      vals[e] = __dadd_rn(c, sub);
+    }
+    __syncthreads();
+  }
+  const int top = d.depth_off[1];
+  double best = vals[0];
+  for (int e = 1; e < top; ++e) best = ref_max(best, vals[e]);
+  return best;
+}
+
+// Sum over rounds of the round maximum by a CTA of kCta threads; red holds
+// 2 * kCta / 32 entries.  The per-round maximum of raw codes is
+// exact under any grouping (no NaN survives the running max from 0), and the
+// rounds are summed in order, so the value equals warp_rounds_cost's.
+template <int kCta, typename T, bool kSmem>
+__device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n, const T* mat, const RoundsArgs& r,
+                                                  double scale, typename MaxAcc<T>::type* red) {
+  using Acc = typename MaxAcc<T>::type;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  double total = 0.0;
+  long long stride = 1;
+  for (int rd = 0; rd < r.rounds; ++rd) {
+    Acc mx = Acc(0);
+    if (r.kind == 0) {
+      const int s = 1 << rd;
+      for (int j = t; j < (n >> 1); j += kCta)
+        mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
+    } else if (r.kind == 1) {
+      const int s = 1 << rd;
+      if (r.sym && n >= 2 * kCta) {  // each unordered pair once (warp_rounds_cost); small n: all lanes busy anyway
+        for (int k = t; k < (n >> 1); k += kCta) {
+          const int j = ((k >> rd) << (rd + 1)) | (k & (s - 1));
+          mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j + s]));
+        }
+      } else {
+        for (int j = t; j < n; j += kCta) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, s_perm[j], s_perm[j ^ s]));
+      }
+    } else {
+      const int st = (int)stride;  // j + (B-1)*B^i <= N-1: no modulo (warp_rounds_cost)
+      for (int j = t; j < n / r.b; j += kCta) {
+        const int a = s_perm[j];
+        for (int k = 1; k < r.b; ++k) mx = ref_max<Acc>(mx, (Acc)mat_at<T, kSmem>(mat, n, a, s_perm[j + k * st]));
+      }
+      stride *= r.b;
+    }
+    mx = warp_max(mx);
+    if (lane == 0) red[(rd & 1) * (kCta / 32) + w] = mx;  // double-buffered by round parity
+    __syncthreads();
+    Acc m = red[(rd & 1) * (kCta / 32)];
+#pragma unroll
+    for (int k = 1; k < kCta / 32; ++k) m = ref_max<Acc>(m, red[(rd & 1) * (kCta / 32) + k]);
+    double rm = to_double((T)m, scale);
+    if (r.mode == RW_LATENCY_TIMES_SIZE) rm = __dmul_rn(rm, r.bytes[rd]);
+    total = __dadd_rn(total, rm);
+  }
+  return total;
+}
+
 }  // namespace dev
 }  // namespace rwb

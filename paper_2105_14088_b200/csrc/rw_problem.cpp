@@ -620,6 +620,7 @@ static Problem* replica_problem(const Problem& src, int device) {
 
 static void destroy_problem(Problem* p) {
   if (!p) return;
+  resident_release(*p);
   {
     DeviceGuard g(p->device);
     cudaDeviceSynchronize();

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_device_query():
-    assert _lib.lib.rw_abi_version() == 2
+    assert _lib.lib.rw_abi_version() == 3
     assert rw.device_count() >= 0
 
 
