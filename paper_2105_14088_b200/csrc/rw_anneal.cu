@@ -822,10 +822,6 @@ struct DbtDelta {
     if constexpr (std::is_same<V, uint32_t>::value) return __dmul_rn((double)best, d.w);
     else return best;
   }
-  __device__ static V top_max(V a, V b) {
-    if constexpr (std::is_same<V, uint32_t>::value) return b > a ? b : a;
-    else return ref_max(a, b);
-  }
 };
 
 template <typename T, typename V, bool kSmem>
@@ -843,8 +839,7 @@ __device__ __forceinline__ double cta_dbt_full(const uint16_t* s_perm, int n, co
     }
     __syncthreads();
   }
-  V best = val[0];
-  for (int e = 1; e < doff[1]; ++e) best = D::top_max(best, val[e]);
+  const V best = dbt_top_max<V>(doff[1], [&](int e) { return val[e]; });
   return D::finish(best, d);
 }
 
@@ -951,8 +946,7 @@ __global__ void __launch_bounds__(kCta) k_anneal_dbt_delta(AnnealArgs a, const T
             }
             __syncwarp();
           }
-          V bv = vmark[0] == gen ? nval[0] : val[0];
-          for (int e = 1; e < top; ++e) bv = D::top_max(bv, vmark[e] == gen ? nval[e] : val[e]);
+          const V bv = dbt_top_max<V>(top, [&](int e) { return vmark[e] == gen ? nval[e] : val[e]; });
           if (t == 0) s_cost = D::finish(bv, d);
         }
         __syncthreads();

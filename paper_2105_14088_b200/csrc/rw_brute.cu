@@ -239,9 +239,7 @@ __device__ double eval_exact(const GenericArgs& a, const double* m, const int* p
         const double sub = a.dbt_c0[e] >= 0 ? ref_max(val[a.dbt_c0[e]], val[a.dbt_c1[e]]) : 0.0;
         val[e] = __dadd_rn(c, sub);
       }
-    double best = val[0];
-    for (int e = 1; e < a.dbt_off[1]; ++e) best = ref_max(best, val[e]);
-    return best;
+    return dbt_top_max<double>(a.dbt_off[1], [&](int e) { return val[e]; });
   }
   double total = 0.0;
   long long stride = 1;

@@ -21,6 +21,19 @@ __device__ __forceinline__ T ref_max(T a, T b) {
   return (a < b) ? b : a;
 }
 
+// The tree model's cost over its top edges.  For n >= 2 there are four, in
+// plan order {primary left, primary right, mirrored left, mirrored right}:
+// max(max(L0, R0), max(L1, R1)), the reference's std::max nesting
+// (cost_model.cpp:112, 115).  A left-to-right fold differs from it when a
+// path value is NaN, because std::max keeps its first argument then.
+template <typename V, typename Get>
+__device__ __forceinline__ V dbt_top_max(int top, Get v) {
+  if (top == 4) return ref_max(ref_max(v(0), v(1)), ref_max(v(2), v(3)));
+  V b = v(0);
+  for (int e = 1; e < top; ++e) b = ref_max(b, v(e));
+  return b;
+}
+
 template <typename T>
 __device__ __forceinline__ T ld_matrix(const T* __restrict__ m, size_t idx) {
   return __ldg(m + idx);

@@ -427,12 +427,10 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
       const int top = __ldg(d.depth_off + 1);
       double best;
       if (im) {
-        uint32_t b = iv[0];
-        for (int e = 1; e < top; ++e) b = iv[e] > b ? iv[e] : b;
+        const uint32_t b = dbt_top_max<uint32_t>(top, [&](int e) { return iv[e]; });
         best = __dmul_rn((double)b, d.w);
       } else {
-        best = dv[0];
-        for (int e = 1; e < top; ++e) best = ref_max(best, dv[e]);
+        best = dbt_top_max<double>(top, [&](int e) { return dv[e]; });
       }
       costs[o] = best;
       if (kValidate && s_bad) report_bad_order(a.err, n, o);

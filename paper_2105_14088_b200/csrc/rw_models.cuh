@@ -129,9 +129,7 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
         }
         __syncwarp();
       }
-      const int top = d.depth_off[1];
-      uint32_t best = iv[0];
-      for (int e = 1; e < top; ++e) best = iv[e] > best ? iv[e] : best;
+      const uint32_t best = dbt_top_max<uint32_t>(d.depth_off[1], [&](int e) { return iv[e]; });
       __syncwarp();
       return __dmul_rn((double)best, d.w);
     }
@@ -149,9 +147,7 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
     }
     __syncwarp();
   }
-  const int top = d.depth_off[1];
-  double best = vals[0];
-  for (int e = 1; e < top; ++e) best = ref_max(best, vals[e]);
+  const double best = dbt_top_max<double>(d.depth_off[1], [&](int e) { return vals[e]; });
   __syncwarp();
   return best;
 }
@@ -197,9 +193,7 @@ __device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, co
         }
         __syncthreads();
       }
-      const int top = d.depth_off[1];
-      uint32_t best = iv[0];
-      for (int e = 1; e < top; ++e) best = iv[e] > best ? iv[e] : best;
+      const uint32_t best = dbt_top_max<uint32_t>(d.depth_off[1], [&](int e) { return iv[e]; });
       return __dmul_rn((double)best, d.w);
     }
   }
@@ -215,9 +209,7 @@ __device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, co
     }
     __syncthreads();
   }
-  const int top = d.depth_off[1];
-  double best = vals[0];
-  for (int e = 1; e < top; ++e) best = ref_max(best, vals[e]);
+  const double best = dbt_top_max<double>(d.depth_off[1], [&](int e) { return vals[e]; });
   return best;
 }
 

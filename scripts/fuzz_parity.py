@@ -4,7 +4,9 @@ symmetric or not, optionally with NaN, negative and -0.0 entries), random
 orders, every model and kernel path, against the oracle port.  Bit-exact for
 every max-based model and for ring on fixed point; ring on FP32/FP64 within
 1e-12 relative (the reference's own summation order is reproduced only by
-the exact mode, which is checked too).
+the exact mode, which is checked too).  Single-order evaluate() calls go
+through the resident evaluator (rw_problem_set_resident) and are held to the
+reference bits.
 
     python scripts/fuzz_parity.py [seconds]
 """
@@ -76,6 +78,20 @@ def main():
                         print(f"MISMATCH n={n} kind={kind} sym={sym} dirty={dirty} alg={alg} b={b} pair={pair} "
                               f"mode={mode} path={path} batch={len(perms)} rows={bad[:5].tolist()} "
                               f"got={got[bad[:3]].tolist()} want={want[bad[:3]].tolist()}", flush=True)
+        # single-order evaluate() through the resident evaluator (exact path)
+        res = rw.Problem(m)
+        res.set_resident(300)
+        for alg, b, pair in models:
+            for mode in (1, 0):
+                spec = rw.CollectiveSpec(rw.Algorithm(alg), n, 2.0 ** 17, b, rw.CostMode(mode), rw.HdPairing(pair))
+                want = port.evaluate_batch(m, perms[:2], make_spec(alg, n, 2.0 ** 17, b, mode, pair))
+                got = np.array([res.evaluate(spec, perms[k]) for k in range(min(2, len(perms)))])
+                cases += 1
+                if not np.array_equal(got, want[:len(got)], equal_nan=True):
+                    fails += 1
+                    print(f"RESIDENT MISMATCH n={n} kind={kind} sym={sym} dirty={dirty} alg={alg} b={b} "
+                          f"pair={pair} mode={mode} got={got.tolist()} want={want.tolist()}", flush=True)
+        res.close()
         del probs
     print(f"fuzz: {cases} comparisons, {fails} mismatches, {time.time() - t0:.0f} s", flush=True)
     return 1 if fails else 0

@@ -576,6 +576,31 @@ def test_unvalidated_matrices_nan_and_negative(port, path):
         np.testing.assert_array_equal(got, want)  # NaN positions must agree too
 
 
+@pytest.mark.parametrize("n", [8, 16, 256, 2048])
+def test_tree_model_nan_top_combine(port, n):
+    """The tree model's cost is max(max(L0, R0), max(L1, R1)) over the two
+    trees' root edges (cost_model.cpp:112, 115).  std::max keeps its first
+    argument when either side is NaN, so with NaN path values a left-to-right
+    fold over the four root edges gives a different cost; found by the fuzz
+    sweep (scripts/fuzz_parity.py).  Few NaN entries, so that only some root
+    paths are NaN, on every tree-model kernel: per-warp (batch of 3 and of 400),
+    CTA per order (N=2048, batch >= 2 x SMs), the resident evaluator."""
+    rng = np.random.default_rng(n)
+    m = rng.random((n, n)) * 50.0
+    frac = {8: 0.04, 16: 0.03, 256: 0.002, 2048: 0.0002}[n]
+    m[rng.random((n, n)) < frac] = np.nan
+    prob = rw.Problem(m)
+    perms = np.stack([rng.permutation(n) for _ in range(400)]).astype(np.int32)
+    spec = rw.CollectiveSpec(rw.Algorithm.DoubleBinaryTree, n, 1e6)
+    want = port.evaluate_batch(m, perms, make_spec(2, n, 1e6, 2, 1, 0))
+    assert 0 < np.isnan(want).sum() < len(want) or n == 2048
+    np.testing.assert_array_equal(prob.evaluate_batch(spec, perms), want)
+    np.testing.assert_array_equal(prob.evaluate_batch(spec, perms[:3]), want[:3])
+    prob.set_resident(300)
+    np.testing.assert_array_equal(np.array([prob.evaluate(spec, p) for p in perms[:8]]), want[:8])
+    prob.set_resident(0)
+
+
 def test_device_calls_on_separate_streams_and_host_calls_do_not_share_scratch():
     """rw_evaluate_batch_device takes its exchange buffers from the
     stream-ordered allocator on the caller's stream: two device calls in
