@@ -21,6 +21,7 @@
 //    sorted hops, serial sum).
 #include <algorithm>
 #include <cmath>
+#include <vector>
 #include <cstring>
 
 #include "rw_device.cuh"
@@ -369,6 +370,15 @@ void unrank(const rw_spec& s, uint64_t index, int32_t* perm) {
     perm[pinned + i] = rem[static_cast<size_t>(d)];
     rem.erase(rem.begin() + d);
   }
+}
+
+uint64_t brute_force_resolve(Problem& p, const EvalPlan& plan, const rw_spec& s, uint64_t index) {
+  if (index >= brute_force_space(s)) return 0;
+  std::vector<int32_t> first(static_cast<size_t>(s.n));
+  unrank(s, 0, first.data());
+  double c0 = 0.0;
+  evaluate_host_orders(p, plan, first.data(), 1, &c0, true, false, nullptr);
+  return std::isnan(c0) ? 0 : index;
 }
 
 void brute_force_range(const Problem& p, const EvalPlan& plan, uint64_t first, uint64_t count, double* cost_out,

@@ -333,6 +333,7 @@ rw_status rw_brute_force(const rw_problem* p, const rw_spec* spec, int32_t thres
     double cost = 0.0;
     uint64_t index = 0;
     rwb::brute_force_range(q, plan, 0, space, &cost, &index);
+    index = rwb::brute_force_resolve(q, plan, *spec, index);
     rwb::unrank(*spec, index, perm_out);
     // Reported cost is the reference-identical evaluation of the winner.
     rwb::evaluate_host_orders(q, plan, perm_out, 1, cost_out, true, true, nullptr);

@@ -215,6 +215,11 @@ void brute_force_range(const Problem& p, const EvalPlan& plan, uint64_t first, u
                        uint64_t* index_out);
 uint64_t brute_force_space(const rw_spec& s);
 void unrank(const rw_spec& s, uint64_t index, int32_t* perm_out);
+// Best::offer (solver.cpp:34-46, 73-105): the first order of the enumeration is
+// taken unconditionally and later ones only when c < best.  So when its cost is
+// NaN, or no order costs less than +inf (argmin index ~0), it is the answer.
+// `index` is the argmin over the whole space; returns the reference's index.
+uint64_t brute_force_resolve(Problem& p, const EvalPlan& plan, const rw_spec& s, uint64_t index);
 
 // Simulated annealing and local search.
 struct AnnealResult {

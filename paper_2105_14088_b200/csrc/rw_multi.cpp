@@ -366,9 +366,10 @@ void brute_force_set(ProblemSet& s, const rw_spec& spec, int32_t* perm_out, doub
     const Reduce r = read_reduce(s, 0);
     index = r.key;
   }
-  unrank(spec, index, perm_out);
   Problem& m0 = *s.members[0];
   const EvalPlan plan = make_plan(m0, spec);
+  index = brute_force_resolve(m0, plan, spec, index);
+  unrank(spec, index, perm_out);
   evaluate_host_orders(m0, plan, perm_out, 1, cost_out, true, true, nullptr);
   if (evals_out) *evals_out = evals;
 }

@@ -21,6 +21,7 @@ plumbing; the compute is librankweave_b200.so.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from typing import Optional, Tuple
 
 import numpy as np
@@ -114,6 +115,11 @@ def brute_force_sharded(prob: Problem, spec: CollectiveSpec, threshold: int = 10
         cost, index = float("inf"), INT64_MAX
     best, win, _ = reduce_argmin(cost, int(index))
     perm = np.empty(spec.n, dtype=np.int32)
+    # Best::offer (solver.cpp:34-46): the first order of the enumeration stays
+    # when its cost is NaN or when no order costs less than +inf
+    check(lib.rw_unrank(C.byref(spec._c()), 0, ptr(perm, C.c_int32)))
+    if win >= cnt.value or math.isnan(float(prob.evaluate_batch(spec, perm[None, :], exact=True)[0])):
+        win = 0
     check(lib.rw_unrank(C.byref(spec._c()), win, ptr(perm, C.c_int32)))
     exact = float(prob.evaluate_batch(spec, perm, exact=True)[0])
     return Solution(RankOrder(perm.tolist()), exact, SolveMethod.BruteForce, int(cnt.value))

@@ -53,6 +53,40 @@ def test_brute_matches_oracle_on_generic_fp64_matrices():
                     assert (sol.cost, sol.order.perm, sol.evaluations) == (cost, perm.tolist(), ev), (n, alg, mode)
 
 
+def test_brute_nan_matrices_follow_the_reference():
+    """brute_force on matrices with NaN entries (unvalidated):
+    the reference keeps the first order's cost even when it is NaN, and
+    afterwards only takes `c < best` (solver.cpp:73-105, Best::offer), so a NaN
+    identity cost is never replaced and NaN costs later never win.  Checked
+    against oracle/_ref (the reference itself) for every model."""
+    from oracle.pyoracle import Reference, reference_available
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    ref = Reference()
+    rng = np.random.default_rng(67)
+    for n in (7, 8):
+        for case in range(5):
+            m = rng.uniform(1, 1000, (n, n))
+            np.fill_diagonal(m, 0)
+            m[rng.random((n, n)) < 0.08] = np.nan
+            if case == 0:
+                m[1, 0] = np.nan  # on the identity's ring and tree edges
+                m[0, 1] = np.nan
+            if case == 4:
+                m[:] = np.inf  # no order costs less than +inf: the first one stays
+                np.fill_diagonal(m, 0)
+            algs = [(0, 2, 0)] + ([(1, 2, 0), (1, 2, 1), (2, 2, 0), (3, 2, 0)] if n == 8 else [])
+            for alg, b, pair in algs:
+                s = make_spec(alg, n, 3.5, b, 1, pair)
+                perm, cost, ev = ref.brute_force(m, s)
+                sol = rw.brute_force(cm(m), rw.CollectiveSpec(rw.Algorithm(alg), n, 3.5, b,
+                                                              rw.CostMode.LatencyTimesSize, rw.HdPairing(pair)),
+                                     threshold=16)
+                same_cost = sol.cost == cost or (np.isnan(sol.cost) and np.isnan(cost))
+                assert same_cost and sol.order.perm == perm.tolist() and sol.evaluations == ev, \
+                    (n, case, alg, pair, sol.cost, cost, sol.order.perm, perm.tolist())
+
+
 def test_brute_ties_resolve_to_lexicographic_minimum():
     """uniform matrix: every order ties, identity (lex smallest) wins (test_solver.cpp:49-56)."""
     for n in (5, 9, 11):
