@@ -78,6 +78,21 @@ def main():
                         print(f"MISMATCH n={n} kind={kind} sym={sym} dirty={dirty} alg={alg} b={b} pair={pair} "
                               f"mode={mode} path={path} batch={len(perms)} rows={bad[:5].tolist()} "
                               f"got={got[bad[:3]].tolist()} want={want[bad[:3]].tolist()}", flush=True)
+        # the other host layouts (uint16, packed) and device-resident orders score the same
+        if n <= 4096 and len(perms) >= 7:
+            # (the fast ring sum on FP matrices is path-dependent within 1e-12: compare exact sums)
+            spec = rw.CollectiveSpec(rw.Algorithm(0), n, 2.0 ** 17)
+            ex = kind != "u16"
+            base = probs["auto"].evaluate_batch(spec, perms, exact=ex)
+            bits = rw.api.packed_bits(n)
+            got_u16 = probs["auto"].evaluate_batch(spec, perms.astype(np.uint16), exact=ex)
+            got_pk = probs["auto"].evaluate_batch_packed(spec, rw.api.pack_orders(perms, bits), bits, len(perms),
+                                                         exact=ex)
+            cases += 2
+            for name, got in (("u16", got_u16), ("packed", got_pk)):
+                if not np.array_equal(got, base, equal_nan=True):
+                    fails += 1
+                    print(f"LAYOUT MISMATCH {name} n={n} kind={kind} batch={len(perms)}", flush=True)
         # single-order evaluate() through the resident evaluator (exact path)
         res = rw.Problem(m)
         res.set_resident(300)
