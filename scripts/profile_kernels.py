@@ -54,6 +54,10 @@ def main():
         score(torch, rw, "C5", "fixed",
               lambda n, s: rw.CollectiveSpec(A.HalvingDoubling, n, s, 2, rw.CostMode.LatencyTimesSize,
                                              rw.HdPairing.XorPairing), 1 << 12)
+    if which in ("hdpaper", "all"):
+        score(torch, rw, "C5", "fixed",
+              lambda n, s: rw.CollectiveSpec(A.HalvingDoubling, n, s, 2, rw.CostMode.LatencyTimesSize,
+                                             rw.HdPairing.PaperFormula), 1 << 12)
     if which in ("bcube8_c5", "all"):
         score(torch, rw, "C5", "fixed", lambda n, s: rw.CollectiveSpec(A.BCube, n, s, 8), 1 << 14)
     if which in ("dbt_c5", "all"):

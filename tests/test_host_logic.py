@@ -153,6 +153,22 @@ def test_spearman_and_stats_match_the_reference_bits():
         assert L.ref_distribution_stats(y.ctypes.data_as(C.POINTER(C.c_double)), n,
                                         o4.ctypes.data_as(C.POINTER(C.c_double))) == 0
         assert (st.min, st.max, st.mean, st.stddev) == tuple(o4)
+    # special values: NaN, infinities, signed zeros, overflow of the sum
+    nan, inf = float("nan"), float("inf")
+    for c in ([nan, 1.0, 2.0], [1.0, nan], [inf, 1.0], [-inf, inf], [5.0], [-0.0, 0.0], [nan, nan],
+              [1e308, 1e308, -1e308]):
+        y = np.array(c)
+        o4 = np.empty(4)
+        assert L.ref_distribution_stats(y.ctypes.data_as(C.POINTER(C.c_double)), len(y),
+                                        o4.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        st = api.distribution_stats(y)
+        assert np.array([st.min, st.max, st.mean, st.stddev]).tobytes() == o4.tobytes(), c
+    for c in ([nan, 1.0, 2.0, 3.0], [1.0, 2.0, inf, 0.5], [1.0, nan, nan, 2.0]):
+        x, y = np.array(c), rng.uniform(0, 1, len(c))
+        out = C.c_double()
+        assert L.ref_spearman(x.ctypes.data_as(C.POINTER(C.c_double)), y.ctypes.data_as(C.POINTER(C.c_double)),
+                              len(x), C.byref(out)) == 0
+        assert np.float64(api.spearman(x, y)).tobytes() == np.float64(out.value).tobytes(), c
     with pytest.raises(rw.DomainError, match="lengths differ"):
         api.spearman([1.0, 2.0], [1.0, 2.0, 3.0])
     with pytest.raises(rw.DomainError, match="constant series"):
