@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -354,6 +355,7 @@ bool resident_evaluate(Problem& p, const EvalPlan& plan, const int32_t* perm, do
   std::atomic_thread_fence(std::memory_order_seq_cst);
   const unsigned long long seq = ++s->seq;
   v->req = seq;
+  const auto t0 = std::chrono::steady_clock::now();
   for (unsigned spin = 1;; ++spin) {
     if (v->done == seq) break;
     if (v->exited == s->epoch && v->done != seq) {
@@ -364,6 +366,10 @@ bool resident_evaluate(Problem& p, const EvalPlan& plan, const int32_t* perm, do
     if ((spin & 4095u) == 0) {
       const cudaError_t e = cudaStreamQuery(s->st);
       if (e != cudaSuccess && e != cudaErrorNotReady) RW_CUDA(e);
+      // a server that never gets an SM (the device is held by other work) must
+      // not spin the caller forever
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        throw Failure(RW_ERR_CUDA, "resident evaluator: no answer within 30 s");
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
