@@ -93,8 +93,10 @@ struct Problem {
   uint32_t* d_rank = nullptr;
   double* d_rank_vals = nullptr;
   uint32_t zero_rank = 0;
-  // Resident evaluator for single-order calls (rw_problem_set_resident).
-  ResidentServer* resident = nullptr;
+  // Resident evaluator for single-order calls (rw_problem_set_resident);
+  // read and replaced with std::atomic_load / atomic_store, so a call in
+  // flight keeps the server it took alive across a reconfiguration.
+  std::shared_ptr<ResidentServer> resident;
   size_t elem_bytes() const { return storage == RW_STORAGE_U16 ? 2 : storage == RW_STORAGE_F32 ? 4 : 8; }
 };
 

@@ -26,6 +26,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -213,6 +214,7 @@ size_t resident_smem(int n) {
 }  // namespace
 
 struct ResidentServer {
+  ~ResidentServer();
   std::mutex mu;
   int device = 0;
   long long idle_ns = 0;
@@ -271,21 +273,21 @@ void stop_server(ResidentServer& s) {
 
 }  // namespace
 
-void resident_release(Problem& p) {
-  ResidentServer* s = p.resident;
-  if (!s) return;
-  {
-    DeviceGuard g(p.device);
-    std::lock_guard<std::mutex> lock(s->mu);
-    try {
-      stop_server(*s);
-    } catch (...) {
-    }
-    if (s->st) cudaStreamDestroy(s->st);
-    if (s->mb) cudaFreeHost(s->mb);
+// The last holder (the problem, or a call still in flight) stops the CTA and
+// frees the mailbox.
+ResidentServer::~ResidentServer() {
+  DeviceGuard g(device);
+  try {
+    stop_server(*this);
+  } catch (...) {
   }
-  delete s;
-  p.resident = nullptr;
+  if (st) cudaStreamDestroy(st);
+  if (mb) cudaFreeHost(mb);
+}
+
+void resident_release(Problem& p) {
+  std::shared_ptr<ResidentServer> s = std::atomic_exchange(&p.resident, std::shared_ptr<ResidentServer>());
+  s.reset();
 }
 
 void resident_configure(Problem& p, int idle_us) {
@@ -296,29 +298,26 @@ void resident_configure(Problem& p, int idle_us) {
   if (p.n > kResidentMaxN) fail_domain("resident evaluation supports N <= " + std::to_string(kResidentMaxN));
   if (resident_smem(p.n) > 220 * 1024) fail_domain("resident evaluation: shared memory budget exceeded");
   const long long idle_ns = (long long)std::min(idle_us, 100000) * 1000;
-  if (p.resident) {
-    std::lock_guard<std::mutex> lock(p.resident->mu);
-    p.resident->idle_ns = idle_ns;  // taken by the next launch
+  if (std::shared_ptr<ResidentServer> cur = std::atomic_load(&p.resident)) {
+    std::lock_guard<std::mutex> lock(cur->mu);
+    cur->idle_ns = idle_ns;  // taken by the next launch
     return;
   }
   DeviceGuard g(p.device);
-  auto* s = new ResidentServer();
+  auto s = std::make_shared<ResidentServer>();
   s->device = p.device;
   s->idle_ns = idle_ns;
-  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&s->mb), sizeof(Mailbox), cudaHostAllocMapped | cudaHostAllocPortable);
-  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->d_mb), s->mb, 0);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking);
-  if (e != cudaSuccess) {
-    if (s->mb) cudaFreeHost(s->mb);
-    delete s;
-    RW_CUDA(e);
-  }
+  RW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->mb), sizeof(Mailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+  RW_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->d_mb), s->mb, 0));
+  RW_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
   std::memset(s->mb, 0, sizeof(Mailbox));
-  p.resident = s;
+  std::shared_ptr<ResidentServer> expected;
+  // a concurrent configure may have installed one first: keep that one
+  std::atomic_compare_exchange_strong(&p.resident, &expected, s);
 }
 
 bool resident_evaluate(Problem& p, const EvalPlan& plan, const int32_t* perm, double* cost) {
-  ResidentServer* s = p.resident;
+  const std::shared_ptr<ResidentServer> s = std::atomic_load(&p.resident);
   if (!s || plan.n != p.n) return false;
   std::unique_lock<std::mutex> lock(s->mu, std::try_to_lock);
   if (!lock.owns_lock()) return false;  // another thread holds the server: take the launched path

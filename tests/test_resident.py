@@ -126,6 +126,45 @@ def test_resident_concurrent_callers():
     prob.close()
 
 
+def test_resident_reconfigured_while_callers_run():
+    """set_resident toggled from one thread while others evaluate: a call in
+    flight keeps the server it took (shared ownership), later calls take the
+    launched path or a new server; every result stays exact."""
+    n = 128
+    m = matrix(n, "fixed", True, 12)
+    prob = rw.Problem(m)
+    spec = rw.CollectiveSpec(rw.Algorithm.HalvingDoubling, n, 1e5, 2, rw.CostMode.LatencyTimesSize,
+                             rw.HdPairing.XorPairing)
+    rng = np.random.default_rng(5)
+    perms = np.stack([rng.permutation(n) for _ in range(32)]).astype(np.int32)
+    want = prob.evaluate_batch(spec, perms)
+    errors = []
+    stop = threading.Event()
+
+    def caller(t):
+        k = 0
+        try:
+            while not stop.is_set():
+                i = (k * 5 + t) % 32
+                if prob.evaluate(spec, perms[i]) != want[i]:
+                    errors.append((t, i))
+                k += 1
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=caller, args=(t,)) for t in range(3)]
+    for th in threads:
+        th.start()
+    for k in range(60):
+        prob.set_resident(0 if k % 2 else 100 + k)
+        time.sleep(0.002)
+    stop.set()
+    for th in threads:
+        th.join()
+    assert not errors
+    prob.close()
+
+
 def test_resident_rejects_large_n_and_keeps_batches_exact():
     n = 5000
     prob = rw.Problem(matrix(n, "fixed", False, 9))
