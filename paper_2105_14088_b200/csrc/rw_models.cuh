@@ -214,10 +214,11 @@ __device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, co
 }
 
 // Sum over rounds of the round maximum by a CTA of kCta threads; red holds
-// 2 * kCta / 32 entries.  The per-round maximum of raw codes is
+// 2 * kCta / 32 entries (kFlat: rounds * kCta / 32, and the rounds' gathers
+// run without a barrier between them).  The per-round maximum of raw codes is
 // exact under any grouping (no NaN survives the running max from 0), and the
 // rounds are summed in order, so the value equals warp_rounds_cost's.
-template <int kCta, typename T, bool kSmem>
+template <int kCta, typename T, bool kSmem, bool kFlat = false>
 __device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n, const T* mat, const RoundsArgs& r,
                                                   double scale, typename MaxAcc<T>::type* red) {
   using Acc = typename MaxAcc<T>::type;
@@ -249,6 +250,11 @@ __device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n,
       stride *= r.b;
     }
     mx = warp_max(mx);
+    if constexpr (kFlat) {
+      // red holds rounds x (kCta / 32) entries: no barrier per round, one at the end
+      if (lane == 0) red[rd * (kCta / 32) + w] = mx;
+      continue;
+    }
     if (lane == 0) red[(rd & 1) * (kCta / 32) + w] = mx;  // double-buffered by round parity
     __syncthreads();
     Acc m = red[(rd & 1) * (kCta / 32)];
@@ -257,6 +263,17 @@ __device__ __forceinline__ double cta_rounds_cost(const uint16_t* s_perm, int n,
     double rm = to_double((T)m, scale);
     if (r.mode == RW_LATENCY_TIMES_SIZE) rm = __dmul_rn(rm, r.bytes[rd]);
     total = __dadd_rn(total, rm);
+  }
+  if constexpr (kFlat) {
+    __syncthreads();
+    for (int rd = 0; rd < r.rounds; ++rd) {
+      Acc m = red[rd * (kCta / 32)];
+#pragma unroll
+      for (int k = 1; k < kCta / 32; ++k) m = ref_max<Acc>(m, red[rd * (kCta / 32) + k]);
+      double rm = to_double((T)m, scale);
+      if (r.mode == RW_LATENCY_TIMES_SIZE) rm = __dmul_rn(rm, r.bytes[rd]);
+      total = __dadd_rn(total, rm);  // rounds summed in order, as above
+    }
   }
   return total;
 }

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(Mailbox* mb, const 
   __shared__ __align__(16) ResRequest s_rq;
   __shared__ unsigned long long s_seq;
   __shared__ unsigned long long s_part[kResThreads / 32];
-  __shared__ typename MaxAcc<T>::type s_red[2 * (kResThreads / 32)];
+  __shared__ typename MaxAcc<T>::type s_red[kMaxRounds * (kResThreads / 32)];
   __shared__ const int4* s_plan_src;  // DBT plan currently staged in shared memory
   volatile Mailbox* vmb = mb;
   const int ecap = resident_edge_cap(n);
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(Mailbox* mb, const 
         const double best = cta_dbt_cost<kResThreads, T, false>(s_perm, n, gmat, d, scale, vals);
         if (threadIdx.x == 0) cost = best;
       } else {
-        const double total = cta_rounds_cost<kResThreads, T, false>(s_perm, n, gmat, q.r, scale, s_red);
+        const double total = cta_rounds_cost<kResThreads, T, false, true>(s_perm, n, gmat, q.r, scale, s_red);
         if (threadIdx.x == 0) cost = total;
       }
     }
