@@ -411,6 +411,7 @@ __device__ __forceinline__ void anneal_ring_chain(const AnnealArgs& a, int chain
   uint4 rnext[kSlots];
 #pragma unroll
   for (int sl = 0; sl < kSlots; ++sl) rnext[sl] = philox_at(ctr, sl);
+  bool cur_is_best = false;  // p is the best-so-far order and a.best is not yet written
   for (int level = a.level_begin; level < a.level_end; ++level) {
     const double t = a.temps[level];
     const double inv_t = a.mul / t;  // real delta / t = units * mul / t
@@ -488,14 +489,23 @@ __device__ __forceinline__ void anneal_ring_chain(const AnnealArgs& a, int chain
             mw.k = __shfl_sync(kFull, ms[sl].k, w);
             dw = __shfl_sync(kFull, ds[sl], w);
           }
+        // The best order is written lazily: only when the chain leaves a
+        // best-so-far state (this move does not improve on it), and at the
+        // end.  A run of improvements then costs one 2 KB store instead of one
+        // per step; the recorded order and cost are unchanged.
+        const double next = cur + (double)dw;
+        if (cur_is_best && !(next < best)) {
+          store_order(a.best + (size_t)chain * n, p, n, lane);
+          cur_is_best = false;
+        }
         apply_move(p, n, mw, lane, pos, true);
-        cur += (double)dw;
+        cur = next;
         const int used = wsl * 32 + w + 1;
         props += (unsigned long long)used;
         remaining -= used;
         if (cur < best) {
           best = cur;
-          store_order(a.best + (size_t)chain * n, p, n, lane);
+          cur_is_best = true;
         }
       } else {
         props += (unsigned long long)active;
@@ -505,6 +515,7 @@ __device__ __forceinline__ void anneal_ring_chain(const AnnealArgs& a, int chain
     if constexpr (!std::is_same<T, uint16_t>::value) cur = resync(p);  // drift resync
   }
   __syncwarp();
+  if (cur_is_best) store_order(a.best + (size_t)chain * n, p, n, lane);
   store_order(a.cur + (size_t)chain * n, p, n, lane);
   if (lane == 0) {
     a.cur_cost[chain] = cur;
