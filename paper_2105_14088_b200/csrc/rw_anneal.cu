@@ -234,7 +234,8 @@ __device__ __forceinline__ Move draw_move_nb(uint4 r, const uint16_t* p, const u
                                              const uint16_t* __restrict__ nb, int K, int n) {
   Move m;
   const int i = (int)(((uint64_t)r.y * (uint32_t)n) >> 32);
-  const int b = nb[p[i] * K + (int)(r.z % (uint32_t)K)];
+  const uint32_t kk = K == 8 ? (r.z & 7u) : r.z % (uint32_t)K;  // K = min(8, n - 1)
+  const int b = nb[p[i] * K + (int)kk];
   const int j = pos[b];
   m.type = 1;
   m.i = min(i, j) + 1;
