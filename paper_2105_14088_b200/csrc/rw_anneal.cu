@@ -838,13 +838,13 @@ struct DbtDelta {
 
 template <typename T, typename V, bool kSmem>
 __device__ __forceinline__ double cta_dbt_full(const uint16_t* s_perm, int n, const T* mat, const DbtArgs& d,
-                                               const int4* rec, const int32_t* doff, double scale, V* val, V* own) {
+                                               const uint2* rec, const int32_t* doff, double scale, V* val, V* own) {
   using D = DbtDelta<T, V, kSmem>;
   for (int depth = d.depths - 1; depth >= 0; --depth) {
     const int lo = doff[depth], hi = doff[depth + 1];
 #pragma unroll 2
     for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
-      const int4 r = rec[e];
+      const int4 r = dbt_rec(rec[e]);
       const V c = D::own(mat, n, d, scale, s_perm[r.x], s_perm[r.y]);
       own[e] = c;
       val[e] = r.z >= 0 ? D::path(c, false, val[r.z], val[r.w]) : D::path(c, true, c, c);
@@ -866,8 +866,8 @@ __global__ void __launch_bounds__(kCta) k_anneal_dbt_delta(AnnealArgs a, const T
   const int n = a.n, E = d.edges, t = threadIdx.x, lane = t & 31;
   // layout after the matrix: rec | depth_off | pd | posedges | p | q | val x2 | own x2 | nval | nown | marks x2
   unsigned char* b = smem + al16(a.mat_smem);
-  int4* rec = reinterpret_cast<int4*>(b);
-  b += al16((size_t)E * 16);
+  uint2* rec = reinterpret_cast<uint2*>(b);
+  b += al16((size_t)E * 8);
   int32_t* doff = reinterpret_cast<int32_t*>(b);
   b += al16((size_t)(d.depths + 1) * 4);
   int32_t* pd = reinterpret_cast<int32_t*>(b);
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(kCta) k_anneal_dbt_delta(AnnealArgs a, const T
           const int hi = p[m.j], hj = p[m.i];  // hosts after the swap at positions i and j
           if (lane < 16) node = pe[(lane < 8 ? m.i : m.j) * 8 + (lane & 7)];
           if (node >= 0) {
-            const int4 rr = rec[node];
+            const int4 rr = dbt_rec(rec[node]);
             const int ha = rr.x == m.i ? hi : rr.x == m.j ? hj : p[rr.x];
             const int hb = rr.y == m.i ? hi : rr.y == m.j ? hj : p[rr.y];
             nown[node] = D::own(mat, n, d, a.scale, ha, hb);
@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(kCta) k_anneal_dbt_delta(AnnealArgs a, const T
           int nd = node >= 0 ? (pd[node] & 0xFF) : -1;
           for (int depth = d.depths - 1; depth >= 0; --depth) {
             if (node >= 0 && nd == depth) {
-              const int4 rr = rec[node];
+              const int4 rr = dbt_rec(rec[node]);
               const V o = omark[node] == gen ? nown[node] : own[node];
               V x = o, y = o;
               if (rr.z >= 0) {
@@ -1033,7 +1033,7 @@ __global__ void __launch_bounds__(kCta) k_anneal_dbt_delta(AnnealArgs a, const T
 }
 
 __host__ __device__ inline size_t dbt_delta_smem(size_t mat_smem, int n, int edges, int depths, size_t vb) {
-  return al16(mat_smem) + al16((size_t)edges * 16) + al16((size_t)(depths + 1) * 4) + al16((size_t)edges * 4) +
+  return al16(mat_smem) + al16((size_t)edges * 8) + al16((size_t)(depths + 1) * 4) + al16((size_t)edges * 4) +
          al16((size_t)n * 32) + 2 * al16((size_t)n * 2) + 6 * al16((size_t)edges * vb) + 2 * al16((size_t)edges * 4);
 }
 

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
       const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
 #pragma unroll 2
       for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-        const int4 r = __ldg(d.rec + e);  // {src, dst, c0, c1}
+        const int4 r = dbt_rec(__ldg(d.rec + e));  // {src, dst, c0, c1}
         const T raw = ld_matrix<T>(mat, (size_t)p[r.x] * n + p[r.y]);
         if (im) {
           uint32_t sub = 0;

@@ -57,10 +57,11 @@ struct DbtPlan {
   int edges = 0;
   int depths = 0;
   std::vector<int32_t> h_src, h_dst, h_c0, h_c1, h_depth_off;
-  // [edge records {src, dst, c0, c1} (one 16-byte load per edge) | depth_off]
+  // [edge records {src | dst << 16, c0} (one 8-byte load per edge; the second
+  // child is c0 + 1, see build_dbt_plan) | depth_off]
   int32_t* d_all = nullptr;
-  const int4* d_rec() const { return reinterpret_cast<const int4*>(d_all); }
-  const int32_t* d_depth_off() const { return d_all + 4 * edges; }
+  const uint2* d_rec() const { return reinterpret_cast<const uint2*>(d_all); }
+  const int32_t* d_depth_off() const { return d_all + 2 * edges; }
   // [per edge (parent << 8) | depth | per position 8 incident edges, -1 padded]
   int32_t* d_aux = nullptr;
   const int32_t* d_pd() const { return d_aux; }

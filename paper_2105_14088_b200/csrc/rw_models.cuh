@@ -26,7 +26,7 @@ struct RoundsArgs {
 };
 
 struct DbtArgs {
-  const int4* rec;  // per edge {src, dst, c0, c1}: positions and child edges (-1: none)
+  const uint2* rec;  // per edge {src | dst << 16, c0}: positions, first child edge (-1: none; c1 = c0 + 1)
   const int32_t* depth_off;
   int depths;
   int edges;
@@ -41,14 +41,20 @@ struct DbtArgs {
   const int32_t* posedges;  //   per position 8 incident edges, -1 padded
 };
 
-// Plan (edge records {src, dst, c0, c1} | depth_off, int32) in shared memory:
-// 16 B per edge, one LDS.128 per edge.  All threads of the CTA call it before any early exit.
+// Unpacked edge record {src, dst, c0, c1} (children -1 when none).
+__device__ __forceinline__ int4 dbt_rec(uint2 v) {
+  const int c0 = (int)v.y;
+  return make_int4((int)(v.x & 0xFFFFu), (int)(v.x >> 16), c0, c0 < 0 ? -1 : c0 + 1);
+}
+
+// Plan (edge records | depth_off, int32) in shared memory: 8 B per edge, one
+// LDS.64 per edge.  All threads of the CTA call it before any early exit.
 __host__ __device__ inline size_t dbt_plan_bytes(int edges, int depths) {
-  return ((size_t)4 * edges + depths + 1) * 4 + 16;
+  return ((size_t)2 * edges + depths + 1) * 4 + 16;
 }
 __device__ __forceinline__ void stage_dbt_plan(DbtArgs& d, unsigned char* smem) {
   if (!d.stage_plan) return;
-  int4* r = reinterpret_cast<int4*>(smem + d.plan_off);
+  uint2* r = reinterpret_cast<uint2*>(smem + d.plan_off);
   const int E = d.edges;
   for (int k = threadIdx.x; k < E; k += blockDim.x) r[k] = d.rec[k];
   int32_t* off = reinterpret_cast<int32_t*>(r + E);
@@ -118,7 +124,7 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
         const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 4
         for (int e = lo + lane; e < hi; e += 32) {
-          const int4 r = d.rec[e];
+          const int4 r = dbt_rec(d.rec[e]);
           const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
           uint32_t sub = 0;
           if (r.z >= 0) {
@@ -138,7 +144,7 @@ __device__ double warp_dbt_cost(const uint16_t* s_perm, int n, const T* mat, con
     const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 4
     for (int e = lo + lane; e < hi; e += 32) {
-      const int4 r = d.rec[e];
+      const int4 r = dbt_rec(d.rec[e]);
       double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
       if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
       // value = cost(edge) + T(sub-interval); T(empty) = 0.0 (cost_model.cpp:105-113)
@@ -182,7 +188,7 @@ __device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, co
         const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 2
         for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
-          const int4 r = d.rec[e];
+          const int4 r = dbt_rec(d.rec[e]);
           const uint32_t c = (uint32_t)mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]);
           uint32_t sub = 0;
           if (r.z >= 0) {
@@ -201,7 +207,7 @@ __device__ __forceinline__ double cta_dbt_cost(const uint16_t* s_perm, int n, co
     const int lo = d.depth_off[depth], hi = d.depth_off[depth + 1];
 #pragma unroll 2
     for (int e = lo + (int)threadIdx.x; e < hi; e += kCta) {
-      const int4 r = d.rec[e];
+      const int4 r = dbt_rec(d.rec[e]);
       double c = to_double(mat_at<T, kSmem>(mat, n, s_perm[r.x], s_perm[r.y]), scale);
       if (d.mode == RW_LATENCY_TIMES_SIZE) c = __dmul_rn(c, d.half);
       const double sub = r.z >= 0 ? ref_max(vals[r.z], vals[r.w]) : 0.0;

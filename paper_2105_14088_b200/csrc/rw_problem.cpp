@@ -275,10 +275,18 @@ static void build_dbt_plan(DbtPlan& plan, int n) {
       }
     }
   }
+  // Packed records: positions fit 16 bits (n <= 65536), and the two children of
+  // an edge are adjacent in their depth list (the left edge of the child node
+  // is pushed, then only deeper edges, then its right edge), so c1 = c0 + 1.
   std::vector<int32_t> all;
-  all.reserve(4 * plan.edges + plan.depths + 1);
-  for (int e = 0; e < plan.edges; ++e)
-    for (const auto* v : {&plan.h_src, &plan.h_dst, &plan.h_c0, &plan.h_c1}) all.push_back((*v)[static_cast<size_t>(e)]);
+  all.reserve(2 * static_cast<size_t>(plan.edges) + plan.depths + 1);
+  for (int e = 0; e < plan.edges; ++e) {
+    const size_t k = static_cast<size_t>(e);
+    if ((plan.h_c0[k] < 0) != (plan.h_c1[k] < 0) || (plan.h_c0[k] >= 0 && plan.h_c1[k] != plan.h_c0[k] + 1))
+      throw Failure(RW_ERR_INTERNAL, "dbt plan: children of an edge are not adjacent");
+    all.push_back(static_cast<int32_t>(static_cast<uint32_t>(plan.h_src[k]) | (static_cast<uint32_t>(plan.h_dst[k]) << 16)));
+    all.push_back(plan.h_c0[k]);
+  }
   all.insert(all.end(), plan.h_depth_off.begin(), plan.h_depth_off.end());
   RW_CUDA(cudaMalloc(&plan.d_all, all.size() * sizeof(int32_t)));
   RW_CUDA(cudaMemcpy(plan.d_all, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice));

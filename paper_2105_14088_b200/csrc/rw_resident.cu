@@ -86,12 +86,12 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(Mailbox* mb, const 
   __shared__ unsigned long long s_seq;
   __shared__ unsigned long long s_part[kResThreads / 32];
   __shared__ typename MaxAcc<T>::type s_red[kMaxRounds * (kResThreads / 32)];
-  __shared__ const int4* s_plan_src;  // DBT plan currently staged in shared memory
+  __shared__ const uint2* s_plan_src;  // DBT plan currently staged in shared memory
   volatile Mailbox* vmb = mb;
   const int ecap = resident_edge_cap(n);
   uint16_t* s_perm = reinterpret_cast<uint16_t*>(smem);
   double* vals = reinterpret_cast<double*>(smem + al16((size_t)n * 2));
-  int4* s_rec = reinterpret_cast<int4*>(smem + al16((size_t)n * 2) + (size_t)ecap * 8);
+  uint2* s_rec = reinterpret_cast<uint2*>(smem + al16((size_t)n * 2) + (size_t)ecap * 8);
   int32_t* s_doff = reinterpret_cast<int32_t*>(s_rec + ecap);
   if (threadIdx.x == 0) s_plan_src = nullptr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -205,10 +205,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(Mailbox* mb, const 
   }
 }
 
-// order (u16) | edge values (FP64) | DBT plan (int4 records, depth offsets)
+// order (u16) | edge values (FP64) | DBT plan (8-byte records, depth offsets)
 size_t resident_smem(int n) {
   const size_t e = (size_t)resident_edge_cap(n);
-  return al16((size_t)n * 2) + e * 8 + e * 16 + (kResDepthCap + 1) * 4;
+  return al16((size_t)n * 2) + e * 8 + e * 8 + (kResDepthCap + 1) * 4;
 }
 
 }  // namespace
