@@ -112,6 +112,8 @@ def test_null_and_shape_arguments_are_domain_errors():
         _lib.check(_lib.lib.rw_evaluate(None, None, None, None))
     with pytest.raises(rw.DomainError):
         rw.Problem(np.zeros((3, 4)))
+    with pytest.raises(rw.DomainError, match="null rw_problem"):
+        _lib.check(_lib.lib.rw_problem_set_resident(None, 100))
 
 
 def test_packed_layout_helpers_on_the_host():
