@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256) k_dbt_cta(KArgs a, DbtArgs d, const P* __
     if (bad) s_bad = 1;
     for (int depth = d.depths - 1; depth >= 0; --depth) {
       const int lo = __ldg(d.depth_off + depth), hi = __ldg(d.depth_off + depth + 1);
-#pragma unroll 2
+#pragma unroll 8
       for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
         const int4 r = dbt_rec(__ldg(d.rec + e));  // {src, dst, c0, c1}
         const T raw = ld_matrix<T>(mat, (size_t)p[r.x] * n + p[r.y]);
