@@ -16,7 +16,7 @@
 //   pass 2 (k_ring_score)  a CTA holds a row block of the matrix in shared
 //       memory (one TMA bulk copy); a producer warp streams the block's
 //       predecessor slices through a two-stage TMA bulk-copy ring (full /
-//       empty mbarriers) and 31 consumer warps do the shared-memory lookups
+//       empty mbarriers) and 24 consumer warps do the shared-memory lookups
 //       blk[row][pred[row]].  (row block, stage) units are split stream-K
 //       over every SM.  u16 codes: per-(order, block) integer partials are
 //       added atomically into the cost array (exact, order-independent) and
@@ -207,9 +207,10 @@ __device__ __forceinline__ void score_stage_vec(uint32_t gi, int stage_orders, b
   // U orders per lane group per step: more lookups in flight, loop and
   // atomic-address overhead shared.
   // Lane-group steps are dealt round-robin over the consumer warps as one
-  // continuous stream across stages (rotated by the stage counter gi): a
-  // 384-order stage is 48 steps of 8 orders for 31 warps, and a fixed
-  // warp-0-first deal would give the same 17 warps the extra step every stage.
+  // continuous stream across stages (rotated by the stage counter gi): when
+  // the steps of a stage do not divide over the consumer warps (48 steps for
+  // 31 warps when the CTA had 1024 threads), a fixed warp-0-first deal would
+  // give the same warps the extra step every stage.
   const int rot = rotate ? (int)((uint64_t)gi * (uint32_t)(stage_orders / (OPW * U)) % (uint32_t)cw) : 0;
   const int w0 = warp - rot < 0 ? warp - rot + cw : warp - rot;
   for (int k0 = w0 * OPW * U; k0 < cnt; k0 += cw * OPW * U) {
@@ -301,8 +302,13 @@ __device__ __forceinline__ void score_stage_vec_fp(uint32_t gi, int stage_orders
 // block's predecessor slices (contiguous in predbuf) through a 4-stage TMA
 // bulk-copy ring; each warp scores one order per step with shared-memory
 // lookups and writes the (order, block) partial.
+// 24 consumer warps + 1 producer warp.  A 384-order stage at C4 is 48 lane-
+// group steps, two per consumer warp; measured on B200 (C4 u16, bench.py):
+// 1024 threads 7.11e8, 800 threads 7.36e8, 544 7.00e8, 416 6.82e8 evals/s.
+constexpr int kScoreThreads = 800;
+
 template <typename T>
-__global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint16_t* __restrict__ pred,
+__global__ void __launch_bounds__(kScoreThreads, 1) k_ring_score(ScoreArgs a, const uint16_t* __restrict__ pred,
                                                         const T* __restrict__ gmat) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n, R = a.R, nb = a.nblocks;
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(1024, 1) k_ring_score(ScoreArgs a, const uint1
     stage_rows(blk, gmat + (size_t)row0 * n, (size_t)rows * n * sizeof(T), &mat_bar, &mat_phase);
     const uint16_t* base = pred + ((size_t)b * a.count + o0) * R;
     // Producer / consumer ring: the last warp issues the bulk copies, gated
-    // by per-slot "empty" barriers that the 31 consumer warps arrive on; no
+    // by per-slot "empty" barriers that the consumer warps arrive on; no
     // CTA-wide barrier per stage.
     if (warp == nwarps - 1) {
       if (lane == 0) {
@@ -539,19 +545,19 @@ bool launch_ring_transpose(const Problem& p, const EvalPlan& plan, const void* d
       case RW_STORAGE_U16: {
         auto k = k_ring_score<uint16_t>;
         set(k, score_smem);
-        k<<<sgrid, 1024, score_smem, st>>>(sa, predbuf, static_cast<const uint16_t*>(p.d_mat));
+        k<<<sgrid, kScoreThreads, score_smem, st>>>(sa, predbuf, static_cast<const uint16_t*>(p.d_mat));
         break;
       }
       case RW_STORAGE_F32: {
         auto k = k_ring_score<float>;
         set(k, score_smem);
-        k<<<sgrid, 1024, score_smem, st>>>(sa, predbuf, static_cast<const float*>(p.d_mat));
+        k<<<sgrid, kScoreThreads, score_smem, st>>>(sa, predbuf, static_cast<const float*>(p.d_mat));
         break;
       }
       default: {
         auto k = k_ring_score<double>;
         set(k, score_smem);
-        k<<<sgrid, 1024, score_smem, st>>>(sa, predbuf, static_cast<const double*>(p.d_mat));
+        k<<<sgrid, kScoreThreads, score_smem, st>>>(sa, predbuf, static_cast<const double*>(p.d_mat));
         break;
       }
     }

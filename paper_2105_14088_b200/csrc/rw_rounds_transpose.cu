@@ -236,7 +236,11 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
 
 // ------------------------------------------------------------------ score --
 constexpr int kRMaxStages = 4;
-constexpr int kRThreads = 1024;  // 31 consumer warps + 1 producer warp
+// 16 consumer warps + 1 producer warp: a 256-order stage is 1,536 (xor, round
+// pairs) or 3,072 (paper) tasks, 3 or 6 per consumer thread.  Measured on B200
+// at C5 (u16 xor / paper, evals/s): 1024 threads 2.38e7 / 1.24e7, 800 2.42e7 /
+// 1.26e7, 544 2.49e7 / 1.33e7, 416 2.47e7 / 1.33e7, 288 2.39e7 / 1.28e7.
+constexpr int kRThreads = 544;
 
 struct RScoreArgs {
   int64_t count;
