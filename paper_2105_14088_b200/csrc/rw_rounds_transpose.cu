@@ -364,6 +364,286 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
   }
 }
 
+// ------------------------------------------------ paper pairing, compacted --
+// Paper pairing (the reference's default, cost_model.cpp:84-85): only the
+// hosts at positions < N/2 are sources, so the slot layout above stores a
+// sentinel for half the hosts in every round.  The compact layout keeps, per
+// (row block, order), the first C sources of the block's R hosts:
+//   msk[block][order]          u16, the hosts (bits of the block) stored
+//   rec[block][order][r][C]    their partners, round-major, padded to whole
+//                              groups of kGroup rounds (16-byte multiples)
+// A block holds Binomial(R, 1/2) sources; the few beyond C (R=16, C=10: 0.16
+// hosts per block) are looked up by the route itself from the global matrix
+// and folded into the order's initial round keys, so nothing is dropped.
+constexpr int kGroup = 4;  // rounds per score task: 4*C u16 is a 16-byte multiple for C in {6, 10}
+
+struct RCompactArgs {
+  int64_t count;
+  int64_t count_pad;  // multiple of 8: row stride of msk / rec (16-byte aligned stage copies)
+  int64_t base;
+  int n;
+  int rounds;
+  int groups;         // ceil(rounds / kGroup)
+  int rec_u16;        // groups * kGroup * C
+  unsigned long long* err;
+  unsigned int* keys;  // [round][order]: set to max(zero key, overflow lookups)
+  unsigned int zero_key;
+  int aligned;
+};
+
+// One CTA per order: stage p, scatter pos; phase 1, one thread per row block:
+// the block's source mask, its first C sources' positions (shared memory) and
+// a list of the over-capacity sources; phase 2, their lookups in the global
+// matrix, one (host, round) per thread, then one thread per (block, group of
+// kGroup rounds): the stored sources' partners, 16-byte stores.
+template <typename P, typename T, int R, int C, bool kValidate>
+__global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, const P* __restrict__ perms,
+                                                              const T* __restrict__ gmat,
+                                                              uint16_t* __restrict__ rec, uint16_t* __restrict__ msk) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int okey[kMaxRounds];
+  const int n = a.n;
+  const int nblocks = n / R;
+  uint16_t* p = reinterpret_cast<uint16_t*>(smem);
+  uint16_t* pos = reinterpret_cast<uint16_t*>(smem + al16((size_t)n * 2));
+  uint16_t* cpos = reinterpret_cast<uint16_t*>(smem + 2 * al16((size_t)n * 2));  // [block][C]
+  uint32_t* ovf = reinterpret_cast<uint32_t*>(smem + 2 * al16((size_t)n * 2) + al16((size_t)nblocks * C * 2));
+  __shared__ unsigned int novf;
+  uint4* pos4 = reinterpret_cast<uint4*>(pos);
+  const uint4 none = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  for (int k = threadIdx.x; k < (n >> 3); k += blockDim.x) pos4[k] = none;
+  const uint32_t half = (uint32_t)n >> 1;
+  const uint32_t pmask = (uint32_t)n - 1;
+  const uint32_t jmask = pmask * 0x10001u;
+  const bool aligned = a.aligned != 0;
+  for (int64_t o = blockIdx.x; o < a.count; o += gridDim.x) {
+    __syncthreads();
+    bool bad = stage_order_vec<P>(perms + o * n, n, p, aligned);
+    if ((int)threadIdx.x < a.rounds) okey[threadIdx.x] = a.zero_key;
+    if (threadIdx.x == 0) novf = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) pos[p[i]] = (uint16_t)i;
+    __syncthreads();
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+      // source mask of the block's R hosts (a host no position names keeps
+      // the sentinel: the bijection check)
+      uint32_t m = 0;
+#pragma unroll
+      for (int c = 0; c < R / 8; ++c) {
+        const uint4 q = pos4[b * (R / 8) + c];
+        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
+        if ((q.x | q.y | q.z | q.w) & ~jmask) bad = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          m |= (uint32_t)((qs[k] & pmask) < half) << (c * 8 + 2 * k);
+          m |= (uint32_t)(((qs[k] >> 16) & pmask) < half) << (c * 8 + 2 * k + 1);
+        }
+      }
+      uint32_t mm = m, mc = 0;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        uint32_t j = 0;
+        if (mm) {
+          const int e = __ffs(mm) - 1;
+          mm &= mm - 1;
+          mc |= 1u << e;
+          j = pos[b * R + e] & pmask;
+        }
+        cpos[b * C + i] = (uint16_t)j;
+      }
+      msk[(size_t)b * a.count_pad + o] = (uint16_t)mc;
+      // sources beyond the record's capacity: listed (host, position) for
+      // the phase-2 lookups from the global matrix
+      while (mm) {
+        const int e = __ffs(mm) - 1;
+        mm &= mm - 1;
+        ovf[atomicAdd(&novf, 1u)] = ((uint32_t)(b * R + e) << 16) | (pos[b * R + e] & pmask);
+      }
+    }
+    __syncthreads();
+    // over-capacity lookups, one (host, round) per thread: the L2 latencies
+    // overlap instead of serialising on the few threads that found them
+    const int oitems = (int)novf * a.rounds;
+    for (int w = threadIdx.x; w < oitems; w += blockDim.x) {
+      const int k = w / a.rounds;
+      const int r = w - k * a.rounds;
+      const uint32_t e = ovf[k];
+      const T v = gmat[(size_t)(e >> 16) * n + p[(e & 0xFFFFu) + (1u << r)]];
+      atomicMax(&okey[r], KeyOf<T>::enc(v));
+    }
+    // one thread per (block, group of kGroup rounds): C positions, kGroup*C
+    // gathers, C*kGroup/8 16-byte stores.  Entries past the block's count
+    // gather from position 0 and padding rounds use shift 0 (always in range;
+    // the score never reads them).
+    const int gitems = nblocks * a.groups;
+    for (int w = threadIdx.x; w < gitems; w += blockDim.x) {
+      const int b = w / a.groups;
+      const int g = w - b * a.groups;
+      const uint32_t* c2 = reinterpret_cast<const uint32_t*>(cpos + b * C);
+      uint32_t jc2[C / 2];
+#pragma unroll
+      for (int k = 0; k < C / 2; ++k) jc2[k] = c2[k];
+      uint32_t outw[C * kGroup / 2];
+#pragma unroll
+      for (int k = 0; k < C * kGroup / 2; ++k) outw[k] = 0;
+#pragma unroll
+      for (int rr = 0; rr < kGroup; ++rr) {
+        const uint32_t sh = (1u << (g * kGroup + rr)) & pmask;
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const uint32_t j = (jc2[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+          const int idx = rr * C + i;
+          outw[idx >> 1] |= (uint32_t)p[j + sh] << ((idx & 1) * 16);
+        }
+      }
+      uint4* dst = reinterpret_cast<uint4*>(rec + ((size_t)b * a.count_pad + o) * a.rec_u16) + g * (C * kGroup / 8);
+#pragma unroll
+      for (int k = 0; k < C * kGroup / 8; ++k)
+        dst[k] = make_uint4(outw[4 * k], outw[4 * k + 1], outw[4 * k + 2], outw[4 * k + 3]);
+    }
+    __syncthreads();  // every reader of pos and okey is done
+    for (int k = threadIdx.x; k < (n >> 3); k += blockDim.x) pos4[k] = none;
+    if ((int)threadIdx.x < a.rounds) a.keys[(size_t)threadIdx.x * a.count + o] = okey[threadIdx.x];
+    if (kValidate && __syncthreads_or(bad) && threadIdx.x == 0) report_bad_order(a.err, n, a.base + o);
+  }
+}
+
+// 9 consumer warps + 1 producer: a stage of 96*k orders at 3 groups is a
+// whole number of tasks per consumer thread.
+constexpr int kCThreads = 320;
+
+struct RCompactScoreArgs {
+  int64_t count;
+  int64_t count_pad;
+  int n;
+  int rounds;
+  int groups;
+  int rec_u16;
+  int nblocks;
+  int stages;
+  int stage_orders;
+  unsigned int* keys;
+};
+
+template <typename T, int R, int C>
+__global__ void __launch_bounds__(kCThreads, 1) k_rounds_score_compact(RCompactScoreArgs a,
+                                                                       const uint16_t* __restrict__ rec,
+                                                                       const uint16_t* __restrict__ msk,
+                                                                       const T* __restrict__ gmat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  T* blk = reinterpret_cast<T*>(smem);
+  unsigned char* ring = smem + al16((size_t)R * n * sizeof(T));
+  __shared__ __align__(8) uint64_t full[kRMaxStages], empty[kRMaxStages], mat_bar;
+  unsigned mat_phase = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kConsumers = kCThreads - 32;
+  const bool producer = warp == (kCThreads >> 5) - 1;
+  const int so = a.stage_orders;
+  const size_t rec_bytes = (size_t)a.rec_u16 * 2;
+  const size_t stage_bytes = (size_t)so * rec_bytes + (size_t)so * 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
+    }
+    mbar_init(&mat_bar, 1);
+  }
+  __syncthreads();
+  const int64_t nstage = (a.count + so - 1) / so;
+  const int64_t units = nstage * a.nblocks;
+  const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+  uint32_t g = 0;
+  for (int64_t u = units * blockIdx.x / gridDim.x; u < u_end;) {
+    const int b = (int)(u / nstage);
+    const int64_t st0 = u - (int64_t)b * nstage;
+    const int64_t my_stages = min(nstage - st0, u_end - u);
+    u += my_stages;
+    __syncthreads();
+    stage_rows(blk, gmat + (size_t)b * R * n, (size_t)R * n * sizeof(T), &mat_bar, &mat_phase);
+    if (producer) {
+      if (lane == 0) {
+        for (int64_t i = 0; i < my_stages; ++i) {
+          const uint32_t gi = g + (uint32_t)i;
+          const int slot = (int)(gi % a.stages);
+          const uint32_t use = gi / a.stages;
+          if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1u);
+          const int64_t o0 = (st0 + i) * so;
+          const int cnt = (int)min((int64_t)so, a.count - o0);
+          const unsigned rb = (unsigned)(cnt * rec_bytes);
+          const unsigned mb = (unsigned)(((cnt + 7) & ~7) * 2);  // within count_pad
+          mbar_expect_tx(&full[slot], rb + mb);
+          unsigned char* dst = ring + slot * stage_bytes;
+          bulk_g2s(dst, rec + ((size_t)b * a.count_pad + o0) * a.rec_u16, rb, &full[slot]);
+          bulk_g2s(dst + (size_t)so * rec_bytes, msk + (size_t)b * a.count_pad + o0, mb, &full[slot]);
+        }
+      }
+    } else {
+      for (int64_t i = 0; i < my_stages; ++i) {
+        const uint32_t gi = g + (uint32_t)i;
+        const int slot = (int)(gi % a.stages);
+        mbar_wait(&full[slot], (gi / a.stages) & 1u);
+        const int64_t o0 = (st0 + i) * so;
+        const int cnt = (int)min((int64_t)so, a.count - o0);
+        const unsigned char* sp = ring + slot * stage_bytes;
+        const uint16_t* sm = reinterpret_cast<const uint16_t*>(sp + (size_t)so * rec_bytes);
+        const int tasks = cnt * a.groups;
+        const float inv_cnt = 1.0f / (float)cnt;
+        for (int t = threadIdx.x; t < tasks; t += kConsumers) {
+          int gr = (int)((float)t * inv_cnt);
+          int k = t - gr * cnt;
+          if (k < 0) {
+            --gr;
+            k += cnt;
+          } else if (k >= cnt) {
+            ++gr;
+            k -= cnt;
+          }
+          uint32_t m = sm[k];
+          const int cntm = __popc(m);
+          int hoff[C];
+#pragma unroll
+          for (int i = 0; i < C; ++i) {
+            const int e = m ? __ffs(m) - 1 : 0;
+            m &= m - 1;
+            hoff[i] = e * n;
+          }
+          const uint4* q4 = reinterpret_cast<const uint4*>(sp + (size_t)k * rec_bytes) + gr * (C * kGroup / 8);
+          uint32_t w[C * kGroup / 2];
+#pragma unroll
+          for (int c = 0; c < C * kGroup / 8; ++c) {
+            const uint4 q = q4[c];
+            w[4 * c] = q.x;
+            w[4 * c + 1] = q.y;
+            w[4 * c + 2] = q.z;
+            w[4 * c + 3] = q.w;
+          }
+          using K = typename KeyOf<T>::type;
+          const K zero = KeyOf<T>::enc(T(0));
+#pragma unroll
+          for (int rr = 0; rr < kGroup; ++rr) {
+            const int r = gr * kGroup + rr;
+            K key = zero;
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+              const int idx = rr * C + i;
+              const uint32_t col = (w[idx >> 1] >> ((idx & 1) * 16)) & 0xFFFFu;
+              if (i < cntm) {
+                const K v = KeyOf<T>::enc(blk[hoff[i] + col]);
+                key = v > key ? v : key;
+              }
+            }
+            if (r < a.rounds && key != zero) atomicMax(a.keys + (size_t)r * a.count + o0 + k, key);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+    }
+    g += (uint32_t)my_stages;
+  }
+}
+
 // --------------------------------------------------------------- finalize --
 struct RFinalArgs {
   int64_t count;
@@ -490,6 +770,120 @@ void launch_score_r(int R, const RScoreArgs& sa, int grid, size_t smem, const ui
   else launch_score<T, 8>(sa, grid, smem, buf, mat, st, all, paired);
 }
 
+template <typename T, int R, int C>
+void launch_compact_kernels(const RCompactArgs& ra, const RCompactScoreArgs& sa, bool validate, int perm_bytes,
+                            const char* perms, const T* mat, uint16_t* rec, uint16_t* msk, int rgrid, size_t route_smem,
+                            int sgrid, size_t score_smem, cudaStream_t st) {
+  auto route = validate ? (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, true>
+                                           : (void*)k_rounds_route_compact<int32_t, T, R, C, true>)
+                        : (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, false>
+                                           : (void*)k_rounds_route_compact<int32_t, T, R, C, false>);
+  RW_CUDA(cudaFuncSetAttribute(route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)route_smem));
+  RCompactArgs rac = ra;
+  void* rargs[] = {&rac, (void*)&perms, (void*)&mat, (void*)&rec, (void*)&msk};
+  RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), rargs, route_smem, st));
+  auto score = k_rounds_score_compact<T, R, C>;
+  RW_CUDA(cudaFuncSetAttribute(score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem));
+  score<<<sgrid, kCThreads, score_smem, st>>>(sa, rec, msk, mat);
+  RW_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_compact_r(int R, const RCompactArgs& ra, const RCompactScoreArgs& sa, bool validate, int perm_bytes,
+                      const char* perms, const void* mat, uint16_t* rec, uint16_t* msk, int rgrid, size_t route_smem,
+                      int sgrid, size_t score_smem, cudaStream_t st) {
+  const T* m = static_cast<const T*>(mat);
+  if (R == 16)
+    launch_compact_kernels<T, 16, 10>(ra, sa, validate, perm_bytes, perms, m, rec, msk, rgrid, route_smem, sgrid,
+                                      score_smem, st);
+  else
+    launch_compact_kernels<T, 8, 6>(ra, sa, validate, perm_bytes, perms, m, rec, msk, rgrid, route_smem, sgrid,
+                                    score_smem, st);
+}
+
+// Paper pairing through the compact layout (k_rounds_route_compact /
+// k_rounds_score_compact); 4-byte keys only (u16, FP32, FP64 ranks).
+bool launch_paper_compact(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
+                          double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot, int R, bool ranks,
+                          int sms, size_t budget) {
+  const int n = plan.n;
+  const int rounds = plan.rounds;
+  const int C = R == 16 ? 10 : 6;
+  const int groups = (rounds + kGroup - 1) / kGroup;
+  const int rec_u16 = groups * kGroup * C;
+  const size_t esz = ranks ? 4 : p.elem_bytes();
+  const int nblocks = n / R;
+  const size_t mat = al16((size_t)R * n * esz);
+  const size_t per_order = (size_t)rec_u16 * 2 + 2;
+  int so = (int)std::min<size_t>(512, (budget - mat) / (2 * per_order));
+  // whole tasks per consumer thread where the group count allows it
+  const int quantum = (groups == 3) ? 96 : 32;
+  so = so / quantum * quantum;
+  if (so < 32) return false;
+  const int stages = 2;
+  const size_t score_smem = mat + (size_t)stages * so * per_order;
+  const size_t route_smem = 2 * al16((size_t)n * 2) + al16((size_t)nblocks * C * 2) + (size_t)nblocks * (R - C) * 4;
+  const int64_t per_order_bytes = (int64_t)nblocks * (int64_t)per_order;
+  static const int64_t buf_override = [] {
+    const char* e = std::getenv("RW_TRANSPOSE_BUF_MB");
+    return e ? std::max(8L, std::atol(e)) << 20 : 0L;
+  }();
+  const int64_t buf_bytes =
+      buf_override ? buf_override : std::min<int64_t>(384ll << 20, std::max<int64_t>(48ll << 20, per_order_bytes * 16384));
+  const int64_t chunk = std::max<int64_t>(so, buf_bytes / per_order_bytes) & ~int64_t(7);
+  const int64_t kmax = std::min(batch, chunk);
+  const int64_t kpad = (kmax + 7) & ~int64_t(7);
+  ThreadCtx& c = thread_ctx(p.device);
+  const size_t rec_bytes_total = (size_t)nblocks * kpad * rec_u16 * 2;
+  uint16_t* rec = static_cast<uint16_t*>(c.scratch(slot, rec_bytes_total + (size_t)nblocks * kpad * 2 + 64));
+  uint16_t* msk = rec + rec_bytes_total / 2;
+  unsigned int* keys = static_cast<unsigned int*>(c.scratch(slot + 1, (size_t)rounds * kmax * 4));
+  unsigned int zero_key = 0;
+  if (p.storage == RW_STORAGE_F32) zero_key = 0x80000000u;
+  if (ranks) zero_key = p.zero_rank;
+  RFinalArgs fa{};
+  fa.rounds = rounds;
+  fa.mode = plan.mode;
+  fa.scale = p.scale;
+  for (int r = 0; r < rounds; ++r) fa.bytes[r] = plan.round_bytes[r];
+  for (int64_t off = 0; off < batch; off += kmax) {
+    const int64_t cnt_o = std::min(kmax, batch - off);
+    const int64_t cpad = (cnt_o + 7) & ~int64_t(7);
+    RCompactArgs ra{cnt_o, cpad, off, n, rounds, groups, rec_u16, reinterpret_cast<unsigned long long*>(err_slot),
+                    keys, zero_key, 0};
+    const char* perms = static_cast<const char*>(d_perms) + (size_t)off * n * perm_bytes;
+    ra.aligned = (reinterpret_cast<uintptr_t>(perms) & 15) == 0 ? 1 : 0;
+    const int rgrid = (int)std::min<int64_t>(cnt_o, (int64_t)sms * 8);
+    RCompactScoreArgs sa{cnt_o, cpad, n, rounds, groups, rec_u16, nblocks, stages, so, keys};
+    const int sgrid = (int)std::min<int64_t>(sms, nblocks * ((cnt_o + so - 1) / so));
+    switch (p.storage) {
+      case RW_STORAGE_U16:
+        launch_compact_r<uint16_t>(R, ra, sa, validate, perm_bytes, perms, p.d_mat, rec, msk, rgrid, route_smem, sgrid,
+                                   score_smem, st);
+        break;
+      case RW_STORAGE_F32:
+        launch_compact_r<float>(R, ra, sa, validate, perm_bytes, perms, p.d_mat, rec, msk, rgrid, route_smem, sgrid,
+                                score_smem, st);
+        break;
+      default:
+        launch_compact_r<uint32_t>(R, ra, sa, validate, perm_bytes, perms, p.d_rank, rec, msk, rgrid, route_smem,
+                                   sgrid, score_smem, st);
+        break;
+    }
+    fa.count = cnt_o;
+    const int fgrid = (int)((cnt_o + 127) / 128);
+    switch (p.storage) {
+      case RW_STORAGE_U16: k_rounds_finalize<uint16_t><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
+      case RW_STORAGE_F32: k_rounds_finalize<float><<<fgrid, 128, 0, st>>>(fa, keys, d_costs + off); break;
+      default:
+        k_rounds_finalize_ranks<<<fgrid, 128, 0, st>>>(fa, keys, p.d_rank_vals, d_costs + off);
+        break;
+    }
+    RW_CUDA(cudaGetLastError());
+  }
+  return true;
+}
+
 }  // namespace
 
 bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
@@ -529,6 +923,13 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   }
   if (!R) return false;
   const int nblocks = n / R;
+  static const bool compact_env = [] {
+    const char* e = std::getenv("RW_HD_COMPACT");
+    return !(e && e[0] == '0');
+  }();
+  if (compact_env && plan.pairing == RW_PAIRING_PAPER && esz <= 4 && (R == 16 || R == 8))
+    return launch_paper_compact(p, plan, d_perms, perm_bytes, batch, d_costs, validate, err_slot, st, slot, R, ranks,
+                                sms, budget);
   const size_t score_smem = al16((size_t)R * n * esz) + (size_t)stages * kRStageOrders * slots * R * 2;
   const size_t route_smem = 2 * al16((size_t)n * 2);
 

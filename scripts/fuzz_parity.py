@@ -27,7 +27,7 @@ def main():
     t0 = time.time()
     cases = fails = 0
     while time.time() - t0 < budget:
-        n = int(rng.choice([8, 16, 64, 128, 256, 512, 1024, 2048]))
+        n = int(rng.choice([8, 16, 64, 128, 256, 512, 1024, 2048, 4096]))
         kind = rng.choice(["u16", "f32", "f64"])
         sym = bool(rng.integers(0, 2))
         dirty = kind == "f64" and rng.random() < 0.3

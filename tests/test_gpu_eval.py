@@ -268,6 +268,43 @@ def test_hd_paths_agree(port, cfg, kind):
             assert np.array_equal(c.cpu().numpy(), want), (pairing, mode, "u16")
 
 
+@pytest.mark.parametrize("n,kind", [(4096, "u16"), (4096, "f32"), (4096, "f64"), (8192, "u16"), (2048, "f32")])
+def test_hd_paper_compact_layout(port, n, kind):
+    """Paper pairing through the compact transpose layout (per row block only
+    the first C sources' partners; the rest looked up by the route): equal to
+    the L2-gather path bit for bit on random orders and on orders that put
+    every source in the same row blocks (all of them over capacity), plus
+    a repeated host, which must still be reported."""
+    from paper_2105_14088_b200 import _lib
+    rng = np.random.default_rng(n + len(kind))
+    m = rng.integers(1, 60000, size=(n, n)).astype(np.float64)
+    if kind == "f32":
+        m = (m * 0.375 + rng.random((n, n))).astype(np.float32).astype(np.float64)
+    elif kind == "f64":
+        m = m + rng.random((n, n)) * 1e-3
+    storage = {"u16": _lib.RW_STORAGE_U16, "f32": _lib.RW_STORAGE_F32, "f64": _lib.RW_STORAGE_F64}[kind]
+    l2, tr = rw.Problem(m, storage), rw.Problem(m, storage)
+    assert tr.info["storage"] == storage
+    l2.set_path("l2")
+    tr.set_path("transpose")
+    half = n // 2
+    rand = [rng.permutation(n) for _ in range(40)]
+    lowfirst = [np.concatenate([rng.permutation(half), half + rng.permutation(half)]) for _ in range(20)]
+    highfirst = [np.concatenate([half + rng.permutation(half), rng.permutation(half)]) for _ in range(20)]
+    perms = np.array(rand + lowfirst + highfirst, dtype=np.int32)
+    for mode in (rw.CostMode.LatencyTimesSize, rw.CostMode.LatencyOnly):
+        spec = rw.CollectiveSpec(rw.Algorithm.HalvingDoubling, n, 1 << 20, 2, mode, rw.HdPairing.PaperFormula)
+        want = l2.evaluate_batch(spec, perms)
+        got = tr.evaluate_batch(spec, perms)
+        assert np.array_equal(got, want), (mode, np.nonzero(got != want)[0][:5])
+    ospec = make_spec(1, n, 1 << 20, 2, int(rw.CostMode.LatencyOnly), 0)
+    assert np.array_equal(got[[0, 40, 60]], port.evaluate_batch(m, perms[[0, 40, 60]], ospec))
+    bad = perms.copy()
+    bad[45, 7] = bad[45, 3000 % n]
+    with pytest.raises(rw.DomainError, match="batch entry 45"):
+        tr.evaluate_batch(spec, bad)
+
+
 def test_host_orders_narrowed_pipeline():
     """Large host batches (>= 4M positions) travel as uint16 narrowed on host
     threads: results equal the device path, and out-of-range int32 values
