@@ -416,51 +416,75 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
   const uint32_t pmask = (uint32_t)n - 1;
   const uint32_t jmask = pmask * 0x10001u;
   const bool aligned = a.aligned != 0;
+  // uint16 orders, 16-byte aligned, n <= 4096: the next order is loaded into
+  // registers during this order's gathers (its HBM latency hidden)
+  constexpr int kPF = 2;
+  const int nc8 = n >> 3;
+  const bool use_pf = sizeof(P) == 2 && aligned && nc8 <= kPF * (int)blockDim.x;
+  uint4 pf[kPF];
+  auto prefetch = [&](int64_t oo) {
+    const uint4* src = reinterpret_cast<const uint4*>(perms + oo * n);
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) {
+      const int c = threadIdx.x + k * blockDim.x;
+      if (c < nc8) pf[k] = __ldg(src + c);
+    }
+  };
+  if (use_pf && blockIdx.x < a.count) prefetch(blockIdx.x);
   for (int64_t o = blockIdx.x; o < a.count; o += gridDim.x) {
     __syncthreads();
-    bool bad = stage_order_vec<P>(perms + o * n, n, p, aligned);
+    bool bad = false;
+    if (use_pf) {
+      uint4* p4 = reinterpret_cast<uint4*>(p);
+#pragma unroll
+      for (int k = 0; k < kPF; ++k) {
+        const int c = threadIdx.x + k * blockDim.x;
+        if (c < nc8) {
+          const uint4 q = pf[k];
+          bad |= ((q.x | q.y | q.z | q.w) & ~jmask) != 0;
+          p4[c] = make_uint4(q.x & jmask, q.y & jmask, q.z & jmask, q.w & jmask);
+        }
+      }
+    } else {
+      bad = stage_order_vec<P>(perms + o * n, n, p, aligned);
+    }
     if ((int)threadIdx.x < a.rounds) okey[threadIdx.x] = a.zero_key;
     if (threadIdx.x == 0) novf = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) pos[p[i]] = (uint16_t)i;
     __syncthreads();
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
-      // source mask of the block's R hosts (a host no position names keeps
-      // the sentinel: the bijection check)
-      uint32_t m = 0;
+      // the block's sources (positions < N/2) in host order: the first C go
+      // to cpos (independent stores, no dependent re-reads of pos), the rest
+      // to the over-capacity list; a host no position names keeps the
+      // sentinel (the bijection check)
+      uint32_t mc = 0;
+      int i = 0;
 #pragma unroll
       for (int c = 0; c < R / 8; ++c) {
         const uint4 q = pos4[b * (R / 8) + c];
         const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
         if ((q.x | q.y | q.z | q.w) & ~jmask) bad = true;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          m |= (uint32_t)((qs[k] & pmask) < half) << (c * 8 + 2 * k);
-          m |= (uint32_t)(((qs[k] >> 16) & pmask) < half) << (c * 8 + 2 * k + 1);
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t j = (qs[k >> 1] >> ((k & 1) * 16)) & pmask;
+          const int e = c * 8 + k;
+          if (j < half) {
+            if (i < C) {
+              cpos[b * C + i] = (uint16_t)j;
+              mc |= 1u << e;
+            } else {
+              ovf[atomicAdd(&novf, 1u)] = ((uint32_t)(b * R + e) << 16) | j;
+            }
+            ++i;
+          }
         }
       }
-      uint32_t mm = m, mc = 0;
-#pragma unroll
-      for (int i = 0; i < C; ++i) {
-        uint32_t j = 0;
-        if (mm) {
-          const int e = __ffs(mm) - 1;
-          mm &= mm - 1;
-          mc |= 1u << e;
-          j = pos[b * R + e] & pmask;
-        }
-        cpos[b * C + i] = (uint16_t)j;
-      }
+      for (; i < C; ++i) cpos[b * C + i] = 0;
       msk[(size_t)b * a.count_pad + o] = (uint16_t)mc;
-      // sources beyond the record's capacity: listed (host, position) for
-      // the phase-2 lookups from the global matrix
-      while (mm) {
-        const int e = __ffs(mm) - 1;
-        mm &= mm - 1;
-        ovf[atomicAdd(&novf, 1u)] = ((uint32_t)(b * R + e) << 16) | (pos[b * R + e] & pmask);
-      }
     }
     __syncthreads();
+    if (use_pf && o + gridDim.x < a.count) prefetch(o + gridDim.x);
     // over-capacity lookups, one (host, round) per thread: the L2 latencies
     // overlap instead of serialising on the few threads that found them
     const int oitems = (int)novf * a.rounds;
