@@ -532,9 +532,12 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
   }
 }
 
-// 9 consumer warps + 1 producer: a stage of 96*k orders at 3 groups is a
-// whole number of tasks per consumer thread.
-constexpr int kCThreads = 320;
+// Consumer warps + 1 producer warp: with 3 round groups a stage of 192
+// (R=16) or 288 (R=8) orders is one task per consumer thread.
+template <int R>
+struct CompactThreads {
+  static constexpr int value = R == 16 ? 608 : 896;
+};
 
 struct RCompactScoreArgs {
   int64_t count;
@@ -549,7 +552,7 @@ struct RCompactScoreArgs {
   unsigned int* keys;
 };
 
-template <typename T, int R, int C>
+template <typename T, int R, int C, int kCThreads = CompactThreads<R>::value>
 __global__ void __launch_bounds__(kCThreads, 1) k_rounds_score_compact(RCompactScoreArgs a,
                                                                        const uint16_t* __restrict__ rec,
                                                                        const uint16_t* __restrict__ msk,
@@ -808,7 +811,7 @@ void launch_compact_kernels(const RCompactArgs& ra, const RCompactScoreArgs& sa,
   RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), rargs, route_smem, st));
   auto score = k_rounds_score_compact<T, R, C>;
   RW_CUDA(cudaFuncSetAttribute(score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem));
-  score<<<sgrid, kCThreads, score_smem, st>>>(sa, rec, msk, mat);
+  score<<<sgrid, CompactThreads<R>::value, score_smem, st>>>(sa, rec, msk, mat);
   RW_CUDA(cudaGetLastError());
 }
 
