@@ -806,6 +806,7 @@ void launch_compact_kernels(const RCompactArgs& ra, const RCompactScoreArgs& sa,
                         : (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, false>
                                            : (void*)k_rounds_route_compact<int32_t, T, R, C, false>);
   RW_CUDA(cudaFuncSetAttribute(route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)route_smem));
+  RW_CUDA(cudaFuncSetAttribute(route, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   RCompactArgs rac = ra;
   void* rargs[] = {&rac, (void*)&perms, (void*)&mat, (void*)&rec, (void*)&msk};
   RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), rargs, route_smem, st));
@@ -954,9 +955,11 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
     const char* e = std::getenv("RW_HD_COMPACT");
     return !(e && e[0] == '0');
   }();
-  if (compact_env && plan.pairing == RW_PAIRING_PAPER && esz <= 4 && (R == 16 || R == 8))
-    return launch_paper_compact(p, plan, d_perms, perm_bytes, batch, d_costs, validate, err_slot, st, slot, R, ranks,
-                                sms, budget);
+  // (a 32-row block takes the 16-row compact layout: its route has 64 blocks
+  // per order to spread over the CTA instead of 32)
+  if (compact_env && plan.pairing == RW_PAIRING_PAPER && esz <= 4 && (R == 32 || R == 16 || R == 8))
+    return launch_paper_compact(p, plan, d_perms, perm_bytes, batch, d_costs, validate, err_slot, st, slot,
+                                R == 32 ? 16 : R, ranks, sms, budget);
   const size_t score_smem = al16((size_t)R * n * esz) + (size_t)stages * kRStageOrders * slots * R * 2;
   const size_t route_smem = 2 * al16((size_t)n * 2);
 

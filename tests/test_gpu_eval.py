@@ -268,7 +268,8 @@ def test_hd_paths_agree(port, cfg, kind):
             assert np.array_equal(c.cpu().numpy(), want), (pairing, mode, "u16")
 
 
-@pytest.mark.parametrize("n,kind", [(4096, "u16"), (4096, "f32"), (4096, "f64"), (8192, "u16"), (2048, "f32")])
+@pytest.mark.parametrize("n,kind", [(4096, "u16"), (4096, "f32"), (4096, "f64"), (8192, "u16"), (2048, "f32"),
+                                    (2048, "u16"), (1024, "u16"), (1024, "f32"), (512, "u16")])
 def test_hd_paper_compact_layout(port, n, kind):
     """Paper pairing through the compact transpose layout (per row block only
     the first C sources' partners; the rest looked up by the route): equal to
