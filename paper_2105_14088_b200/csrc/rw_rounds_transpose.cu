@@ -364,18 +364,20 @@ __global__ void __launch_bounds__(kRThreads, 1) k_rounds_score(RScoreArgs a, con
   }
 }
 
-// ------------------------------------------------ paper pairing, compacted --
-// Paper pairing (the reference's default, cost_model.cpp:84-85): only the
-// hosts at positions < N/2 are sources, so the slot layout above stores a
-// sentinel for half the hosts in every round.  The compact layout keeps, per
-// (row block, order), the first C sources of the block's R hosts:
-//   msk[block][order]          u16, the hosts (bits of the block) stored
-//   rec[block][order][r][C]    their partners, round-major, padded to whole
-//                              groups of kGroup rounds (16-byte multiples)
-// A block holds Binomial(R, 1/2) sources; the few beyond C (R=16, C=10: 0.16
-// hosts per block) are looked up by the route itself from the global matrix
-// and folded into the order's initial round keys, so nothing is dropped.
-constexpr int kGroup = 4;  // rounds per score task: 4*C u16 is a 16-byte multiple for C in {6, 10}
+// ------------------------------------- source-compacted rounds (paper, BCube) --
+// Paper pairing (the reference's default, cost_model.cpp:84-85) and BCube
+// (cost_model.cpp:118-138) share one shape: in round r the sources are the
+// positions j < N/B (B = 2 for paper pairing) and source j meets the B-1
+// partners j + k*B^r, k = 1..B-1 (the reference's % n never fires).  The slot
+// layout above would store a sentinel for every non-source host in every
+// round.  The compact layout keeps, per (row block, order), the first C
+// sources of the block's R hosts:
+//   msk[block][order]                  u16, the hosts (bits of the block) stored
+//   rec[block][order][r][k-1][C]       their partners, round-major, padded to
+//                                      whole groups of GR rounds (16-byte multiples)
+// A block holds Binomial(R, 1/B) sources; the few beyond C (R=16, paper C=10:
+// 0.16 hosts per block) are looked up by the route itself from the global
+// matrix and folded into the order's initial round keys, so nothing is dropped.
 
 struct RCompactArgs {
   int64_t count;
@@ -383,8 +385,8 @@ struct RCompactArgs {
   int64_t base;
   int n;
   int rounds;
-  int groups;         // ceil(rounds / kGroup)
-  int rec_u16;        // groups * kGroup * C
+  int groups;         // ceil(rounds / GR)
+  int rec_u16;        // groups * GR * (B-1) * C
   unsigned long long* err;
   unsigned int* keys;  // [round][order]: set to max(zero key, overflow lookups)
   unsigned int zero_key;
@@ -394,9 +396,9 @@ struct RCompactArgs {
 // One CTA per order: stage p, scatter pos; phase 1, one thread per row block:
 // the block's source mask, its first C sources' positions (shared memory) and
 // a list of the over-capacity sources; phase 2, their lookups in the global
-// matrix, one (host, round) per thread, then one thread per (block, group of
-// kGroup rounds): the stored sources' partners, 16-byte stores.
-template <typename P, typename T, int R, int C, bool kValidate>
+// matrix, one (host, round, partner) per thread, then one thread per (block,
+// group of GR rounds): the stored sources' partners, 16-byte stores.
+template <typename P, typename T, int R, int C, int B, int GR, bool kValidate>
 __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, const P* __restrict__ perms,
                                                               const T* __restrict__ gmat,
                                                               uint16_t* __restrict__ rec, uint16_t* __restrict__ msk) {
@@ -412,7 +414,9 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
   uint4* pos4 = reinterpret_cast<uint4*>(pos);
   const uint4 none = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
   for (int k = threadIdx.x; k < (n >> 3); k += blockDim.x) pos4[k] = none;
-  const uint32_t half = (uint32_t)n >> 1;
+  constexpr int LB = B == 2 ? 1 : B == 4 ? 2 : 3;  // log2 B
+  constexpr int E = (B - 1) * C;                   // entries per round
+  const uint32_t nsrc = (uint32_t)n >> LB;
   const uint32_t pmask = (uint32_t)n - 1;
   const uint32_t jmask = pmask * 0x10001u;
   const bool aligned = a.aligned != 0;
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
     for (int i = threadIdx.x; i < n; i += blockDim.x) pos[p[i]] = (uint16_t)i;
     __syncthreads();
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
-      // the block's sources (positions < N/2) in host order: the first C go
+      // the block's sources (positions < N/B) in host order: the first C go
       // to cpos (independent stores, no dependent re-reads of pos), the rest
       // to the over-capacity list; a host no position names keeps the
       // sentinel (the bijection check)
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
         for (int k = 0; k < 8; ++k) {
           const uint32_t j = (qs[k >> 1] >> ((k & 1) * 16)) & pmask;
           const int e = c * 8 + k;
-          if (j < half) {
+          if (j < nsrc) {
             if (i < C) {
               cpos[b * C + i] = (uint16_t)j;
               mc |= 1u << e;
@@ -485,20 +489,23 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
     }
     __syncthreads();
     if (use_pf && o + gridDim.x < a.count) prefetch(o + gridDim.x);
-    // over-capacity lookups, one (host, round) per thread: the L2 latencies
-    // overlap instead of serialising on the few threads that found them
-    const int oitems = (int)novf * a.rounds;
+    // over-capacity lookups, one (host, round, partner) per thread: the L2
+    // latencies overlap instead of serialising on the threads that found them
+    const int per_host = a.rounds * (B - 1);
+    const int oitems = (int)novf * per_host;
     for (int w = threadIdx.x; w < oitems; w += blockDim.x) {
-      const int k = w / a.rounds;
-      const int r = w - k * a.rounds;
-      const uint32_t e = ovf[k];
-      const T v = gmat[(size_t)(e >> 16) * n + p[(e & 0xFFFFu) + (1u << r)]];
+      const int h = w / per_host;
+      const int rk = w - h * per_host;
+      const int r = rk / (B - 1);
+      const uint32_t k = (uint32_t)(rk - r * (B - 1)) + 1u;
+      const uint32_t e = ovf[h];
+      const T v = gmat[(size_t)(e >> 16) * n + p[(e & 0xFFFFu) + (k << (r * LB))]];
       atomicMax(&okey[r], KeyOf<T>::enc(v));
     }
-    // one thread per (block, group of kGroup rounds): C positions, kGroup*C
-    // gathers, C*kGroup/8 16-byte stores.  Entries past the block's count
-    // gather from position 0 and padding rounds use shift 0 (always in range;
-    // the score never reads them).
+    // one thread per (block, group of GR rounds): C positions, GR*E gathers,
+    // GR*E/8 16-byte stores.  Entries past the block's count gather from
+    // position 0 and padding rounds use offset 0 (always in range; the score
+    // never reads them).
     const int gitems = nblocks * a.groups;
     for (int w = threadIdx.x; w < gitems; w += blockDim.x) {
       const int b = w / a.groups;
@@ -507,22 +514,26 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
       uint32_t jc2[C / 2];
 #pragma unroll
       for (int k = 0; k < C / 2; ++k) jc2[k] = c2[k];
-      uint32_t outw[C * kGroup / 2];
+      uint32_t outw[GR * E / 2];
 #pragma unroll
-      for (int k = 0; k < C * kGroup / 2; ++k) outw[k] = 0;
+      for (int k = 0; k < GR * E / 2; ++k) outw[k] = 0;
 #pragma unroll
-      for (int rr = 0; rr < kGroup; ++rr) {
-        const uint32_t sh = (1u << (g * kGroup + rr)) & pmask;
+      for (int rr = 0; rr < GR; ++rr) {
+        const int r = g * GR + rr;
 #pragma unroll
-        for (int i = 0; i < C; ++i) {
-          const uint32_t j = (jc2[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
-          const int idx = rr * C + i;
-          outw[idx >> 1] |= (uint32_t)p[j + sh] << ((idx & 1) * 16);
+        for (int kk = 1; kk < B; ++kk) {
+          const uint32_t off = r < a.rounds ? (uint32_t)kk << (r * LB) : 0u;
+#pragma unroll
+          for (int i = 0; i < C; ++i) {
+            const uint32_t j = (jc2[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+            const int idx = rr * E + (kk - 1) * C + i;
+            outw[idx >> 1] |= (uint32_t)p[j + off] << ((idx & 1) * 16);
+          }
         }
       }
-      uint4* dst = reinterpret_cast<uint4*>(rec + ((size_t)b * a.count_pad + o) * a.rec_u16) + g * (C * kGroup / 8);
+      uint4* dst = reinterpret_cast<uint4*>(rec + ((size_t)b * a.count_pad + o) * a.rec_u16) + g * (GR * E / 8);
 #pragma unroll
-      for (int k = 0; k < C * kGroup / 8; ++k)
+      for (int k = 0; k < GR * E / 8; ++k)
         dst[k] = make_uint4(outw[4 * k], outw[4 * k + 1], outw[4 * k + 2], outw[4 * k + 3]);
     }
     __syncthreads();  // every reader of pos and okey is done
@@ -532,8 +543,8 @@ __global__ void __launch_bounds__(256) k_rounds_route_compact(RCompactArgs a, co
   }
 }
 
-// Consumer warps + 1 producer warp: with 3 round groups a stage of 192
-// (R=16) or 288 (R=8) orders is one task per consumer thread.
+// Consumer warps + 1 producer warp: with 3 round groups (paper pairing at
+// C5) a stage of 192 (R=16) or 288 (R=8) orders is one task per consumer thread.
 template <int R>
 struct CompactThreads {
   static constexpr int value = R == 16 ? 608 : 896;
@@ -552,12 +563,13 @@ struct RCompactScoreArgs {
   unsigned int* keys;
 };
 
-template <typename T, int R, int C, int kCThreads = CompactThreads<R>::value>
+template <typename T, int R, int C, int B, int GR, int kCThreads = CompactThreads<R>::value>
 __global__ void __launch_bounds__(kCThreads, 1) k_rounds_score_compact(RCompactScoreArgs a,
                                                                        const uint16_t* __restrict__ rec,
                                                                        const uint16_t* __restrict__ msk,
                                                                        const T* __restrict__ gmat) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int E = (B - 1) * C;  // entries per round
   const int n = a.n;
   T* blk = reinterpret_cast<T*>(smem);
   unsigned char* ring = smem + al16((size_t)R * n * sizeof(T));
@@ -635,10 +647,10 @@ __global__ void __launch_bounds__(kCThreads, 1) k_rounds_score_compact(RCompactS
             m &= m - 1;
             hoff[i] = e * n;
           }
-          const uint4* q4 = reinterpret_cast<const uint4*>(sp + (size_t)k * rec_bytes) + gr * (C * kGroup / 8);
-          uint32_t w[C * kGroup / 2];
+          const uint4* q4 = reinterpret_cast<const uint4*>(sp + (size_t)k * rec_bytes) + gr * (GR * E / 8);
+          uint32_t w[GR * E / 2];
 #pragma unroll
-          for (int c = 0; c < C * kGroup / 8; ++c) {
+          for (int c = 0; c < GR * E / 8; ++c) {
             const uint4 q = q4[c];
             w[4 * c] = q.x;
             w[4 * c + 1] = q.y;
@@ -648,12 +660,13 @@ __global__ void __launch_bounds__(kCThreads, 1) k_rounds_score_compact(RCompactS
           using K = typename KeyOf<T>::type;
           const K zero = KeyOf<T>::enc(T(0));
 #pragma unroll
-          for (int rr = 0; rr < kGroup; ++rr) {
-            const int r = gr * kGroup + rr;
+          for (int rr = 0; rr < GR; ++rr) {
+            const int r = gr * GR + rr;
             K key = zero;
 #pragma unroll
-            for (int i = 0; i < C; ++i) {
-              const int idx = rr * C + i;
+            for (int q = 0; q < E; ++q) {
+              const int i = q % C;
+              const int idx = rr * E + q;
               const uint32_t col = (w[idx >> 1] >> ((idx & 1) * 16)) & 0xFFFFu;
               if (i < cntm) {
                 const K v = KeyOf<T>::enc(blk[hoff[i] + col]);
@@ -797,48 +810,65 @@ void launch_score_r(int R, const RScoreArgs& sa, int grid, size_t smem, const ui
   else launch_score<T, 8>(sa, grid, smem, buf, mat, st, all, paired);
 }
 
-template <typename T, int R, int C>
+template <typename T, int R, int C, int B, int GR>
 void launch_compact_kernels(const RCompactArgs& ra, const RCompactScoreArgs& sa, bool validate, int perm_bytes,
                             const char* perms, const T* mat, uint16_t* rec, uint16_t* msk, int rgrid, size_t route_smem,
                             int sgrid, size_t score_smem, cudaStream_t st) {
-  auto route = validate ? (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, true>
-                                           : (void*)k_rounds_route_compact<int32_t, T, R, C, true>)
-                        : (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, false>
-                                           : (void*)k_rounds_route_compact<int32_t, T, R, C, false>);
+  auto route = validate ? (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, B, GR, true>
+                                           : (void*)k_rounds_route_compact<int32_t, T, R, C, B, GR, true>)
+                        : (perm_bytes == 2 ? (void*)k_rounds_route_compact<uint16_t, T, R, C, B, GR, false>
+                                           : (void*)k_rounds_route_compact<int32_t, T, R, C, B, GR, false>);
   RW_CUDA(cudaFuncSetAttribute(route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)route_smem));
   RW_CUDA(cudaFuncSetAttribute(route, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   RCompactArgs rac = ra;
   void* rargs[] = {&rac, (void*)&perms, (void*)&mat, (void*)&rec, (void*)&msk};
   RW_CUDA(cudaLaunchKernel(route, dim3(rgrid), dim3(256), rargs, route_smem, st));
-  auto score = k_rounds_score_compact<T, R, C>;
+  auto score = k_rounds_score_compact<T, R, C, B, GR>;
   RW_CUDA(cudaFuncSetAttribute(score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem));
   score<<<sgrid, CompactThreads<R>::value, score_smem, st>>>(sa, rec, msk, mat);
   RW_CUDA(cudaGetLastError());
 }
 
-template <typename T>
-void launch_compact_r(int R, const RCompactArgs& ra, const RCompactScoreArgs& sa, bool validate, int perm_bytes,
-                      const char* perms, const void* mat, uint16_t* rec, uint16_t* msk, int rgrid, size_t route_smem,
-                      int sgrid, size_t score_smem, cudaStream_t st) {
-  const T* m = static_cast<const T*>(mat);
-  if (R == 16)
-    launch_compact_kernels<T, 16, 10>(ra, sa, validate, perm_bytes, perms, m, rec, msk, rgrid, route_smem, sgrid,
-                                      score_smem, st);
-  else
-    launch_compact_kernels<T, 8, 6>(ra, sa, validate, perm_bytes, perms, m, rec, msk, rgrid, route_smem, sgrid,
-                                    score_smem, st);
+// Record shape per (R, B): capacity C of a block's Binomial(R, 1/B) sources
+// and GR rounds per score task, with GR*(B-1)*C a multiple of 8 (16 bytes).
+struct CompactShape {
+  int C, GR;
+};
+inline CompactShape compact_shape(int R, int B) {
+  if (R == 16) return B == 2 ? CompactShape{10, 4} : B == 4 ? CompactShape{8, 1} : CompactShape{4, 2};
+  return B == 2 ? CompactShape{6, 4} : CompactShape{4, 2};
 }
 
-// Paper pairing through the compact layout (k_rounds_route_compact /
-// k_rounds_score_compact); 4-byte keys only (u16, FP32, FP64 ranks).
+template <typename T>
+void launch_compact_r(int R, int B, const RCompactArgs& ra, const RCompactScoreArgs& sa, bool validate,
+                      int perm_bytes, const char* perms, const void* mat, uint16_t* rec, uint16_t* msk, int rgrid,
+                      size_t route_smem, int sgrid, size_t score_smem, cudaStream_t st) {
+  const T* m = static_cast<const T*>(mat);
+#define RW_COMPACT(RR, BB, CC, GG)                                                                                    \
+  if (R == RR && B == BB)                                                                                           \
+    return launch_compact_kernels<T, RR, CC, BB, GG>(ra, sa, validate, perm_bytes, perms, m, rec, msk, rgrid,        \
+                                                     route_smem, sgrid, score_smem, st);
+  RW_COMPACT(16, 2, 10, 4)
+  RW_COMPACT(16, 4, 8, 1)
+  RW_COMPACT(16, 8, 4, 2)
+  RW_COMPACT(8, 2, 6, 4)
+  RW_COMPACT(8, 4, 4, 2)
+  RW_COMPACT(8, 8, 4, 2)
+#undef RW_COMPACT
+}
+
+// Paper pairing (B = 2) and BCube (B = 4, 8) through the source-compacted
+// layout (k_rounds_route_compact / k_rounds_score_compact); 4-byte keys only
+// (u16, FP32, FP64 ranks).
 bool launch_paper_compact(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
-                          double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot, int R, bool ranks,
-                          int sms, size_t budget) {
+                          double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot, int R, int B,
+                          bool ranks, int sms, size_t budget) {
   const int n = plan.n;
   const int rounds = plan.rounds;
-  const int C = R == 16 ? 10 : 6;
-  const int groups = (rounds + kGroup - 1) / kGroup;
-  const int rec_u16 = groups * kGroup * C;
+  const CompactShape shape = compact_shape(R, B);
+  const int C = shape.C;
+  const int groups = (rounds + shape.GR - 1) / shape.GR;
+  const int rec_u16 = groups * shape.GR * (B - 1) * C;
   const size_t esz = ranks ? 4 : p.elem_bytes();
   const int nblocks = n / R;
   const size_t mat = al16((size_t)R * n * esz);
@@ -886,15 +916,15 @@ bool launch_paper_compact(const Problem& p, const EvalPlan& plan, const void* d_
     const int sgrid = (int)std::min<int64_t>(sms, nblocks * ((cnt_o + so - 1) / so));
     switch (p.storage) {
       case RW_STORAGE_U16:
-        launch_compact_r<uint16_t>(R, ra, sa, validate, perm_bytes, perms, p.d_mat, rec, msk, rgrid, route_smem, sgrid,
+        launch_compact_r<uint16_t>(R, B, ra, sa, validate, perm_bytes, perms, p.d_mat, rec, msk, rgrid, route_smem, sgrid,
                                    score_smem, st);
         break;
       case RW_STORAGE_F32:
-        launch_compact_r<float>(R, ra, sa, validate, perm_bytes, perms, p.d_mat, rec, msk, rgrid, route_smem, sgrid,
+        launch_compact_r<float>(R, B, ra, sa, validate, perm_bytes, perms, p.d_mat, rec, msk, rgrid, route_smem, sgrid,
                                 score_smem, st);
         break;
       default:
-        launch_compact_r<uint32_t>(R, ra, sa, validate, perm_bytes, perms, p.d_rank, rec, msk, rgrid, route_smem,
+        launch_compact_r<uint32_t>(R, B, ra, sa, validate, perm_bytes, perms, p.d_rank, rec, msk, rgrid, route_smem,
                                    sgrid, score_smem, st);
         break;
     }
@@ -917,12 +947,16 @@ bool launch_paper_compact(const Problem& p, const EvalPlan& plan, const void* d_
 bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void* d_perms, int perm_bytes, int64_t batch,
                              double* d_costs, bool validate, int* err_slot, cudaStream_t st, int slot) {
   const int n = plan.n;
-  if (plan.model != kHalvingDoubling || n < 512 || n > 16384 || (n & (n - 1)) != 0 || batch <= 0) return false;
+  // BCube (B = 2, 4, 8) takes the source-compacted layout only
+  const bool bcube = plan.model == kBCube;
+  if ((plan.model != kHalvingDoubling && !bcube) || n < 512 || n > 16384 || (n & (n - 1)) != 0 || batch <= 0)
+    return false;
+  if (bcube && plan.bcube_b != 2 && plan.bcube_b != 4 && plan.bcube_b != 8) return false;
   const int rounds = plan.rounds;
   if (rounds < 1 || rounds > 14) return false;
   // Symmetric matrix + xor pairing: one partner slot per host per round pair
   // (half the lookups and half the exchange buffer, see k_rounds_route).
-  const bool paired = plan.pairing == RW_PAIRING_XOR && p.symmetric && rounds >= 2;
+  const bool paired = !bcube && plan.pairing == RW_PAIRING_XOR && p.symmetric && rounds >= 2;
   const int slots = paired ? (rounds + 1) / 2 : rounds;
   int sms = 148, optin = 227 * 1024;
   RW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
@@ -957,9 +991,10 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   }();
   // (a 32-row block takes the 16-row compact layout: its route has 64 blocks
   // per order to spread over the CTA instead of 32)
-  if (compact_env && plan.pairing == RW_PAIRING_PAPER && esz <= 4 && (R == 32 || R == 16 || R == 8))
+  if ((bcube || (compact_env && plan.pairing == RW_PAIRING_PAPER)) && esz <= 4 && (R == 32 || R == 16 || R == 8))
     return launch_paper_compact(p, plan, d_perms, perm_bytes, batch, d_costs, validate, err_slot, st, slot,
-                                R == 32 ? 16 : R, ranks, sms, budget);
+                                R == 32 ? 16 : R, bcube ? plan.bcube_b : 2, ranks, sms, budget);
+  if (bcube) return false;  // FP64 matrices below N=2048: the gather kernels
   const size_t score_smem = al16((size_t)R * n * esz) + (size_t)stages * kRStageOrders * slots * R * 2;
   const size_t route_smem = 2 * al16((size_t)n * 2);
 

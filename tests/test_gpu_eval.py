@@ -306,6 +306,43 @@ def test_hd_paper_compact_layout(port, n, kind):
         tr.evaluate_batch(spec, bad)
 
 
+@pytest.mark.parametrize("n,b,kind", [(4096, 8, "u16"), (4096, 8, "f32"), (4096, 4, "u16"), (4096, 4, "f64"),
+                                      (512, 8, "u16"), (1024, 4, "f32"), (2048, 2, "u16"), (4096, 2, "f32")])
+def test_bcube_compact_layout(port, n, b, kind):
+    """BCube through the source-compacted transpose layout (sources j < N/B,
+    B-1 partners per round): equal to the L2-gather path bit for bit on random
+    orders and on orders that crowd every source into the same row blocks (all
+    over capacity), asymmetric matrices, both cost modes; a repeated host is
+    reported."""
+    from paper_2105_14088_b200 import _lib
+    rng = np.random.default_rng(n * b + len(kind))
+    m = rng.integers(1, 60000, size=(n, n)).astype(np.float64)
+    if kind == "f32":
+        m = (m * 0.375 + rng.random((n, n))).astype(np.float32).astype(np.float64)
+    elif kind == "f64":
+        m = m + rng.random((n, n)) * 1e-3
+    storage = {"u16": _lib.RW_STORAGE_U16, "f32": _lib.RW_STORAGE_F32, "f64": _lib.RW_STORAGE_F64}[kind]
+    l2, tr = rw.Problem(m, storage), rw.Problem(m, storage)
+    l2.set_path("l2")
+    tr.set_path("transpose")
+    ns = n // b
+    rand = [rng.permutation(n) for _ in range(40)]
+    low = [np.concatenate([rng.permutation(ns), ns + rng.permutation(n - ns)]) for _ in range(12)]
+    high = [np.concatenate([(n - ns) + rng.permutation(ns), rng.permutation(n - ns)]) for _ in range(12)]
+    perms = np.array(rand + low + high, dtype=np.int32)
+    for mode in (rw.CostMode.LatencyTimesSize, rw.CostMode.LatencyOnly):
+        spec = rw.CollectiveSpec(rw.Algorithm.BCube, n, 1 << 20, b, mode)
+        want = l2.evaluate_batch(spec, perms)
+        got = tr.evaluate_batch(spec, perms)
+        assert np.array_equal(got, want), (mode, np.nonzero(got != want)[0][:5])
+    ospec = make_spec(3, n, 1 << 20, b, int(rw.CostMode.LatencyOnly), 0)
+    assert np.array_equal(got[[0, 40, 52]], port.evaluate_batch(m, perms[[0, 40, 52]], ospec))
+    bad = perms.copy()
+    bad[41, 5] = bad[41, 9]
+    with pytest.raises(rw.DomainError, match="batch entry 41"):
+        tr.evaluate_batch(spec, bad)
+
+
 def test_host_orders_narrowed_pipeline():
     """Large host batches (>= 4M positions) travel as uint16 narrowed on host
     threads: results equal the device path, and out-of-range int32 values
