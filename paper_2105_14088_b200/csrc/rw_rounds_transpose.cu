@@ -19,6 +19,10 @@
 //             summed over rounds in order (halving_doubling_cost,
 //             proj/src/cost_model.cpp:71-92).
 //
+// Paper pairing and BCube take a source-compacted variant of route and score
+// (k_rounds_route_compact / k_rounds_score_compact, below): per row block and
+// order only the block's sources and their partners are written.
+//
 // Max is exact under any grouping, so the result is bit-identical to the
 // L2-gather kernel on every storage kind.
 #include <algorithm>
