@@ -158,15 +158,17 @@ rw_status rw_problem_destroy(rw_problem* p);
 rw_status rw_problem_get_info(const rw_problem* p, rw_problem_info* out);
 /* Kernel-path override for A/B measurements and tests, used when the matrix
  * exceeds one CTA's shared memory (results are identical on every path):
- *   RW_PATH_AUTO       default: the transpose path for ring up to N = 1536 and
- *                      for halving-doubling (512 <= N <= 16384, power of 2),
+ *   RW_PATH_AUTO       default: the transpose path for ring up to N = 1536, for
+ *                      halving-doubling (512 <= N <= 16384, power of 2) and for
+ *                      BCube with B = 2 or 4 (B = 8: FP64 matrices from N = 2048),
  *                      the L2-gather kernels otherwise
  *   RW_PATH_L2_GATHER  one warp per order, random gathers from the L2-resident matrix
  *   RW_PATH_CLUSTER    ring only: row-partitioned thread-block cluster, DSMEM hop
  *                      routing (u16 matrices, N = 64*C, C <= 16)
  *   RW_PATH_TRANSPOSE  two passes through an HBM exchange buffer (predecessor /
- *                      partner by host, grouped by matrix row block); lookups from
- *                      a shared-memory row block (ring: N % 8 == 0, 256 <= N <= 8192) */
+ *                      partner by host, grouped by matrix row block; paper pairing
+ *                      and BCube: only each block's sources); lookups from a
+ *                      shared-memory row block (ring: N % 8 == 0, 256 <= N <= 8192) */
 enum { RW_PATH_AUTO = 0, RW_PATH_L2_GATHER = 1, RW_PATH_CLUSTER = 2, RW_PATH_TRANSPOSE = 3 };
 rw_status rw_problem_set_path(rw_problem* p, int32_t path);
 
