@@ -923,7 +923,7 @@ void launch_typed(const Problem& p, const EvalPlan& plan, const void* d_perms_v,
     return;
   // BCube through the source-compacted transpose path (C5 evals/s, transpose
   // vs gathers: B=4 u16 1.72e7 vs 1.32e7, FP32 1.17e7 vs 8.6e6, FP64 1.38e7 vs
-  // 4.5e6; B=8 u16 a tie, FP32 5.9e6 vs 1.05e7, FP64 ranks 8.0e6 vs 5.8e6)
+  // 4.5e6; B=8 u16 a tie, FP32 9.2e6 vs 1.05e7, FP64 ranks 1.17e7 vs 5.8e6)
   const bool bcube_tr = plan.bcube_b != 8 || (p.storage == RW_STORAGE_F64 && n >= 2048);
   if (model == kBCube && !smem_mat && (p.path == RW_PATH_TRANSPOSE || (p.path == RW_PATH_AUTO && !few && bcube_tr)) &&
       launch_rounds_transpose(p, plan, d_perms, (int)sizeof(P), batch, d_costs, validate, err_slot, st, slot))

@@ -840,7 +840,7 @@ struct CompactShape {
 };
 inline CompactShape compact_shape(int R, int B) {
   if (R == 16) return B == 2 ? CompactShape{10, 4} : B == 4 ? CompactShape{8, 1} : CompactShape{4, 2};
-  return B == 2 ? CompactShape{6, 4} : CompactShape{4, 2};
+  return B == 2 ? CompactShape{6, 4} : B == 4 ? CompactShape{4, 2} : CompactShape{2, 4};
 }
 
 template <typename T>
@@ -857,7 +857,7 @@ void launch_compact_r(int R, int B, const RCompactArgs& ra, const RCompactScoreA
   RW_COMPACT(16, 8, 4, 2)
   RW_COMPACT(8, 2, 6, 4)
   RW_COMPACT(8, 4, 4, 2)
-  RW_COMPACT(8, 8, 4, 2)
+  RW_COMPACT(8, 8, 2, 4)
 #undef RW_COMPACT
 }
 
