@@ -637,6 +637,9 @@ def run_config_extras(rw, torch):
         "C5_hd_xor": ("C5", rw.CollectiveSpec(A.HalvingDoubling, 4096, S, 2, rw.CostMode.LatencyTimesSize,
                                               rw.HdPairing.XorPairing), 1 << 15),
         "C5_hd_paper": ("C5", rw.CollectiveSpec(A.HalvingDoubling, 4096, S), 1 << 15),
+        "C5_bcube4": ("C5", rw.CollectiveSpec(A.BCube, 4096, S, 4), 1 << 15),
+        "C5_bcube8": ("C5", rw.CollectiveSpec(A.BCube, 4096, S, 8), 1 << 15),
+        "C5_dbt": ("C5", rw.CollectiveSpec(A.DoubleBinaryTree, 4096, S), 1 << 15),
     }
     out = {"unit": "evals/s", "orders": "uint16, device resident", "reference_single_thread_container": ref_1t}
     for k, (cfg, spec, count) in rows.items():
