@@ -859,6 +859,7 @@ void launch_compact_r(int R, int B, const RCompactArgs& ra, const RCompactScoreA
   RW_COMPACT(8, 4, 4, 2)
   RW_COMPACT(8, 8, 2, 4)
 #undef RW_COMPACT
+  fail_internal("source-compacted transpose: no record shape for this row block / base");
 }
 
 // Paper pairing (B = 2) and BCube (B = 4, 8) through the source-compacted
