@@ -99,6 +99,7 @@ struct RRouteArgs {
   int aligned;      // order rows are 16-byte aligned
   int slots;        // partner slots per host: rounds, or ceil(rounds / 2) when paired
   int paired;       // symmetric matrix, xor pairing: one slot per round pair (below)
+  int prefetch;     // register prefetch of the next order (uint16, aligned, n <= 4096)
 };
 
 // Stages one order into shared memory as uint16 (vectorised when the row is
@@ -165,9 +166,39 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
   const int rshift = 31 - __clz(a.R);
   const int items = a.slots << cshift;
   const bool aligned = a.aligned != 0;
+  const uint32_t jm = (uint32_t)(n - 1) * 0x10001u;
+  // uint16 orders, 16-byte aligned, n <= 4096: the next order is loaded into
+  // registers during this order's gathers (RW_HD_ROUTE_PF=0 disables it)
+  constexpr int kPF = 2;
+  const int nc8 = n >> 3;
+  const bool use_pf = sizeof(P) == 2 && aligned && a.prefetch && nc8 <= kPF * (int)blockDim.x;
+  uint4 pf[kPF];
+  auto prefetch = [&](int64_t oo) {
+    const uint4* src = reinterpret_cast<const uint4*>(perms + oo * n);
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) {
+      const int c = threadIdx.x + k * blockDim.x;
+      if (c < nc8) pf[k] = __ldg(src + c);
+    }
+  };
+  if (use_pf && blockIdx.x < a.count) prefetch(blockIdx.x);
   for (int64_t o = blockIdx.x; o < a.count; o += gridDim.x) {
     __syncthreads();  // the previous order's readers of p / pos are done
-    bool bad = stage_order_vec<P>(perms + o * n, n, p, aligned);
+    bool bad = false;
+    if (use_pf) {
+      uint4* p4 = reinterpret_cast<uint4*>(p);
+#pragma unroll
+      for (int k = 0; k < kPF; ++k) {
+        const int c = threadIdx.x + k * blockDim.x;
+        if (c < nc8) {
+          const uint4 q = pf[k];
+          bad |= ((q.x | q.y | q.z | q.w) & ~jm) != 0;
+          p4[c] = make_uint4(q.x & jm, q.y & jm, q.z & jm, q.w & jm);
+        }
+      }
+    } else {
+      bad = stage_order_vec<P>(perms + o * n, n, p, aligned);
+    }
     if ((int)threadIdx.x < a.rounds) {
       if (a.key_bytes == 8)
         static_cast<unsigned long long*>(a.keys)[(size_t)threadIdx.x * a.count + o] = a.zero_key;
@@ -177,6 +208,7 @@ __global__ void __launch_bounds__(256) k_rounds_route(RRouteArgs a, const P* __r
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) pos[p[i]] = (uint16_t)i;
     __syncthreads();
+    if (use_pf && o + gridDim.x < a.count) prefetch(o + gridDim.x);
     const uint32_t jmask = (uint32_t)(n - 1) * 0x10001u;  // keeps sentinel positions in range
     for (int w = threadIdx.x; w < items; w += blockDim.x) {
       const int r = w >> cshift;  // round, or round pair when a.paired
@@ -1034,9 +1066,13 @@ bool launch_rounds_transpose(const Problem& p, const EvalPlan& plan, const void*
   for (int r = 0; r < rounds; ++r) fa.bytes[r] = plan.round_bytes[r];
   for (int64_t off = 0; off < batch; off += kmax) {
     const int64_t cnt_o = std::min(kmax, batch - off);
+    static const int route_pf = [] {
+      const char* e = std::getenv("RW_HD_ROUTE_PF");
+      return (e && e[0] == '0') ? 0 : 1;
+    }();
     RRouteArgs ra{cnt_o, off, n, rounds, plan.pairing == RW_PAIRING_XOR ? 1 : 0, R,
                   reinterpret_cast<unsigned long long*>(err_slot), keys, key_bytes, zero_key, 0, slots,
-                  paired ? 1 : 0};
+                  paired ? 1 : 0, route_pf};
     const int rgrid = (int)std::min<int64_t>(cnt_o, (int64_t)sms * 8);
     const char* perms = static_cast<const char*>(d_perms) + (size_t)off * n * perm_bytes;
     ra.aligned = (reinterpret_cast<uintptr_t>(perms) & 15) == 0 ? 1 : 0;
